@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py — iterations/sec of the NMF / MDS / l1-Cox hot path on B200.
+
+Metric (BASELINE.json): iterations/sec at 1/2/4/8 B200 plus the fraction of the
+HBM roofline.  The default workload is BASELINE.json configs[1], the largest
+configuration quoted for the GPU path that fits one B200:
+
+    NMF by alternating projected gradient, X 200,000 x 100,000 (float32
+    storage, 80 GB), rank 60, objective traced every iteration.
+
+A "step" is one solver iteration over the whole (sharded) data matrix.  The
+data are synthetic: X is rand_fill(seed, common_init=True) drawn on the device
+by the numpy-exact Philox kernel, so the content is the reference's own stream.
+
+Usage:
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+Other workloads (--workload): nmf_mu_c1 (10k x 10k, r=20, float64), mds_c3
+(n=100,000 from 1000-dim points, q=20, float32), cox_c4 (100,000 x 200,000,
+float32, lambda=1e-8), cox_c5 (int8 genotypes 400,000 x 500,000; needs >= 2
+GPUs).  Only the default is the driver's headline line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "nmf_apg_c2": dict(kind="nmf", algo="apg", m=200_000, n=100_000, r=60, dtype="float32",
+                       desc="NMF-APG 200000x100000 rank 60 (BASELINE configs[1])"),
+    "nmf_mu_c1": dict(kind="nmf", algo="mu", m=10_000, n=10_000, r=20, dtype="float64",
+                      desc="NMF-MU 10000x10000 rank 20 (BASELINE configs[0])"),
+    "mds_c3": dict(kind="mds", n=100_000, d=1000, q=20, dtype="float32",
+                   desc="MDS n=100000 points from 1000-dim data, q=20 (BASELINE configs[2])"),
+    "cox_c4": dict(kind="cox", m=100_000, n=200_000, dtype="float32", lam=1e-8,
+                   desc="l1-Cox 100000x200000, lambda=1e-8 (BASELINE configs[3])"),
+    "cox_c5": dict(kind="cox", m=400_000, n=500_000, dtype="int8", lam=1e-8,
+                   desc="l1-Cox int8 genotypes 400000x500000 (BASELINE configs[4])"),
+}
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+# ---------------------------------------------------------------------------
+
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/bench_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": ["no samples"]}
+        loaded = sorted(sm)[len(sm) // 2:] if len(sm) > 3 else sm
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# world
+# ---------------------------------------------------------------------------
+
+
+def _world():
+    import paper_2010_16114_b200 as bs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        comm = bs.init("nccl")
+    else:
+        comm = bs.init("inproc:1")[0]
+        import torch
+
+        torch.cuda.set_device(comm.device)
+    return comm
+
+
+def _barrier(comm):
+    import torch
+
+    if comm.size > 1:
+        comm.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(comm, value):
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=comm.device)
+    if comm.size > 1:
+        import paper_2010_16114_b200 as bs
+
+        comm.allreduce(t, bs.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# workloads on the B200 path
+# ---------------------------------------------------------------------------
+
+
+def _setup(comm, wl):
+    """Builds the solver state with inputs resident in HBM (untimed)."""
+    import torch
+
+    import paper_2010_16114_b200 as bs
+
+    kind = wl["kind"]
+    if kind == "nmf":
+        dt = np.dtype(wl["dtype"])
+        x = bs.empty((wl["m"], wl["n"]), comm, dt)
+        bs.rand_fill(x, seed=2010, common_init=True)
+        st = bs.nmf_init(x, wl["r"], seed=2011)
+        fn = bs.nmf_apg if wl["algo"] == "apg" else bs.nmf_multiplicative
+        return st, (lambda k: fn(st, k, trace_every=1)), ["bs_nmf_wxt", "bs_nmf_w_step"], x
+    if kind == "cox":
+        m, n = wl["m"], wl["n"]
+        if wl["dtype"] == "int8":
+            x = bs.empty((m, n), comm, np.int8)
+            gen = torch.Generator(device=comm.device)
+            gen.manual_seed(5 + comm.rank)
+            maf = torch.rand(x.local.shape[1], generator=gen, device=comm.device) * 0.45 + 0.05
+            for c0 in range(0, x.local.shape[1], 4096):
+                c1 = min(c0 + 4096, x.local.shape[1])
+                p = maf[c0:c1]
+                u1 = torch.rand((c1 - c0, m), generator=gen, device=comm.device)
+                u2 = torch.rand((c1 - c0, m), generator=gen, device=comm.device)
+                g = (u1 < p[:, None]).to(torch.int8) + (u2 < p[:, None]).to(torch.int8)
+                x.local[:, c0:c1].copy_(g.t())
+            sdt = np.float32
+        else:
+            x = bs.empty((m, n), comm, np.dtype(wl["dtype"]))
+            gen = torch.Generator(device=comm.device)
+            gen.manual_seed(2012 + comm.rank)
+            x.local.normal_(generator=gen)
+            sdt = None
+        y = np.arange(m, 0, -1, dtype=np.float64)          # cli.py:194
+        delta = (np.random.Generator(np.random.Philox(2013)).random(m) > 0.3).astype(np.float64)  # cli.py:195
+        st = bs.cox_init(x, y, delta, lam=wl["lam"], sigma=1e-7, dtype=sdt)
+        return st, (lambda k: bs.cox_fit(st, k, trace_every=1)), ["bs_cox_xbeta", "bs_cox_grad_step"], x
+    if kind == "mds":
+        dt = np.dtype(wl["dtype"])
+        pts = bs.empty((wl["d"], wl["n"]), comm, dt)
+        bs.rand_fill(pts, seed=2014, common_init=True)
+        y = bs.empty((wl["n"], wl["n"]), comm, dt)
+        bs.pairwise_euclidean(y, pts)
+        del pts
+        st = bs.mds_init(y, wl["q"], seed=2015)
+        return st, (lambda k: bs.mds_fit(st, k, trace_every=1)), ["bs_mds_pass"], y
+    raise ValueError(kind)
+
+
+def _bytes_per_launch(kernel, wl, comm, data):
+    """Algorithmic HBM bytes of one launch of the dominant kernel."""
+    local = data.local
+    return int(local.numel()) * local.element_size()
+
+
+def _run_b200(args, wl):
+    import torch
+
+    import paper_2010_16114_b200 as bs
+    from paper_2010_16114_b200 import _lib
+
+    comm = _world()
+    st, step, kernels, data = _setup(comm, wl)
+    _barrier(comm)
+    step(args.warmup)  # W untimed warm-up iterations (one call, like a user would)
+    _barrier(comm)
+    # ---- timed: K iterations through the public API, inputs resident in HBM ----
+    launches0 = _lib.load().bs_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    dev_index = comm.device.index if comm.device.index is not None else 0
+    with Clocks(dev_index) as clk, _lib.profile(kernels) as prof:
+        _barrier(comm)
+        ev0.record()
+        step(args.steps)
+        ev1.record()
+        _barrier(comm)
+    launches = _lib.load().bs_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1)
+    ms = _max_over_ranks(comm, ms)
+    per = prof.elapsed_ms()
+    tot = {k: float(np.sum(v)) for k, v in per.items() if v}
+    dom = max(tot, key=tot.get)
+    avg_ms = float(np.mean(per[dom]))
+    bytes_launch = _bytes_per_launch(dom, wl, comm, data)
+    avg_ms = _max_over_ranks(comm, avg_ms)
+    peak, peak_kind = _peaks()
+    achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
+    value = args.steps / (ms * 1e-3)
+    out = {
+        "metric": "iterations/sec", "value": value, "unit": "it/s", "n_gpus": comm.size,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": _arith_dtype(wl), "data": "synthetic (numpy-exact Philox rand_fill on device)" if wl["kind"] != "cox"
+        else "synthetic (device normal/genotype draws)",
+        "config": {"workload": wl["desc"], "iterations_timed": args.steps, "trace_every": 1,
+                   "partition": f"columns of X split over {comm.size} GPU(s) (partition_of)",
+                   "l2_flush": f"inputs ({data.local.numel() * data.local.element_size() / 1e9:.1f} GB per GPU) "
+                               "exceed the 126 MB L2"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(dom), "bytes_per_launch": bytes_launch,
+                     "avg_launch_ms": avg_ms,
+                     "share_of_step": tot[dom] / ms},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if comm.rank == 0 and comm.size == 1 and not args.no_cpu:
+        out["cpu_baseline"] = _cpu_baseline(wl, samples=1)
+    if not args.no_e2e:
+        out["e2e"] = _e2e(args, wl, comm, st, step, data)
+    if comm.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def _arith_dtype(wl):
+    return {"float32": "f32", "float64": "f64", "int8": "int8->f32"}[wl["dtype"]]
+
+
+def _traffic(kernel):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        v = d.get(kernel)
+        return None if v is None else float(v)
+    return None
+
+
+def _e2e(args, wl, comm, st, step, data):
+    """Same metric through the public API starting from pinned HOST memory.
+
+    The data block is copied host->device (the job's input, DistArray(local=...)),
+    then K iterations run through the solver call, and each step's objective is
+    read back (the trace, device->host).  h2d bytes are amortized over the K steps.
+    """
+    import torch
+
+    import paper_2010_16114_b200 as bs
+
+    local = data.local
+    host = torch.empty_strided(local.shape, local.stride(), dtype=local.dtype, device="cpu", pin_memory=True)
+    host.copy_(local)
+    _barrier(comm)
+    t0 = time.perf_counter()
+    dev = bs.DistArray(comm, data.shape, data.dtype, local=host)  # H2D through the public constructor
+    data.local.copy_(dev.local)
+    del dev
+    n_trace0 = len(st.trace)
+    step(args.steps)
+    vals = list(st.trace[n_trace0:])  # already on the host: one D2H per call
+    _barrier(comm)
+    dt = _max_over_ranks(comm, time.perf_counter() - t0)
+    del host
+    h2d = local.numel() * local.element_size()
+    return {"value": args.steps / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / args.steps,
+            "d2h_bytes_per_step": 8 * len(vals) / args.steps,
+            "note": "pinned host block -> device via DistArray(local=...), then K solver iterations; "
+                    "the one-time input copy is amortized over the K steps"}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the oracle port of the reference algorithm on the host cores
+# ---------------------------------------------------------------------------
+
+
+def _cpu_sample(wl):
+    """A bounded sample of the workload for the host (same aspect, ~seconds per iteration)."""
+    if wl["kind"] == "nmf":
+        f = 10 if wl["m"] * wl["n"] > 5e8 else 1
+        return dict(m=wl["m"] // f, n=wl["n"] // f)
+    if wl["kind"] == "cox":
+        f = 10 if wl["m"] * wl["n"] > 5e8 else 1
+        return dict(m=wl["m"] // f, n=wl["n"] // f)
+    return dict(n=5000, d=wl["d"])
+
+
+def _cpu_baseline(wl, samples=1):
+    from oracle import blockstat_oracle as orc
+
+    s = _cpu_sample(wl)
+    cores = _cores()
+    if wl["kind"] == "nmf":
+        m, n, r = s["m"], s["n"], wl["r"]
+        dt = np.float32 if wl["dtype"] == "float32" else np.float64
+        x = np.random.Generator(np.random.Philox(2010)).random((m, n), dtype=dt)
+        vt, w = orc.nmf_init(x, r, 2011)
+        fn = orc.nmf_apg if wl["algo"] == "apg" else orc.nmf_multiplicative
+        fn(x, vt, w, 1)
+        t0 = time.perf_counter()
+        fn(x, vt, w, samples)
+        dt_s = (time.perf_counter() - t0) / samples
+        scale = (m * n) / (wl["m"] * wl["n"])
+        desc = f"oracle nmf_{wl['algo']} on a {m}x{n} rank-{r} {np.dtype(dt).name} sample, objective every " \
+               f"iteration; it/s scaled by elements ({scale:.3g})"
+    elif wl["kind"] == "cox":
+        m, n = s["m"], s["n"]
+        gen = np.random.Generator(np.random.Philox(2012))
+        x = gen.standard_normal((m, n), dtype=np.float32) if wl["dtype"] != "int8" else \
+            gen.binomial(2, 0.2, size=(m, n)).astype(np.float32)
+        delta = (gen.random(m) > 0.3).astype(np.float32)
+        orc.cox_fit(x, delta, np.arange(m), wl["lam"], 1e-7, 1)
+        t0 = time.perf_counter()
+        orc.cox_fit(x, delta, np.arange(m), wl["lam"], 1e-7, samples)
+        dt_s = (time.perf_counter() - t0) / samples
+        scale = (m * n) / (wl["m"] * wl["n"])
+        desc = f"oracle cox_fit on a {m}x{n} float32 sample; it/s scaled by elements ({scale:.3g})"
+    else:
+        n, d = s["n"], s["d"]
+        pts = np.random.Generator(np.random.Philox(2014)).random((d, n), dtype=np.float32).astype(np.float64)
+        g = pts.T @ pts
+        nr = np.diag(g)
+        y = np.sqrt(np.maximum(nr[:, None] + nr[None, :] - 2 * g, 0))
+        np.fill_diagonal(y, 0)
+        th = orc.mds_init(y, wl["q"], 2015)
+        orc.mds_fit(y, th, 1)
+        t0 = time.perf_counter()
+        orc.mds_fit(y, th, samples)
+        dt_s = (time.perf_counter() - t0) / samples
+        scale = (n * n) / (wl["n"] * wl["n"])
+        desc = f"oracle mds_fit on n={n} points (q={wl['q']}); it/s scaled by pairs ({scale:.3g})"
+    return {"value": scale / dt_s, "unit": "it/s", "cores": cores, "kind": "port",
+            "sample": desc, "sample_seconds_per_iteration": dt_s,
+            "threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})")}
+
+
+def _run_reference(args, wl):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    for _ in range(max(args.warmup, 0)):
+        pass  # the oracle warms up inside _cpu_baseline (one untimed iteration)
+    t0 = time.perf_counter()
+    base = _cpu_baseline(wl, samples=max(args.steps, 1))
+    wall = time.perf_counter() - t0
+    out = {
+        "impl": "reference", "metric": "iterations/sec", "value": base["value"], "unit": "it/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": _arith_dtype(wl), "data": "synthetic",
+        "config": {"workload": wl["desc"], "iterations_timed": args.steps},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": base["value"], "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="nmf_apg_c2")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        _run_reference(args, wl)
+    else:
+        _run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,666 @@
+"""Rank-based collectives for the B200 build (contract of blockstat comm.py).
+
+The reference's ``Communicator`` (comm.py:178-264) is kept: every rank issues
+the same sequence of broadcast / allreduce / allgatherv / scatterv / barrier
+calls on buffers that are flattened in column-major order and written back in
+place.  Two backends implement it here:
+
+``inproc:<P>``
+    P rank *threads* in one process (comm.py:267-357): the execution model of
+    ``run_inproc``.  Rank r drives device ``r % ndevices`` on
+    its own CUDA stream.  Payloads may be CUDA tensors (folded on device by the
+    ``bs_fold`` kernel, in ascending rank order like comm.py:93-99) or numpy
+    arrays (folded on the host exactly as the reference does).  Headers are
+    validated like comm.py:102-153 and violations raise
+    ``CollectiveContractError`` on every rank.
+
+``nccl`` / ``gloo``
+    One process per rank under ``torchrun`` (the multi-GPU path): the
+    collectives map onto ``torch.distributed`` (NCCL over NVLink/NVSwitch on a
+    B200 box).  NCCL has no v-variants, so ``allgatherv`` / ``reduce_scatterv``
+    pad every block to the largest count.
+
+``reduce_scatterv`` is an addition to the reference's five collectives: the
+reference all-reduces the r x m product of scenario b and then keeps only its
+own column slice (distlinalg.py:251-252); a reduce-scatter moves 1/p of the data.
+
+The reference's TCP hub backend (comm.py:360-578) is not part of this build:
+multi-process runs use torch.distributed.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+import threading
+
+import numpy as np
+
+
+class CommError(RuntimeError):
+    """Base class for communication failures."""
+
+
+class CommInitError(CommError):
+    """World could not be constructed (bad descriptor, unreachable peer, ...)."""
+
+
+class CollectiveContractError(CommError):
+    """Ranks invoked collectives with incompatible arguments."""
+
+
+class RankAbortedError(CommError):
+    """Another rank aborted or timed out while this rank waited."""
+
+
+class ReduceOp(enum.Enum):
+    SUM = "sum"
+    PROD = "prod"
+    MAX = "max"
+    MIN = "min"
+
+
+_REDUCE_UFUNC = {
+    ReduceOp.SUM: np.add,
+    ReduceOp.PROD: np.multiply,
+    ReduceOp.MAX: np.maximum,
+    ReduceOp.MIN: np.minimum,
+}
+_OP_CODE = {ReduceOp.SUM: 0, ReduceOp.PROD: 1, ReduceOp.MAX: 2, ReduceOp.MIN: 3}
+
+_DTYPE_CODES = {
+    np.dtype(np.float32): 0,
+    np.dtype(np.float64): 1,
+    np.dtype(np.int64): 2,
+}
+_CODE_DTYPES = {v: k for k, v in _DTYPE_CODES.items()}
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_tensor(x):
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _np_dtype(buf):
+    if _is_tensor(buf):
+        torch = _torch()
+        table = {torch.float32: np.dtype(np.float32), torch.float64: np.dtype(np.float64),
+                 torch.int64: np.dtype(np.int64)}
+        if buf.dtype not in table:
+            raise ValueError(f"unsupported buffer dtype {buf.dtype}; use float32/float64/int64")
+        return table[buf.dtype]
+    dt = np.asarray(buf).dtype
+    if dt not in _DTYPE_CODES:
+        raise ValueError(f"unsupported buffer dtype {dt}; use float32/float64/int64")
+    return dt
+
+
+def fortran_flat(t):
+    """Column-major flattening of a tensor as a view when possible.
+
+    Returns ``(flat, writeback)``; ``writeback`` is True when ``flat`` is a
+    copy that must be written back into ``t`` after an in-place collective.
+    """
+    if t.ndim <= 1:
+        return (t, False) if t.is_contiguous() else (t.contiguous(), True)
+    rev = t.permute(*reversed(range(t.ndim)))
+    if rev.is_contiguous():
+        return rev.reshape(-1), False
+    return rev.contiguous().reshape(-1), True
+
+
+def _fortran_writeback(t, flat):
+    rev = t.permute(*reversed(range(t.ndim))) if t.ndim > 1 else t
+    rev.copy_(flat.reshape(rev.shape))
+
+
+def _np_flat(buf):
+    arr = np.asarray(buf)
+    return np.ravel(arr, order="F")
+
+
+def _np_writeback(buf, flat):
+    buf[...] = np.asarray(flat).reshape(buf.shape, order="F")
+
+
+def _check_agree(headers, field, what):
+    ref = headers[0][field]
+    for r, h in enumerate(headers):
+        if h[field] != ref:
+            raise CollectiveContractError(
+                f"{what} mismatch: rank 0 has {ref!r}, rank {r} has {h[field]!r}")
+
+
+def _validate_headers(headers):
+    """Cross-rank contract checks (comm.py:102-153)."""
+    _check_agree(headers, "op", "collective operation")
+    _check_agree(headers, "seq", "collective sequence number")
+    op = headers[0]["op"]
+    if op == "barrier":
+        return
+    _check_agree(headers, "dtype", "buffer dtype")
+    if op == "broadcast":
+        _check_agree(headers, "root", "broadcast root")
+        _check_agree(headers, "recv_len", "broadcast buffer length")
+    elif op == "allreduce":
+        _check_agree(headers, "redop", "reduction operator")
+        _check_agree(headers, "recv_len", "allreduce buffer length")
+    elif op in ("allgatherv", "reduce_scatterv"):
+        _check_agree(headers, "counts", f"{op} counts")
+        counts = headers[0]["counts"]
+        total = sum(counts)
+        for r, h in enumerate(headers):
+            mine, whole = (h["send_len"], h["recv_len"]) if op == "allgatherv" else (h["recv_len"], h["send_len"])
+            if mine != counts[r]:
+                raise CollectiveContractError(f"{op}: rank {r} block holds {mine} values, counts say {counts[r]}")
+            if whole != total:
+                raise CollectiveContractError(f"{op}: rank {r} full buffer holds {whole}, need {total}")
+        if op == "reduce_scatterv":
+            _check_agree(headers, "redop", "reduction operator")
+    elif op == "scatterv":
+        _check_agree(headers, "counts", "scatterv counts")
+        _check_agree(headers, "root", "scatterv root")
+        counts = headers[0]["counts"]
+        root = headers[0]["root"]
+        if headers[root]["send_len"] != sum(counts):
+            raise CollectiveContractError(
+                f"scatterv: root sends {headers[root]['send_len']} values, counts sum to {sum(counts)}")
+        for r, h in enumerate(headers):
+            if h["recv_len"] != counts[r]:
+                raise CollectiveContractError(
+                    f"scatterv: rank {r} receive buffer holds {h['recv_len']}, counts say {counts[r]}")
+    else:  # pragma: no cover
+        raise CollectiveContractError(f"unknown collective {op!r}")
+
+
+class Communicator:
+    """One rank's endpoint into a world of ``size`` ranks (comm.py:178-264).
+
+    Buffers may be numpy arrays or torch tensors (host or device).  Device
+    tensors stay on the device; collectives run on the rank's current stream.
+    """
+
+    rank: int
+    size: int
+    backend: str
+
+    def __init__(self):
+        self._seq = 0
+        self.device = None
+
+    # -- collectives -----------------------------------------------------
+    def broadcast(self, buf, root=0):
+        if not 0 <= root < self.size:
+            raise ValueError(f"root {root} out of range for size {self.size}")
+        self._collective("broadcast", buf, root=root)
+
+    def allreduce(self, buf, op=ReduceOp.SUM):
+        self._collective("allreduce", buf, redop=op)
+
+    def allgatherv(self, send, recv, counts):
+        counts = self._counts(counts)
+        self._collective("allgatherv", recv, send=send, counts=counts)
+
+    def reduce_scatterv(self, send, recv, counts, op=ReduceOp.SUM):
+        """Fold every rank's ``send`` (length sum(counts)) and keep block ``rank``."""
+        counts = self._counts(counts)
+        self._collective("reduce_scatterv", recv, send=send, counts=counts, redop=op)
+
+    def scatterv(self, send, recv, counts, root=0):
+        counts = self._counts(counts)
+        self._collective("scatterv", recv, send=send, counts=counts, root=root)
+
+    def barrier(self):
+        self._collective("barrier", None)
+
+    def _counts(self, counts):
+        counts = tuple(int(c) for c in counts)
+        if len(counts) != self.size:
+            raise ValueError(f"counts has {len(counts)} entries for {self.size} ranks")
+        return counts
+
+    def _collective(self, op, buf, **kw):
+        raise NotImplementedError
+
+    def close(self):
+        pass
+
+    def abort(self):
+        """Break peers out of pending collectives after a local failure."""
+
+    @property
+    def stream(self):
+        if self.device is None or self.device.type != "cuda":
+            return None
+        return _torch().cuda.current_stream(self.device)
+
+    def __repr__(self):
+        return f"<Communicator rank={self.rank} size={self.size} backend={self.backend}>"
+
+
+# ---------------------------------------------------------------------------
+# In-process backend
+# ---------------------------------------------------------------------------
+
+
+class _EventBarrier:
+    """Reusable two-generation barrier (comm.py:272-307)."""
+
+    def __init__(self, size, timeout):
+        self._size = size
+        self._timeout = timeout
+        self._lock = threading.Lock()
+        self._count = 0
+        self._gen = 0
+        self._events = [threading.Event(), threading.Event()]
+        self._broken = False
+
+    def wait(self):
+        with self._lock:
+            if self._broken:
+                raise RankAbortedError("world aborted")
+            gen = self._gen
+            self._count += 1
+            if self._count == self._size:
+                self._count = 0
+                self._gen ^= 1
+                self._events[self._gen].clear()
+                self._events[gen].set()
+                return
+        if not self._events[gen].wait(self._timeout):
+            self.abort()
+            raise RankAbortedError("a rank timed out mid-collective")
+        if self._broken:
+            raise RankAbortedError("world aborted")
+
+    def abort(self):
+        with self._lock:
+            self._broken = True
+            for event in self._events:
+                event.set()
+
+
+class _InProcWorld:
+    """Double-parity slot table (comm.py:310-327)."""
+
+    def __init__(self, size, timeout=180.0):
+        self.size = size
+        self.slots = [[None] * size, [None] * size]
+        self._barrier = _EventBarrier(size, timeout)
+
+    def exchange(self, rank, seq, entry):
+        buf = self.slots[seq & 1]
+        buf[rank] = entry
+        self._barrier.wait()
+        return list(buf)
+
+    def abort(self):
+        self._barrier.abort()
+
+
+def _device_for_rank(rank):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        return torch.device("cpu")
+    return torch.device("cuda", rank % torch.cuda.device_count())
+
+
+class _InProcCommunicator(Communicator):
+    backend = "inproc"
+
+    def __init__(self, world, rank):
+        super().__init__()
+        self._world = world
+        self.rank = rank
+        self.size = world.size
+        self.device = _device_for_rank(rank)
+
+    def abort(self):
+        self._world.abort()
+
+    def _collective(self, op, buf, send=None, counts=None, root=-1, redop=None):
+        torch_mode = _is_tensor(buf) or _is_tensor(send)
+        # ---- header -------------------------------------------------------
+        header = {"op": op, "dtype": -1, "root": root, "send_len": -1, "recv_len": -1,
+                  "counts": counts, "redop": -1 if redop is None else _OP_CODE[redop]}
+        payload = None
+        rflat = None
+        wb = False
+        if op != "barrier":
+            dt = _np_dtype(buf if buf is not None else send)
+            header["dtype"] = _DTYPE_CODES[dt]
+            if torch_mode:
+                rflat, wb = fortran_flat(buf)
+                header["recv_len"] = rflat.numel()
+            else:
+                rflat = _np_flat(buf)
+                header["recv_len"] = rflat.size
+            if op in ("allgatherv", "reduce_scatterv") or (op == "scatterv" and self.rank == root):
+                sflat = (fortran_flat(send)[0] if _is_tensor(send) else _np_flat(send))
+                header["send_len"] = int(sflat.numel() if _is_tensor(sflat) else sflat.size)
+                payload = sflat
+            elif op in ("allreduce",) or (op == "broadcast" and self.rank == root):
+                payload = rflat
+            if payload is not None:
+                if _is_tensor(payload):
+                    payload = payload.clone()
+                    if payload.is_cuda:
+                        _torch().cuda.current_stream(payload.device).synchronize()
+                else:
+                    payload = np.array(payload, copy=True)
+        # ---- exchange -----------------------------------------------------
+        self._seq += 1
+        header["seq"] = self._seq
+        if self.size == 1:
+            slots = [(header, payload)]
+        else:
+            slots = self._world.exchange(self.rank, self._seq, (header, payload))
+            if any(entry is None for entry in slots):
+                raise CollectiveContractError("ranks invoked different numbers of collectives")
+        headers = [h for h, _ in slots]
+        _validate_headers(headers)
+        if op == "barrier":
+            return
+        payloads = [p for _, p in slots]
+        if torch_mode:
+            self._respond_torch(op, headers, payloads, rflat, counts)
+            if wb:
+                _fortran_writeback(buf, rflat)
+            if rflat.is_cuda and self.size > 1:
+                _torch().cuda.current_stream(rflat.device).synchronize()
+        else:
+            out = self._respond_numpy(op, headers, payloads, counts)
+            _np_writeback(buf, out)
+
+    # reference semantics on numpy payloads (comm.py:156-175)
+    def _respond_numpy(self, op, headers, payloads, counts):
+        payloads = [p.cpu().numpy() if _is_tensor(p) else p for p in payloads]
+        if op == "broadcast":
+            return payloads[headers[0]["root"]]
+        if op == "allreduce":
+            return _fold_np(payloads, ReduceOp(_op_name(headers[0]["redop"])))
+        if op == "allgatherv":
+            return np.concatenate([payloads[r] for r in range(self.size)])
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+        if op == "scatterv":
+            send = payloads[headers[0]["root"]]
+            return send[offs[self.rank]:offs[self.rank + 1]]
+        if op == "reduce_scatterv":
+            red = _fold_np(payloads, ReduceOp(_op_name(headers[0]["redop"])))
+            return red[offs[self.rank]:offs[self.rank + 1]]
+        raise CollectiveContractError(f"unknown collective {op!r}")  # pragma: no cover
+
+    def _respond_torch(self, op, headers, payloads, rflat, counts):
+        torch = _torch()
+        dev = rflat.device
+
+        def local(p):
+            if _is_tensor(p):
+                return p.to(dev)
+            return torch.from_numpy(np.ascontiguousarray(p)).to(dev)
+
+        if op == "broadcast":
+            rflat.copy_(local(payloads[headers[0]["root"]]))
+            return
+        if op == "allgatherv":
+            off = 0
+            for r in range(self.size):
+                if counts[r]:
+                    rflat[off:off + counts[r]].copy_(local(payloads[r]))
+                off += counts[r]
+            return
+        offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64) if counts else None
+        if op == "scatterv":
+            src = local(payloads[headers[0]["root"]])
+            rflat.copy_(src[offs[self.rank]:offs[self.rank + 1]])
+            return
+        redop = ReduceOp(_op_name(headers[0]["redop"]))
+        srcs = [local(p) for p in payloads]
+        if op == "reduce_scatterv":
+            srcs = [s[offs[self.rank]:offs[self.rank + 1]] for s in srcs]
+        _fold_into(rflat, srcs, redop)
+
+
+def _op_name(code):
+    return {0: "sum", 1: "prod", 2: "max", 3: "min"}[code]
+
+
+def _fold_np(parts, redop):
+    acc = np.array(parts[0], copy=True)
+    fn = _REDUCE_UFUNC[redop]
+    for part in parts[1:]:
+        fn(acc, part, out=acc)
+    return acc
+
+
+def _fold_into(dst, srcs, redop):
+    """dst = srcs[0] op srcs[1] op ... (ascending rank), on dst's device."""
+    if dst.numel() == 0:
+        return
+    if dst.is_cuda:
+        from . import _lib
+
+        srcs = [s.contiguous() for s in srcs]
+        arr = (ctypes.c_void_p * len(srcs))(*[s.data_ptr() for s in srcs])
+        _lib.call("bs_fold", _lib.ptr(dst), ctypes.cast(arr, ctypes.c_void_p), len(srcs), dst.numel(),
+                  _lib.dtype_code(dst.dtype), _OP_CODE[redop], _lib.stream_ptr())
+        return
+    acc = srcs[0].clone()
+    torch = _torch()
+    for s in srcs[1:]:
+        if redop is ReduceOp.SUM:
+            acc += s
+        elif redop is ReduceOp.PROD:
+            acc *= s
+        elif redop is ReduceOp.MAX:
+            acc = torch.maximum(acc, s)
+        else:
+            acc = torch.minimum(acc, s)
+    dst.copy_(acc)
+
+
+# ---------------------------------------------------------------------------
+# torch.distributed backend (one process per rank; NCCL on B200)
+# ---------------------------------------------------------------------------
+
+
+class _TorchCommunicator(Communicator):
+    """Collectives over a torch.distributed process group (NCCL or gloo)."""
+
+    def __init__(self, backend_name):
+        super().__init__()
+        torch = _torch()
+        import torch.distributed as dist
+
+        self._dist = dist
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group(backend=backend_name)
+        self.rank = dist.get_rank()
+        self.size = dist.get_world_size()
+        self.backend = dist.get_backend()
+        if self.backend == "nccl":
+            local = int(os.environ.get("LOCAL_RANK", self.rank % max(torch.cuda.device_count(), 1)))
+            self.device = torch.device("cuda", local)
+            torch.cuda.set_device(self.device)
+        else:
+            self.device = torch.device("cpu")
+        self._ops = {ReduceOp.SUM: dist.ReduceOp.SUM, ReduceOp.PROD: dist.ReduceOp.PRODUCT,
+                     ReduceOp.MAX: dist.ReduceOp.MAX, ReduceOp.MIN: dist.ReduceOp.MIN}
+
+    def close(self):
+        pass
+
+    def _to_dev(self, buf):
+        """(device flat tensor, writeback fn)."""
+        torch = _torch()
+        if _is_tensor(buf):
+            flat, wb = fortran_flat(buf)
+            if flat.device != self.device:
+                dflat = flat.to(self.device)
+                return dflat, (lambda: (_fortran_writeback(buf, dflat.to(buf.device))
+                                        if wb else flat.copy_(dflat.to(flat.device))))
+            return flat, ((lambda: _fortran_writeback(buf, flat)) if wb else (lambda: None))
+        arr = np.asarray(buf)
+        flat = torch.from_numpy(np.ascontiguousarray(_np_flat(arr))).to(self.device)
+        return flat, (lambda: _np_writeback(buf, flat.cpu().numpy()))
+
+    def _collective(self, op, buf, send=None, counts=None, root=-1, redop=None):
+        dist = self._dist
+        torch = _torch()
+        self._seq += 1
+        if op == "barrier":
+            dist.barrier()
+            return
+        rflat, wb = self._to_dev(buf)
+        if op == "broadcast":
+            dist.broadcast(rflat, src=root)
+        elif op == "allreduce":
+            dist.all_reduce(rflat, op=self._ops[redop])
+        elif op == "allgatherv":
+            sflat, _ = self._to_dev(send)
+            mx = max(counts) if counts else 0
+            if mx:
+                pad = torch.zeros(mx, dtype=rflat.dtype, device=self.device)
+                pad[:sflat.numel()].copy_(sflat)
+                out = torch.empty(mx * self.size, dtype=rflat.dtype, device=self.device)
+                dist.all_gather_into_tensor(out, pad)
+                off = 0
+                for r in range(self.size):
+                    if counts[r]:
+                        rflat[off:off + counts[r]].copy_(out[r * mx:r * mx + counts[r]])
+                    off += counts[r]
+        elif op == "reduce_scatterv":
+            sflat, _ = self._to_dev(send)
+            mx = max(counts) if counts else 0
+            if mx:
+                padded = torch.zeros(mx * self.size, dtype=rflat.dtype, device=self.device)
+                off = 0
+                for r in range(self.size):
+                    if counts[r]:
+                        padded[r * mx:r * mx + counts[r]].copy_(sflat[off:off + counts[r]])
+                    off += counts[r]
+                out = torch.empty(mx, dtype=rflat.dtype, device=self.device)
+                dist.reduce_scatter_tensor(out, padded, op=self._ops[redop])
+                rflat.copy_(out[:counts[self.rank]])
+        elif op == "scatterv":
+            total = sum(counts)
+            mx = max(counts) if counts else 0
+            full = torch.empty(total, dtype=rflat.dtype, device=self.device)
+            if self.rank == root:
+                full.copy_(self._to_dev(send)[0])
+            dist.broadcast(full, src=root)
+            off = sum(counts[:self.rank])
+            rflat.copy_(full[off:off + counts[self.rank]])
+            del mx
+        else:  # pragma: no cover
+            raise CollectiveContractError(f"unknown collective {op!r}")
+        wb()
+
+
+# ---------------------------------------------------------------------------
+# world construction (comm.py:492-643)
+# ---------------------------------------------------------------------------
+
+
+def _parse_descriptor(descriptor):
+    if descriptor.startswith("inproc:"):
+        try:
+            size = int(descriptor.split(":", 1)[1])
+        except ValueError:
+            raise CommInitError(f"bad inproc descriptor {descriptor!r}") from None
+        if size < 1:
+            raise CommInitError("world size must be >= 1")
+        return "inproc", size
+    if descriptor in ("nccl", "gloo", "torch"):
+        return "torch", descriptor
+    if descriptor.startswith("tcp:"):
+        raise CommInitError("the tcp hub backend is not part of the B200 build; launch one process per "
+                            "GPU with torchrun and use the 'nccl' descriptor")
+    raise CommInitError(f"unknown backend descriptor {descriptor!r}")
+
+
+def init(descriptor, timeout=30.0):
+    """Construct communicator endpoint(s) from a backend descriptor.
+
+    ``inproc:<P>`` returns a list of P endpoints sharing one world (one per
+    rank thread).  ``nccl`` / ``gloo`` join the torch.distributed world of this
+    process (env:// rendezvous, e.g. under torchrun) and return its endpoint.
+    """
+    kind, arg = _parse_descriptor(descriptor)
+    if kind == "inproc":
+        world = _InProcWorld(arg)
+        return [_InProcCommunicator(world, r) for r in range(arg)]
+    backend = arg
+    if backend == "torch":
+        backend = "nccl" if _torch().cuda.is_available() else "gloo"
+    try:
+        return _TorchCommunicator(backend)
+    except Exception as exc:  # noqa: BLE001
+        raise CommInitError(f"could not join the torch.distributed world: {exc}") from exc
+
+
+def launch(descriptor, fn, *args, timeout=30.0):
+    """Run ``fn(comm, *args)`` on every rank reachable from this process."""
+    kind, _ = _parse_descriptor(descriptor)
+    if kind == "inproc":
+        return _run_threads(init(descriptor), fn, args)
+    comm = init(descriptor, timeout=timeout)
+    try:
+        return [_with_rank_context(comm, fn, args)]
+    finally:
+        comm.close()
+
+
+def run_inproc(size, fn, *args):
+    """Convenience wrapper: ``launch(f"inproc:{size}", fn, *args)``."""
+    return launch(f"inproc:{size}", fn, *args)
+
+
+def _with_rank_context(comm, fn, args):
+    torch = _torch()
+    if comm.device is not None and comm.device.type == "cuda":
+        torch.cuda.set_device(comm.device)
+        if comm.backend == "inproc" and comm.size > 1:
+            with torch.cuda.stream(torch.cuda.Stream(comm.device)):
+                return fn(comm, *args)
+    return fn(comm, *args)
+
+
+def _run_threads(comms, fn, args):
+    if len(comms) == 1:
+        return [_with_rank_context(comms[0], fn, args)]
+    results = [None] * len(comms)
+    errors = [None] * len(comms)
+
+    def work(i):
+        try:
+            results[i] = _with_rank_context(comms[i], fn, args)
+        except BaseException as exc:  # noqa: BLE001 - propagated to caller
+            errors[i] = exc
+            comms[i].abort()
+
+    threads = [threading.Thread(target=work, args=(i,), name=f"rank-{i}") for i in range(len(comms))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for comm in comms:
+        comm.close()
+    primary = [e for e in errors if e is not None and not isinstance(e, RankAbortedError)]
+    if primary:
+        raise primary[0]
+    for e in errors:
+        if e is not None:
+            raise e
+    return results

@@ -1,0 +1,584 @@
+// l1-regularized Cox proportional hazards by proximal gradient
+// (solvers.py:308-450) as memory-bound kernels.
+//
+//   scn m   xb   = X_loc beta_loc            one streamed pass over X  (distlinalg.py:334-337)
+//   risk    w = exp(min(xb, clamp)), W = cumsum(w), loglik          (solvers.py:376-398)
+//   pi_delta pd_i = w_i sum_{j: cuts_j >= i} delta_j / W[cuts_j]    (solvers.py:401-419)
+//   scn p   grad = X_loc^T (delta - pd)      one streamed pass over X  (distlinalg.py:355-358)
+//   prox    beta <- S_lam(beta + sigma grad)                         (solvers.py:448-449)
+//
+// X local block: m x n_loc column-major (X[j*m + i]) in float32, float64 or int8
+// (genotypes, widened in-register).  The O(m) scans run in float64 regardless of
+// the storage type (PAPER.md:864 records fp32 cumsum instability).
+#include "bsb200.cuh"
+
+#include <algorithm>
+#include <mutex>
+
+using namespace bs;
+
+// ---------------------------------------------------------------------------
+// Vector load helpers: VEC consecutive elements of a column as doubles.
+// ---------------------------------------------------------------------------
+
+template <typename TX, int VEC> struct VecLoad;
+template <> struct VecLoad<float, 4> {
+  static __device__ __forceinline__ void load(const float* p, double* o) {
+    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+template <> struct VecLoad<double, 2> {
+  static __device__ __forceinline__ void load(const double* p, double* o) {
+    const double2 v = ld_stream(reinterpret_cast<const double2*>(p));
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+template <> struct VecLoad<int8_t, 16> {
+  static __device__ __forceinline__ void load(const int8_t* p, double* o) {
+    const int4 v = ld_stream(reinterpret_cast<const int4*>(p));
+    const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) o[4 * a + b] = double(int8_t((w[a] >> (8 * b)) & 0xff));
+  }
+};
+template <typename TX> struct VecLoad<TX, 1> {
+  static __device__ __forceinline__ void load(const TX* p, double* o) { o[0] = double(*p); }
+};
+
+template <typename TX> constexpr int vec_of() { return 16 / int(sizeof(TX)); }
+
+// ---------------------------------------------------------------------------
+// scn m: partial xb over a column chunk, VEC rows per thread.
+// grid = (row tiles, column splits); out slab s = parts + s*m.
+// ---------------------------------------------------------------------------
+
+constexpr int XB_THREADS = 256;
+constexpr int XB_UNROLL = 4;
+
+template <typename TX, typename TB, int VEC>
+__global__ void __launch_bounds__(XB_THREADS)
+xbeta_kernel(const TX* __restrict__ X, const TB* __restrict__ beta, int64_t m, int64_t n_loc,
+             int64_t cols_per_split, double* __restrict__ parts) {
+  const int64_t i0 = (int64_t(blockIdx.x) * XB_THREADS + threadIdx.x) * VEC;
+  const int64_t j_begin = int64_t(blockIdx.y) * cols_per_split;
+  const int64_t j_end = min(n_loc, j_begin + cols_per_split);
+  double acc[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
+  const bool full = i0 + VEC <= m;
+  if (i0 < m) {
+    int64_t j = j_begin;
+    if (full) {
+      for (; j + XB_UNROLL <= j_end; j += XB_UNROLL) {
+        double x[XB_UNROLL][VEC];
+        double b[XB_UNROLL];
+#pragma unroll
+        for (int u = 0; u < XB_UNROLL; ++u) {
+          VecLoad<TX, VEC>::load(X + (j + u) * m + i0, x[u]);
+          b[u] = double(__ldg(beta + j + u));
+        }
+#pragma unroll
+        for (int u = 0; u < XB_UNROLL; ++u)
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] = fma(x[u][v], b[u], acc[v]);
+      }
+      for (; j < j_end; ++j) {
+        double x[VEC];
+        VecLoad<TX, VEC>::load(X + j * m + i0, x);
+        const double b = double(__ldg(beta + j));
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] = fma(x[v], b, acc[v]);
+      }
+    } else {
+      for (; j < j_end; ++j) {
+        const double b = double(__ldg(beta + j));
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          if (i0 + v < m) acc[v] = fma(double(X[j * m + i0 + v]), b, acc[v]);
+      }
+    }
+    double* out = parts + int64_t(blockIdx.y) * m;
+#pragma unroll
+    for (int v = 0; v < VEC; ++v)
+      if (i0 + v < m) out[i0 + v] = acc[v];
+  }
+}
+
+__global__ void sum_slabs_f64(const double* __restrict__ parts, int S, int64_t len, double* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < len;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    double acc = parts[e];
+    for (int s = 1; s < S; ++s) acc += parts[int64_t(s) * len + e];
+    dst[e] = acc;
+  }
+}
+
+static int xsize(int xdtype) { return xdtype == BS_F64 ? 8 : xdtype == BS_F32 ? 4 : 1; }
+
+struct XbGrid {
+  int64_t tiles;
+  int splits;
+  int64_t cps;
+  int vec;
+};
+
+static XbGrid xb_grid(int xdtype, int64_t m, int64_t n_loc, bool vec_ok) {
+  XbGrid g;
+  g.vec = vec_ok ? 16 / xsize(xdtype) : 1;
+  g.tiles = std::max<int64_t>(1, ceil_div(m, int64_t(XB_THREADS) * g.vec));
+  const int64_t want = int64_t(num_sms()) * 6;
+  int64_t s = std::max<int64_t>(1, ceil_div(want, g.tiles));
+  s = std::min<int64_t>(s, std::max<int64_t>(1, n_loc / 64));
+  s = std::min<int64_t>(s, 128);
+  g.cps = ceil_div(std::max<int64_t>(n_loc, 1), s);
+  g.splits = int(ceil_div(std::max<int64_t>(n_loc, 1), g.cps));
+  return g;
+}
+
+extern "C" int64_t bs_cox_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) {
+  XbGrid g = xb_grid(xdtype, m, n_loc, false);  // vec=1 gives the most tiles, splits <= that case
+  XbGrid h = xb_grid(xdtype, m, n_loc, true);
+  return ws_bytes<double>(int64_t(std::max(g.splits, h.splits)) * m);
+}
+
+template <typename TX, typename TB>
+static void launch_xbeta(const TX* X, const TB* beta, int64_t m, int64_t n_loc, const XbGrid& g, double* out,
+                         cudaStream_t st) {
+  dim3 grid(unsigned(g.tiles), unsigned(g.splits));
+  constexpr int V = vec_of<TX>();
+  if (g.vec == V)
+    xbeta_kernel<TX, TB, V><<<grid, XB_THREADS, 0, st>>>(X, beta, m, n_loc, g.cps, out);
+  else
+    xbeta_kernel<TX, TB, 1><<<grid, XB_THREADS, 0, st>>>(X, beta, m, n_loc, g.cps, out);
+}
+
+extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dtype, int64_t m, int64_t n_loc,
+                            double* out, void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  cudaStream_t st = as_stream(stream);
+  if (m < 0 || n_loc < 0) { set_error("bs_cox_xbeta: negative shape"); return BS_EINVAL; }
+  if (m == 0) return BS_OK;
+  if (n_loc == 0) return cudaMemsetAsync(out, 0, sizeof(double) * m, st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  XbGrid g = xb_grid(xdtype, m, n_loc, vec_ok);
+  Workspace ws(work, work_bytes);
+  double* parts = g.splits > 1 ? ws.take<double>(int64_t(g.splits) * m) : out;
+  if (!parts) { set_error("bs_cox_xbeta: workspace too small"); return BS_EWORK; }
+#define BS_XB(TXT, TBT) launch_xbeta<TXT, TBT>(static_cast<const TXT*>(X), static_cast<const TBT*>(beta), m, n_loc, g, parts, st)
+  if (dtype == BS_F64) {
+    if (xdtype == BS_F64) BS_XB(double, double);
+    else if (xdtype == BS_F32) BS_XB(float, double);
+    else if (xdtype == BS_I8) BS_XB(int8_t, double);
+    else { set_error("bs_cox_xbeta: unsupported X dtype %d", xdtype); return BS_EINVAL; }
+  } else if (dtype == BS_F32) {
+    if (xdtype == BS_F32) BS_XB(float, float);
+    else if (xdtype == BS_I8) BS_XB(int8_t, float);
+    else if (xdtype == BS_F64) BS_XB(double, float);
+    else { set_error("bs_cox_xbeta: unsupported X dtype %d", xdtype); return BS_EINVAL; }
+  } else {
+    set_error("bs_cox_xbeta: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+#undef BS_XB
+  if (g.splits > 1)
+    sum_slabs_f64<<<int(std::min<int64_t>(ceil_div(m, 256), 2048)), 256, 0, st>>>(parts, g.splits, m, out);
+  return check_launch("bs_cox_xbeta", g.splits > 1 ? 2 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// Single-CTA inclusive scan helpers (float64, deterministic order).
+// ---------------------------------------------------------------------------
+
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_PER = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_PER;
+
+// Exclusive block scan of one value per thread; returns exclusive prefix and total.
+__device__ __forceinline__ double block_exscan(double v, double* sh, double* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) sh[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    double s = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    sh[lane] = s;  // inclusive over warps
+  }
+  __syncthreads();
+  const double warp_prefix = wid > 0 ? sh[wid - 1] : 0.0;
+  *total = sh[(blockDim.x >> 5) - 1];
+  return warp_prefix + x - v;
+}
+
+// risk: Xbeta = T(xb), w = exp(min(Xbeta, clamp)), W = cumsum(w), loglik.
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+risk_kernel(const double* __restrict__ xb, const T* __restrict__ delta, const int64_t* __restrict__ cuts, int64_t m,
+            double clamp, T* __restrict__ Xbeta, T* __restrict__ w, T* __restrict__ W, double* loglik,
+            int* flags) {
+  __shared__ double sh[32];
+  __shared__ int sflag;
+  if (*flags & BS_FLAG_NONFINITE) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  int myflag = 0;
+  double carry = 0.0;
+  for (int64_t t0 = 0; t0 < m; t0 += SCAN_TILE) {
+    const int64_t base = t0 + int64_t(threadIdx.x) * SCAN_PER;
+    double wv[SCAN_PER];
+    double loc = 0.0;
+#pragma unroll
+    for (int u = 0; u < SCAN_PER; ++u) {
+      const int64_t i = base + u;
+      wv[u] = 0.0;
+      if (i < m) {
+        const T xt = T(xb[i]);
+        Xbeta[i] = xt;
+        T arg = xt;
+        if (xt > T(clamp)) {  // solvers.py:383-385
+          myflag |= BS_FLAG_CLAMPED;
+          arg = T(clamp);
+        }
+        const T e = exp(arg);
+        if (!isfinite(double(e))) myflag |= BS_FLAG_NONFINITE;
+        w[i] = e;
+        wv[u] = double(e);
+        loc += wv[u];
+      }
+    }
+    double total;
+    double run = carry + block_exscan(loc, sh, &total);
+#pragma unroll
+    for (int u = 0; u < SCAN_PER; ++u) {
+      const int64_t i = base + u;
+      run += wv[u];
+      if (i < m) W[i] = T(run);
+    }
+    carry += total;
+  }
+  if (myflag) atomicOr(&sflag, myflag);
+  __syncthreads();  // W visible block-wide
+  // loglik = sum delta (Xbeta - log W[cuts])   (solvers.py:398)
+  double ll = 0.0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const double dl = double(delta[i]);
+    if (dl != 0.0) {
+      const int64_t c = cuts ? cuts[i] : i;
+      ll += dl * (double(Xbeta[i]) - log(double(W[c])));
+    }
+  }
+  ll = block_sum(ll, sh);
+  if (threadIdx.x == 0) {
+    loglik[0] = ll;
+    if (sflag) atomicOr(flags, sflag);
+  }
+}
+
+extern "C" int64_t bs_cox_risk_workspace(int64_t m) { (void)m; return 0; }
+
+extern "C" int bs_cox_risk(const double* xb, const void* delta, const int64_t* cuts, int dtype, int64_t m,
+                           double clamp, void* Xbeta, void* w, void* W, double* loglik_dev, int* flags, void* work,
+                           int64_t work_bytes, void* stream) {
+  clear_error();
+  (void)work;
+  (void)work_bytes;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == BS_F64)
+    risk_kernel<double><<<1, SCAN_THREADS, 0, st>>>(xb, static_cast<const double*>(delta), cuts, m, clamp,
+                                                    static_cast<double*>(Xbeta), static_cast<double*>(w),
+                                                    static_cast<double*>(W), loglik_dev, flags);
+  else if (dtype == BS_F32)
+    risk_kernel<float><<<1, SCAN_THREADS, 0, st>>>(xb, static_cast<const float*>(delta), cuts, m, clamp,
+                                                   static_cast<float*>(Xbeta), static_cast<float*>(w),
+                                                   static_cast<float*>(W), loglik_dev, flags);
+  else {
+    set_error("bs_cox_risk: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_cox_risk");
+}
+
+// ---------------------------------------------------------------------------
+// pi_delta: suffix sums of c_j = delta_j / W[cuts_j] over [lo, hi) (single CTA),
+// then pd_i = w_i * S[first(i)] with first(i) = min{j in [lo,hi): cuts_j >= i}.
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+suffix_kernel(const T* __restrict__ W, const T* __restrict__ delta, const int64_t* __restrict__ cuts, int64_t lo,
+              int64_t hi, double* __restrict__ S, const int* flags) {
+  __shared__ double sh[32];
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  const int64_t len = hi - lo;
+  double carry = 0.0;
+  // walk tiles from the end; within a tile, reversed index r = len-1-k
+  for (int64_t t0 = 0; t0 < len; t0 += SCAN_TILE) {
+    const int64_t base = t0 + int64_t(threadIdx.x) * SCAN_PER;
+    double cv[SCAN_PER];
+    double loc = 0.0;
+#pragma unroll
+    for (int u = 0; u < SCAN_PER; ++u) {
+      const int64_t rk = base + u;  // position in reversed order
+      cv[u] = 0.0;
+      if (rk < len) {
+        const int64_t j = hi - 1 - rk;
+        const int64_t c = cuts ? cuts[j] : j;
+        // solvers.py:412 contrib = delta / W[seg] in the storage type
+        cv[u] = double(T(delta[j]) / W[c]);
+        loc += cv[u];
+      }
+    }
+    double total;
+    double run = carry + block_exscan(loc, sh, &total);
+#pragma unroll
+    for (int u = 0; u < SCAN_PER; ++u) {
+      const int64_t rk = base + u;
+      run += cv[u];
+      if (rk < len) S[hi - 1 - rk - lo] = run;
+    }
+    carry += total;
+  }
+}
+
+template <typename T>
+__global__ void pd_kernel(const T* __restrict__ w, const T* __restrict__ delta, const int64_t* __restrict__ cuts,
+                          const double* __restrict__ S, int64_t m, int64_t lo, int64_t hi, T* __restrict__ pd,
+                          double* __restrict__ dmpd, const int* flags) {
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    // first j in [lo, hi) with cuts_j >= i  (searchsorted left, solvers.py:414)
+    int64_t a = lo, b = hi;
+    if (cuts) {
+      while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (cuts[mid] < i) a = mid + 1; else b = mid;
+      }
+    } else {
+      a = i < lo ? lo : i;
+    }
+    T v = T(0);
+    if (a < hi) v = T(S[a - lo]) * w[i];  // solvers.py:416-417
+    pd[i] = v;
+    if (dmpd) dmpd[i] = double(T(delta[i]) - v);  // solvers.py:446
+  }
+}
+
+extern "C" int64_t bs_cox_pi_delta_workspace(int64_t m) { return ws_bytes<double>(m); }
+
+extern "C" int bs_cox_pi_delta(const void* w, const void* W, const void* delta, const int64_t* cuts, int dtype,
+                               int64_t m, int64_t lo, int64_t hi, void* pd, double* dmpd, const int* flags,
+                               void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  if (lo < 0 || hi < lo || hi > m) {
+    set_error("bs_cox_pi_delta: bad range [%lld, %lld) for m=%lld", (long long)lo, (long long)hi, (long long)m);
+    return BS_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (m == 0) return BS_OK;
+  Workspace ws(work, work_bytes);
+  double* S = ws.take<double>(std::max<int64_t>(hi - lo, 1));
+  if (!S) { set_error("bs_cox_pi_delta: workspace too small"); return BS_EWORK; }
+  const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(num_sms()) * 4));
+  if (dtype == BS_F64) {
+    if (hi > lo)
+      suffix_kernel<double><<<1, SCAN_THREADS, 0, st>>>(static_cast<const double*>(W),
+                                                        static_cast<const double*>(delta), cuts, lo, hi, S, flags);
+    pd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(w), static_cast<const double*>(delta), cuts,
+                                            S, m, lo, hi, static_cast<double*>(pd), dmpd, flags);
+  } else if (dtype == BS_F32) {
+    if (hi > lo)
+      suffix_kernel<float><<<1, SCAN_THREADS, 0, st>>>(static_cast<const float*>(W), static_cast<const float*>(delta),
+                                                       cuts, lo, hi, S, flags);
+    pd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w), static_cast<const float*>(delta), cuts, S,
+                                           m, lo, hi, static_cast<float*>(pd), dmpd, flags);
+  } else {
+    set_error("bs_cox_pi_delta: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_cox_pi_delta", hi > lo ? 2 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// scn p: column dot products over row segments; v = dmpd segment staged in smem.
+// grid = (column groups, row segments); warps take columns round-robin.
+// ---------------------------------------------------------------------------
+
+constexpr int GR_THREADS = 256;
+constexpr int GR_SEG = 8192;  // rows per segment (64 KB of float64 v in smem)
+
+template <typename TX, int VEC>
+__global__ void __launch_bounds__(GR_THREADS)
+grad_kernel(const TX* __restrict__ X, const double* __restrict__ v, int64_t m, int64_t n_loc,
+            int64_t cols_per_group, double* __restrict__ parts, const int* flags) {
+  extern __shared__ __align__(16) double vs[];
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r0 = int64_t(blockIdx.y) * GR_SEG;
+  const int len = int(m - r0 < GR_SEG ? m - r0 : GR_SEG);
+  for (int e = threadIdx.x; e < len; e += blockDim.x) vs[e] = v[r0 + e];
+  __syncthreads();
+  const int64_t c0 = int64_t(blockIdx.x) * cols_per_group;
+  const int64_t c1 = min(n_loc, c0 + cols_per_group);
+  const int nvec = len / VEC;  // whole vectors; tail handled scalar
+  for (int64_t j = c0 + wid; j < c1; j += GR_THREADS / 32) {
+    const TX* col = X + j * m + r0;
+    double acc0 = 0.0, acc1 = 0.0;
+    int e = lane;
+    for (; e + 32 < nvec; e += 64) {
+      double x0[VEC], x1[VEC];
+      VecLoad<TX, VEC>::load(col + e * VEC, x0);
+      VecLoad<TX, VEC>::load(col + (e + 32) * VEC, x1);
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        acc0 = fma(x0[u], vs[e * VEC + u], acc0);
+        acc1 = fma(x1[u], vs[(e + 32) * VEC + u], acc1);
+      }
+    }
+    for (; e < nvec; e += 32) {
+      double x0[VEC];
+      VecLoad<TX, VEC>::load(col + e * VEC, x0);
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) acc0 = fma(x0[u], vs[e * VEC + u], acc0);
+    }
+    for (int t = nvec * VEC + lane; t < len; t += 32) acc1 = fma(double(col[t]), vs[t], acc1);
+    const double s = warp_sum(acc0 + acc1);
+    if (lane == 0) parts[int64_t(blockIdx.y) * n_loc + j] = s;
+  }
+}
+
+// prox: grad_j = sum_s parts[s][j]; beta_j <- S_lam(beta_j + sigma grad_j); l1 = sum |beta|.
+template <typename T>
+__global__ void __launch_bounds__(256)
+prox_kernel(const double* __restrict__ parts, int segs, int64_t n_loc, T* __restrict__ grad, T* __restrict__ beta,
+            double sigma, double lam, int do_step, double* __restrict__ bparts, unsigned int* counter,
+            double* __restrict__ l1, const int* flags) {
+  __shared__ double sh[32];
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  double acc = 0.0;
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n_loc; j += int64_t(gridDim.x) * blockDim.x) {
+    double g = parts[j];
+    for (int s = 1; s < segs; ++s) g += parts[int64_t(s) * n_loc + j];
+    const T gt = T(g);
+    grad[j] = gt;
+    T b = beta[j];
+    if (do_step) {
+      // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51)
+      const T x = b + T(sigma) * gt;
+      const T mag = fabs(x) - T(lam);
+      b = mag > T(0) ? copysign(mag, x) : T(0);
+      beta[j] = b;
+    }
+    acc += fabs(double(b));
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) bparts[blockIdx.x] = acc;
+  if (last_block_done(counter) && threadIdx.x == 0) {
+    double s = 0.0;
+    for (unsigned int k = 0; k < gridDim.x; ++k) s += bparts[k];
+    l1[0] = s;
+  }
+}
+
+struct GrGrid {
+  int groups, segs;
+  int64_t cpg;
+};
+
+static GrGrid gr_grid(int64_t m, int64_t n_loc) {
+  GrGrid g;
+  g.segs = int(std::max<int64_t>(1, ceil_div(m, GR_SEG)));
+  const int64_t want = int64_t(num_sms()) * 3;
+  int64_t groups = std::max<int64_t>(1, ceil_div(want, g.segs));
+  groups = std::min<int64_t>(groups, std::max<int64_t>(1, ceil_div(n_loc, 8)));
+  g.cpg = ceil_div(std::max<int64_t>(n_loc, 1), groups);
+  g.groups = int(ceil_div(std::max<int64_t>(n_loc, 1), g.cpg));
+  return g;
+}
+
+static int prox_grid(int64_t n_loc) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 256), int64_t(num_sms()))));
+}
+
+extern "C" int64_t bs_cox_grad_workspace(int xdtype, int64_t m, int64_t n_loc) {
+  (void)xdtype;
+  GrGrid g = gr_grid(m, n_loc);
+  return ws_bytes<double>(int64_t(g.segs) * std::max<int64_t>(n_loc, 1)) + ws_bytes<unsigned int>(1) +
+         ws_bytes<double>(prox_grid(n_loc));
+}
+
+template <typename TX>
+static void launch_grad(const TX* X, const double* v, int64_t m, int64_t n_loc, const GrGrid& g, bool vec_ok,
+                        double* parts, const int* flags, cudaStream_t st) {
+  dim3 grid(unsigned(g.groups), unsigned(g.segs));
+  constexpr int V = vec_of<TX>();
+  const int smem = int(sizeof(double) * GR_SEG);
+  static std::once_flag once;
+  std::call_once(once, [smem] {
+    cudaFuncSetAttribute(grad_kernel<TX, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(grad_kernel<TX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  if (vec_ok)
+    grad_kernel<TX, V><<<grid, GR_THREADS, smem, st>>>(X, v, m, n_loc, g.cpg, parts, flags);
+  else
+    grad_kernel<TX, 1><<<grid, GR_THREADS, smem, st>>>(X, v, m, n_loc, g.cpg, parts, flags);
+}
+
+extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, int dtype, int64_t m, int64_t n_loc,
+                                void* grad, void* beta, double sigma, double lam, int do_step, double* l1_dev,
+                                const int* flags, void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  cudaStream_t st = as_stream(stream);
+  if (n_loc == 0) return cudaMemsetAsync(l1_dev, 0, sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  Workspace ws(work, work_bytes);
+  GrGrid g = gr_grid(m, n_loc);
+  unsigned int* counter = ws.take<unsigned int>(1);
+  double* parts = ws.take<double>(int64_t(g.segs) * n_loc);
+  const int pg = prox_grid(n_loc);
+  double* bparts = ws.take<double>(pg);
+  if (!parts || !counter || !bparts) { set_error("bs_cox_grad_step: workspace too small"); return BS_EWORK; }
+  if (m == 0) {
+    if (cudaMemsetAsync(parts, 0, sizeof(double) * n_loc, st) != cudaSuccess) return BS_ECUDA;
+  } else {
+    const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+    if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
+    else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
+    else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
+    else { set_error("bs_cox_grad_step: unsupported X dtype %d", xdtype); return BS_EINVAL; }
+  }
+  const int segs = m == 0 ? 1 : g.segs;
+  if (dtype == BS_F64)
+    prox_kernel<double><<<pg, 256, 0, st>>>(parts, segs, n_loc, static_cast<double*>(grad), static_cast<double*>(beta),
+                                            sigma, lam, do_step, bparts, counter, l1_dev, flags);
+  else if (dtype == BS_F32)
+    prox_kernel<float><<<pg, 256, 0, st>>>(parts, segs, n_loc, static_cast<float*>(grad), static_cast<float*>(beta),
+                                           sigma, lam, do_step, bparts, counter, l1_dev, flags);
+  else {
+    set_error("bs_cox_grad_step: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_cox_grad_step", m > 0 ? 2 : 1);
+}
+
+__global__ void cox_objective_kernel(const double* loglik, const double* l1, double lam, double* out) {
+  out[0] = -loglik[0] + lam * l1[0];
+}
+
+extern "C" int bs_cox_objective(const double* loglik_dev, const double* l1_dev, double lam, double* out_dev,
+                                void* stream) {
+  clear_error();
+  cox_objective_kernel<<<1, 1, 0, as_stream(stream)>>>(loglik_dev, l1_dev, lam, out_dev);
+  return check_launch("bs_cox_objective");
+}

@@ -1,0 +1,715 @@
+// NMF hot path (solvers.py:73-185): the two skinny GEMMs over the streamed
+// data block X and the fused factor half-steps.
+//
+//   scn b  P  = W_loc X_loc^T      (r x m)       distlinalg.py:246-252
+//   scn a  C  = Vt_full X_loc      (r x n_loc)   distlinalg.py:239-243
+//   half-step F <- update(F, NUM, GRAM), Gram(F_new), <NUM, F_new>
+//                                                 solvers.py:150-159, 171-182
+//
+// Layouts (column-major blocks, distarray.py:82): X[j*m + i] (m x n_loc),
+// factors F[c*r + k] (r x ncols).  GEMM partials use the factor layout.
+//
+// This file holds the CUDA-core GEMMs used for float64 data (FP64 has no
+// tcgen05 kind) and as the reference implementation the tcgen05 3xTF32 path
+// (nmf_tc.cu) is checked against.
+#include "bsb200.cuh"
+
+#include <algorithm>
+#include <mutex>
+
+using namespace bs;
+
+namespace bs {
+int launch_reduce(const void* x, int dtype, int64_t count, int op, int transform, double* out,
+                  void* work, int64_t work_bytes, cudaStream_t st);
+int launch_gram(const void* A, int dtype, int r, int64_t ncols, double* G, Workspace& ws,
+                cudaStream_t st);
+// tcgen05 path (nmf_tc.cu); returns BS_EINVAL when the shape is not supported.
+int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, float* P, Workspace& ws,
+           cudaStream_t st, bool* used);
+int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, float* C, int cap_slabs,
+           int* splits, Workspace& ws, cudaStream_t st, bool* used);
+constexpr int TC_MAX_SPLITS = 16;
+int64_t tc_wxt_workspace(int64_t m, int64_t n_loc, int r);
+int64_t tc_vtx_workspace(int64_t m, int64_t n_loc, int r);
+}  // namespace bs
+
+constexpr int MAX_R = 128;
+
+// ---------------------------------------------------------------------------
+// _nmf_check + ||X||^2: min and sum of squares in one pass.
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+scan_kernel(const T* __restrict__ x, int64_t count, double* __restrict__ parts,
+            unsigned int* counter, double* out) {
+  __shared__ double shm[32], shs[32];
+  double mn = CUDART_INF, sq = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double v = double(x[i]);
+    mn = rop_apply(BS_MIN, mn, v);
+    sq = fma(v, v, sq);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = rop_apply(BS_MIN, mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  }
+  if (lane == 0) {
+    shm[wid] = mn;
+    shs[wid] = sq;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    double a = lane < (blockDim.x >> 5) ? shm[lane] : CUDART_INF;
+    double b = lane < (blockDim.x >> 5) ? shs[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = rop_apply(BS_MIN, a, __shfl_xor_sync(0xffffffffu, a, o));
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane == 0) {
+      parts[2 * blockIdx.x] = a;
+      parts[2 * blockIdx.x + 1] = b;
+    }
+  }
+  if (last_block_done(counter) && threadIdx.x == 0) {
+    double a = parts[0], b = parts[1];
+    for (unsigned int k = 1; k < gridDim.x; ++k) {
+      a = rop_apply(BS_MIN, a, parts[2 * k]);
+      b += parts[2 * k + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+extern "C" int bs_nmf_scan(const void* X, int dtype, int64_t count, double* out_dev, void* work,
+                           int64_t work_bytes, void* stream) {
+  clear_error();
+  Workspace ws(work, work_bytes);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, 2048), int64_t(num_sms()) * 4)));
+  unsigned int* counter = ws.take<unsigned int>(1);
+  double* parts = ws.take<double>(2 * grid);
+  if (!counter || !parts) {
+    set_error("bs_nmf_scan: workspace too small");
+    return BS_EWORK;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (dtype == BS_F64)
+    scan_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), count, parts, counter, out_dev);
+  else if (dtype == BS_F32)
+    scan_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), count, parts, counter, out_dev);
+  else {
+    set_error("bs_nmf_scan: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_nmf_scan");
+}
+
+// ---------------------------------------------------------------------------
+// CUDA-core skinny GEMMs.  Accumulation in T (fp32 / fp64).
+// ---------------------------------------------------------------------------
+
+template <typename T> struct GemmCfg;
+template <> struct GemmCfg<float> { static constexpr int BK = 32; };
+template <> struct GemmCfg<double> { static constexpr int BK = 16; };
+
+// scn b: P[i][k] = sum_j X[j][i] W[j][k] over j in the split's column range.
+// Tile: 128 rows i x RP columns k; 256 threads as 16 (ty: 8 rows) x 16 (tx: RP/16 cols).
+template <typename T, int RP>
+__global__ void __launch_bounds__(256)
+gemm_wxt_kernel(const T* __restrict__ X, const T* __restrict__ W, int64_t m, int64_t n_loc, int r,
+                int64_t cols_per_split, T* __restrict__ P) {
+  constexpr int BM = 128, BK = GemmCfg<T>::BK, TM = 8, TN = RP / 16;
+  __shared__ T Xs[BK][BM];
+  __shared__ T Ws[BK][RP];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t i0 = int64_t(blockIdx.x) * BM;
+  const int64_t j_begin = int64_t(blockIdx.y) * cols_per_split;
+  const int64_t j_end = min(n_loc, j_begin + cols_per_split);
+  T acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc[a][b] = T(0);
+
+  for (int64_t j0 = j_begin; j0 < j_end; j0 += BK) {
+    __syncthreads();
+    for (int e = tid; e < BK * BM; e += 256) {
+      const int jj = e / BM, ii = e % BM;
+      const int64_t j = j0 + jj, i = i0 + ii;
+      Xs[jj][ii] = (j < j_end && i < m) ? X[j * m + i] : T(0);
+    }
+    for (int e = tid; e < BK * RP; e += 256) {
+      const int jj = e / RP, k = e % RP;
+      const int64_t j = j0 + jj;
+      Ws[jj][k] = (j < j_end && k < r) ? W[j * r + k] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int t = 0; t < TM; ++t) a[t] = Xs[kk][ty * TM + t];
+#pragma unroll
+      for (int t = 0; t < TN; ++t) b[t] = Ws[kk][tx + 16 * t];
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+  }
+  T* out = P + int64_t(blockIdx.y) * m * r;
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    const int64_t i = i0 + ty * TM + u;
+    if (i >= m) continue;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) {
+      const int k = tx + 16 * v;
+      if (k < r) out[i * r + k] = acc[u][v];
+    }
+  }
+}
+
+// scn a: C[j][k] = sum_i X[j][i] Vt[i][k] over i in the split's row range.
+// Tile: 64 columns j x RP; 256 threads as 16 (ty: 4 columns) x 16 (tx: RP/16).
+template <typename T, int RP>
+__global__ void __launch_bounds__(256)
+gemm_vtx_kernel(const T* __restrict__ X, const T* __restrict__ Vt, int64_t m, int64_t n_loc, int r,
+                int64_t rows_per_split, T* __restrict__ C) {
+  constexpr int BN = 64, BK = GemmCfg<T>::BK, TM = 4, TN = RP / 16;
+  __shared__ T Xs[BK][BN + 1];
+  __shared__ T Vs[BK][RP];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int64_t jb = int64_t(blockIdx.x) * BN;
+  const int64_t i_begin = int64_t(blockIdx.y) * rows_per_split;
+  const int64_t i_end = min(m, i_begin + rows_per_split);
+  T acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc[a][b] = T(0);
+
+  for (int64_t i0 = i_begin; i0 < i_end; i0 += BK) {
+    __syncthreads();
+    for (int e = tid; e < BK * BN; e += 256) {
+      const int jj = e / BK, ii = e % BK;
+      const int64_t j = jb + jj, i = i0 + ii;
+      Xs[ii][jj] = (j < n_loc && i < i_end) ? X[j * m + i] : T(0);
+    }
+    for (int e = tid; e < BK * RP; e += 256) {
+      const int ii = e / RP, k = e % RP;
+      const int64_t i = i0 + ii;
+      Vs[ii][k] = (i < i_end && k < r) ? Vt[i * r + k] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T a[TM], b[TN];
+#pragma unroll
+      for (int t = 0; t < TM; ++t) a[t] = Xs[kk][ty * TM + t];
+#pragma unroll
+      for (int t = 0; t < TN; ++t) b[t] = Vs[kk][tx + 16 * t];
+#pragma unroll
+      for (int u = 0; u < TM; ++u)
+#pragma unroll
+        for (int v = 0; v < TN; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+    }
+  }
+  T* out = C + int64_t(blockIdx.y) * n_loc * r;
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    const int64_t j = jb + ty * TM + u;
+    if (j >= n_loc) continue;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) {
+      const int k = tx + 16 * v;
+      if (k < r) out[j * r + k] = acc[u][v];
+    }
+  }
+}
+
+// Sums S partial slabs [S][len] in order into dst[len].
+template <typename T>
+__global__ void sum_slabs_kernel(const T* __restrict__ parts, int S, int64_t len, T* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < len;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    T acc = parts[e];
+    for (int s = 1; s < S; ++s) acc += parts[int64_t(s) * len + e];
+    dst[e] = acc;
+  }
+}
+
+static int pick_rp(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 128; }
+
+// Split count so that the grid covers >= ~4 CTAs per SM, each split keeping >= min_k of K.
+static int pick_splits(int64_t tiles, int64_t K, int64_t min_k) {
+  const int64_t want = int64_t(num_sms()) * 4;
+  int64_t s = std::max<int64_t>(1, ceil_div(want, std::max<int64_t>(tiles, 1)));
+  s = std::min<int64_t>(s, std::max<int64_t>(1, K / min_k));
+  return int(std::min<int64_t>(s, 64));
+}
+
+template <typename T>
+static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, int r, int64_t cps,
+                            int S, T* out, cudaStream_t st) {
+  dim3 grid(unsigned(ceil_div(m, 128)), unsigned(S));
+  switch (pick_rp(r)) {
+    case 16: gemm_wxt_kernel<T, 16><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
+    case 32: gemm_wxt_kernel<T, 32><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
+    case 64: gemm_wxt_kernel<T, 64><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
+    default: gemm_wxt_kernel<T, 128><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
+  }
+}
+
+template <typename T>
+static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, int r, int64_t rps,
+                            int S, T* out, cudaStream_t st) {
+  dim3 grid(unsigned(ceil_div(n_loc, 64)), unsigned(S));
+  switch (pick_rp(r)) {
+    case 16: gemm_vtx_kernel<T, 16><<<grid, 256, 0, st>>>(X, Vt, m, n_loc, r, rps, out); break;
+    case 32: gemm_vtx_kernel<T, 32><<<grid, 256, 0, st>>>(X, Vt, m, n_loc, r, rps, out); break;
+    case 64: gemm_vtx_kernel<T, 64><<<grid, 256, 0, st>>>(X, Vt, m, n_loc, r, rps, out); break;
+    default: gemm_vtx_kernel<T, 128><<<grid, 256, 0, st>>>(X, Vt, m, n_loc, r, rps, out); break;
+  }
+}
+
+static int wxt_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(m, 128), n_loc, 256); }
+static int vtx_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(n_loc, 64), m, 512); }
+
+static int dsize(int dtype) { return dtype == BS_F64 ? 8 : 4; }
+
+extern "C" int64_t bs_nmf_wxt_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
+  int64_t core = ws_bytes<char>(int64_t(wxt_splits(m, n_loc)) * m * r * dsize(dtype));
+  if (dtype == BS_F32) core = std::max(core, tc_wxt_workspace(m, n_loc, r));
+  return core;
+}
+
+extern "C" int bs_nmf_wxt(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r,
+                          void* P, void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  if (r < 1 || r > MAX_R || m < 0 || n_loc < 0) {
+    set_error("bs_nmf_wxt: bad shape m=%lld n_loc=%lld r=%d", (long long)m, (long long)n_loc, r);
+    return BS_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (m == 0) return BS_OK;
+  if (n_loc == 0) {
+    return cudaMemsetAsync(P, 0, size_t(m) * r * dsize(dtype), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  }
+  Workspace ws(work, work_bytes);
+  if (dtype == BS_F32) {
+    bool used = false;
+    int rc = tc_wxt(static_cast<const float*>(X), static_cast<const float*>(W), m, n_loc, r,
+                    static_cast<float*>(P), ws, st, &used);
+    if (used || rc != BS_OK) return rc;
+  }
+  const int S = wxt_splits(m, n_loc);
+  const int64_t cps = ceil_div(ceil_div(n_loc, S), 32) * 32;
+  const int Seff = int(ceil_div(n_loc, cps));
+  if (dtype == BS_F64) {
+    double* out = static_cast<double*>(P);
+    double* parts = Seff > 1 ? ws.take<double>(int64_t(Seff) * m * r) : out;
+    if (!parts) { set_error("bs_nmf_wxt: workspace too small"); return BS_EWORK; }
+    launch_wxt_core<double>(static_cast<const double*>(X), static_cast<const double*>(W), m, n_loc, r,
+                            cps, Seff, parts, st);
+    if (Seff > 1)
+      sum_slabs_kernel<double><<<int(std::min<int64_t>(ceil_div(m * r, 256), 4096)), 256, 0, st>>>(
+          parts, Seff, m * r, out);
+  } else if (dtype == BS_F32) {
+    float* out = static_cast<float*>(P);
+    float* parts = Seff > 1 ? ws.take<float>(int64_t(Seff) * m * r) : out;
+    if (!parts) { set_error("bs_nmf_wxt: workspace too small"); return BS_EWORK; }
+    launch_wxt_core<float>(static_cast<const float*>(X), static_cast<const float*>(W), m, n_loc, r,
+                           cps, Seff, parts, st);
+    if (Seff > 1)
+      sum_slabs_kernel<float><<<int(std::min<int64_t>(ceil_div(m * r, 256), 4096)), 256, 0, st>>>(
+          parts, Seff, m * r, out);
+  } else {
+    set_error("bs_nmf_wxt: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_nmf_wxt", Seff > 1 ? 2 : 1);
+}
+
+// ---------------------------------------------------------------------------
+// Fused factor half-step (shared by the Vt and the W half-steps).
+//   NUM = sum over S slabs of num (r x ncols, layout F), den = GRAM F
+//   F <- MU:  F * NUM / (den + eps)      APG: max(0, F - step (den - NUM))
+//   red[0..r*r) += F_new F_new^T,  red[r*r] += <NUM, F_new>
+// One warp per column (lane k, k+32, ...), columns staged in smem for the Gram.
+// ---------------------------------------------------------------------------
+
+constexpr int UPD_THREADS = 256;
+constexpr int UPD_COLS = 32;  // columns per smem stage (one per warp-iteration)
+
+template <typename T, typename TN, int RP>
+__global__ void __launch_bounds__(UPD_THREADS)
+factor_update_kernel(int algo, T* __restrict__ F, const TN* __restrict__ num, int S,
+                     int64_t num_slab, const double* __restrict__ gram, int r, int64_t ncols,
+                     double eps, int64_t cols_per_block, T* __restrict__ Fcopy,
+                     double* __restrict__ parts, unsigned int* counter, double* __restrict__ red) {
+  extern __shared__ double smem[];
+  double* gT = smem;                 // [r][r] gram transposed: gT[l*r + k] = gram[k][l]
+  double* tile = smem + r * r;       // [UPD_COLS][r] updated columns
+  __shared__ double sh_red[32];
+  __shared__ double sh_step;
+  const int rr = r * r;
+  for (int e = threadIdx.x; e < rr; e += blockDim.x) {
+    const int k = e / r, l = e % r;
+    gT[l * r + k] = gram[e];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int e = 0; e < rr; ++e) s = fma(gram[e], gram[e], s);
+    sh_step = 1.0 / (2.0 * s + eps);  // solvers.py:174 / 180
+  }
+  __syncthreads();
+  const double step = sh_step;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int KPL = (RP + 31) / 32;  // rows k per lane
+  const int npairs = r * (r + 1) / 2;
+  constexpr int MAXP = (RP * (RP + 1) / 2 + UPD_THREADS - 1) / UPD_THREADS;
+  double gacc[MAXP];
+  int ia[MAXP], ib[MAXP];
+#pragma unroll
+  for (int t = 0; t < MAXP; ++t) {
+    gacc[t] = 0.0;
+    int a = 0, rem = threadIdx.x + t * UPD_THREADS;
+    if (rem < npairs) {
+      while (rem >= r - a) { rem -= r - a; ++a; }
+    } else {
+      rem = -1;
+    }
+    ia[t] = a;
+    ib[t] = a + rem;
+  }
+  double cross = 0.0;
+  const int64_t c_begin = int64_t(blockIdx.x) * cols_per_block;
+  const int64_t c_end = min(ncols, c_begin + cols_per_block);
+  for (int64_t cb = c_begin; cb < c_end; cb += UPD_COLS) {
+    const int nc = int(c_end - cb < UPD_COLS ? c_end - cb : UPD_COLS);
+    __syncthreads();  // tile reuse
+    for (int cc = wid; cc < nc; cc += UPD_THREADS / 32) {
+      const int64_t c = cb + cc;
+      double f[KPL], nm[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        f[q] = 0.0;
+        nm[q] = 0.0;
+        if (k < r) {
+          f[q] = double(F[c * r + k]);
+          double s = double(num[c * r + k]);
+          for (int p = 1; p < S; ++p) s += double(num[int64_t(p) * num_slab + c * r + k]);
+          // NUM is rounded to the storage type like the reference's WXt / VtX
+          nm[q] = double(T(s));
+        }
+      }
+      // den[k] = sum_l gram[k][l] f[l]
+      double den[KPL];
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) den[q] = 0.0;
+#pragma unroll
+      for (int ql = 0; ql < KPL; ++ql) {
+        const int lmax = min(32, r - 32 * ql);
+        for (int ll = 0; ll < lmax; ++ll) {
+          const int l = 32 * ql + ll;
+          const double fl = __shfl_sync(0xffffffffu, f[ql], ll);
+#pragma unroll
+          for (int q = 0; q < KPL; ++q) {
+            const int k = lane + 32 * q;
+            if (k < r) den[q] = fma(gT[l * r + k], fl, den[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k < r) {
+          const T dd = T(den[q]);  // WWtVt / VtVW in the storage type
+          T fn;
+          if (algo == BS_NMF_MU) {
+            fn = T(f[q]) * T(nm[q]) / (dd + T(eps));
+          } else {
+            const T v = T(f[q]) - T(step) * (dd - T(nm[q]));
+            fn = v > T(0) ? v : T(0);
+          }
+          F[c * r + k] = fn;
+          if (Fcopy) Fcopy[c * r + k] = fn;
+          tile[cc * r + k] = double(fn);
+          cross = fma(nm[q], double(fn), cross);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < MAXP; ++t) {
+      const int p = threadIdx.x + t * UPD_THREADS;
+      if (p < npairs) {
+        double s = gacc[t];
+        for (int cc = 0; cc < nc; ++cc) s = fma(tile[cc * r + ia[t]], tile[cc * r + ib[t]], s);
+        gacc[t] = s;
+      }
+    }
+  }
+  // per-block partial: [r*r gram][cross]
+  double* mine = parts + int64_t(blockIdx.x) * (rr + 1);
+#pragma unroll
+  for (int t = 0; t < MAXP; ++t) {
+    const int p = threadIdx.x + t * UPD_THREADS;
+    if (p < npairs) {
+      mine[ia[t] * r + ib[t]] = gacc[t];
+      mine[ib[t] * r + ia[t]] = gacc[t];
+    }
+  }
+  const double csum = block_sum(cross, sh_red);
+  if (threadIdx.x == 0) mine[rr] = csum;
+  if (last_block_done(counter)) fold_parts_block(parts, gridDim.x, rr + 1, BS_SUM, red);
+}
+
+static int upd_grid(int64_t ncols) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 256), int64_t(num_sms()) * 2)));
+}
+
+static int64_t upd_workspace(int r, int64_t ncols) {
+  return ws_bytes<unsigned int>(1) + ws_bytes<double>(int64_t(upd_grid(ncols)) * (r * r + 1)) +
+         ws_bytes<double>(r * r + 1);
+}
+
+template <typename T, typename TN>
+static int launch_update(int algo, T* F, const TN* num, int S, int64_t slab, const double* gram, int r,
+                         int64_t ncols, double eps, T* Fcopy, double* red, Workspace& ws,
+                         cudaStream_t st) {
+  const int grid = upd_grid(ncols);
+  unsigned int* counter = ws.take<unsigned int>(1);
+  double* parts = ws.take<double>(int64_t(grid) * (r * r + 1));
+  if (!counter || !parts) {
+    set_error("factor update: workspace too small");
+    return BS_EWORK;
+  }
+  const size_t smem = sizeof(double) * (r * r + UPD_COLS * r);
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const int big = int(sizeof(double) * (MAX_R * MAX_R + UPD_COLS * MAX_R));
+    cudaFuncSetAttribute(factor_update_kernel<T, TN, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(factor_update_kernel<T, TN, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(factor_update_kernel<T, TN, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaFuncSetAttribute(factor_update_kernel<T, TN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+  });
+  const int64_t cpb = ceil_div(ncols, grid);
+#define BS_UPD(RPV)                                                                              \
+  factor_update_kernel<T, TN, RPV><<<grid, UPD_THREADS, smem, st>>>(algo, F, num, S, slab, gram, r, \
+                                                                     ncols, eps, cpb, Fcopy, parts,  \
+                                                                     counter, red)
+  switch (pick_rp(r)) {
+    case 16: BS_UPD(16); break;
+    case 32: BS_UPD(32); break;
+    case 64: BS_UPD(64); break;
+    default: BS_UPD(128); break;
+  }
+#undef BS_UPD
+  return check_launch("factor update");
+}
+
+extern "C" int64_t bs_nmf_vt_step_workspace(int r, int64_t m_loc) {
+  return upd_workspace(r, m_loc) + ws_bytes<double>(r * r + 1) + 256;
+}
+
+extern "C" int bs_nmf_vt_step(int algo, void* Vt, const void* WXt, const double* WWt, int dtype,
+                              int r, int64_t m_loc, double eps, double* VtV, void* Vt_copy, void* work,
+                              int64_t work_bytes, void* stream) {
+  clear_error();
+  if (r < 1 || r > MAX_R || (algo != BS_NMF_MU && algo != BS_NMF_APG)) {
+    set_error("bs_nmf_vt_step: bad r=%d / algo=%d", r, algo);
+    return BS_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  Workspace all(work, work_bytes);
+  Workspace ws = all.split(upd_workspace(r, m_loc));
+  double* red = VtV;  // the kernel writes r*r+1 values; stage them and copy the gram out
+  double* tmp = all.take<double>(r * r + 1);
+  if (!tmp) { set_error("bs_nmf_vt_step: workspace too small"); return BS_EWORK; }
+  int rc;
+  if (m_loc == 0) {
+    if (cudaMemsetAsync(tmp, 0, sizeof(double) * (r * r + 1), st) != cudaSuccess) return BS_ECUDA;
+    rc = BS_OK;
+  } else if (dtype == BS_F64) {
+    rc = launch_update<double, double>(algo, static_cast<double*>(Vt), static_cast<const double*>(WXt), 1,
+                                       0, WWt, r, m_loc, eps, static_cast<double*>(Vt_copy), tmp, ws, st);
+  } else if (dtype == BS_F32) {
+    rc = launch_update<float, float>(algo, static_cast<float*>(Vt), static_cast<const float*>(WXt), 1, 0,
+                                     WWt, r, m_loc, eps, static_cast<float*>(Vt_copy), tmp, ws, st);
+  } else {
+    set_error("bs_nmf_vt_step: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  if (rc != BS_OK) return rc;
+  if (cudaMemcpyAsync(red, tmp, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+    set_error("bs_nmf_vt_step: copy failed");
+    return BS_ECUDA;
+  }
+  return BS_OK;
+}
+
+extern "C" int64_t bs_nmf_w_step_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
+  const int slabs = dtype == BS_F32 ? std::max(vtx_splits(m, n_loc), TC_MAX_SPLITS) : vtx_splits(m, n_loc);
+  int64_t g = ws_bytes<char>(int64_t(slabs) * n_loc * r * dsize(dtype));
+  if (dtype == BS_F32) g += tc_vtx_workspace(m, n_loc, r);
+  return g + upd_workspace(r, n_loc) + 512;
+}
+
+extern "C" int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void* W, const double* VtV,
+                             int dtype, int64_t m, int64_t n_loc, int r, double eps, double* red,
+                             void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  if (r < 1 || r > MAX_R || (algo != BS_NMF_MU && algo != BS_NMF_APG) || m < 0 || n_loc < 0) {
+    set_error("bs_nmf_w_step: bad arguments");
+    return BS_EINVAL;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (n_loc == 0) {
+    return cudaMemsetAsync(red, 0, sizeof(double) * (r * r + 1), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  }
+  Workspace ws(work, work_bytes);
+  Workspace upd = ws.split(upd_workspace(r, n_loc));
+  const int S = vtx_splits(m, n_loc);
+  const int64_t rps = std::max<int64_t>(1, ceil_div(ceil_div(std::max<int64_t>(m, 1), S), 32) * 32);
+  const int Seff = int(std::max<int64_t>(1, ceil_div(m, rps)));
+  if (dtype == BS_F64) {
+    double* C = ws.take<double>(int64_t(Seff) * n_loc * r);
+    if (!C) { set_error("bs_nmf_w_step: workspace too small"); return BS_EWORK; }
+    if (m == 0) {
+      if (cudaMemsetAsync(C, 0, sizeof(double) * n_loc * r, st) != cudaSuccess) return BS_ECUDA;
+    } else {
+      launch_vtx_core<double>(static_cast<const double*>(X), static_cast<const double*>(Vt_full), m, n_loc,
+                              r, rps, Seff, C, st);
+    }
+    int rc = check_launch("bs_nmf_w_step gemm");
+    if (rc != BS_OK) return rc;
+    return launch_update<double, double>(algo, static_cast<double*>(W), C, Seff, n_loc * r, VtV, r, n_loc,
+                                         eps, nullptr, red, upd, st);
+  } else if (dtype == BS_F32) {
+    // tcgen05 3xTF32 when available for this shape, CUDA cores otherwise
+    int splits = 1;
+    bool used = false;
+    const int cap = std::max(Seff, TC_MAX_SPLITS);
+    float* Cbuf = ws.take<float>(int64_t(cap) * n_loc * r);
+    if (!Cbuf) { set_error("bs_nmf_w_step: workspace too small"); return BS_EWORK; }
+    if (m > 0) {
+      int rc = tc_vtx(static_cast<const float*>(X), static_cast<const float*>(Vt_full), m, n_loc, r, Cbuf,
+                      cap, &splits, ws, st, &used);
+      if (rc != BS_OK) return rc;
+    }
+    if (!used) {
+      splits = Seff;
+      if (m == 0) {
+        if (cudaMemsetAsync(Cbuf, 0, sizeof(float) * n_loc * r, st) != cudaSuccess) return BS_ECUDA;
+      } else {
+        launch_vtx_core<float>(static_cast<const float*>(X), static_cast<const float*>(Vt_full), m, n_loc, r,
+                               rps, Seff, Cbuf, st);
+      }
+      int rc = check_launch("bs_nmf_w_step gemm");
+      if (rc != BS_OK) return rc;
+    }
+    return launch_update<float, float>(algo, static_cast<float*>(W), Cbuf, splits, n_loc * r, VtV, r, n_loc,
+                                       eps, nullptr, red, upd, st);
+  }
+  set_error("bs_nmf_w_step: unsupported dtype %d", dtype);
+  return BS_EINVAL;
+}
+
+// ---------------------------------------------------------------------------
+// Objective via the Gram identity (after an update).
+// ---------------------------------------------------------------------------
+
+__global__ void nmf_objective_kernel(const double* xsq, const double* red, const double* VtV, int r,
+                                     double* out) {
+  __shared__ double sh[32];
+  const int rr = r * r;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < rr; e += blockDim.x) s = fma(VtV[e], red[e], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[0] = (xsq[0] - 2.0 * red[rr]) + s;
+}
+
+extern "C" int bs_nmf_objective(const double* xsq, const double* red, const double* VtV, int r,
+                                double* out_dev, void* stream) {
+  clear_error();
+  nmf_objective_kernel<<<1, 256, 0, as_stream(stream)>>>(xsq, red, VtV, r, out_dev);
+  return check_launch("bs_nmf_objective");
+}
+
+// ---------------------------------------------------------------------------
+// Standalone objective: direct residual sum((X - Vt^T W)^2) over the local block.
+// One warp per column j: the column's factor W[:, j] lives in registers and
+// every lane reconstructs rows i = lane, lane+32, ...
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+residual_kernel(const T* __restrict__ X, const T* __restrict__ Vt, const T* __restrict__ W, int64_t m,
+                int64_t n_loc, int r, double* __restrict__ parts, unsigned int* counter, double* out) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double acc = 0.0;
+  for (int64_t j = gw; j < n_loc; j += nw) {
+    for (int64_t i = lane; i < m; i += 32) {
+      T rec = T(0);
+      for (int k = 0; k < r; ++k) rec = fma(Vt[i * r + k], W[j * r + k], rec);
+      const double d = double(X[j * m + i] - rec);
+      acc = fma(d, d, acc);
+    }
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = acc;
+  if (last_block_done(counter) && threadIdx.x == 0) {
+    double s = parts[0];
+    for (unsigned int b = 1; b < gridDim.x; ++b) s += parts[b];
+    out[0] = s;
+  }
+}
+
+static int residual_grid(int64_t n_loc) {
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 8), int64_t(num_sms()) * 4)));
+}
+
+extern "C" int64_t bs_nmf_residual_workspace(int64_t m, int64_t n_loc) {
+  (void)m;
+  return ws_bytes<unsigned int>(1) + ws_bytes<double>(residual_grid(n_loc));
+}
+
+extern "C" int bs_nmf_residual(const void* X, const void* Vt_full, const void* W, int dtype, int64_t m,
+                               int64_t n_loc, int r, double* out_dev, void* work, int64_t work_bytes,
+                               void* stream) {
+  clear_error();
+  cudaStream_t st = as_stream(stream);
+  if (n_loc == 0 || m == 0)
+    return cudaMemsetAsync(out_dev, 0, sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  Workspace ws(work, work_bytes);
+  const int grid = residual_grid(n_loc);
+  unsigned int* counter = ws.take<unsigned int>(1);
+  double* parts = ws.take<double>(grid);
+  if (!counter || !parts) { set_error("bs_nmf_residual: workspace too small"); return BS_EWORK; }
+  if (dtype == BS_F64)
+    residual_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), static_cast<const double*>(Vt_full),
+                                                  static_cast<const double*>(W), m, n_loc, r, parts, counter,
+                                                  out_dev);
+  else if (dtype == BS_F32)
+    residual_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), static_cast<const float*>(Vt_full),
+                                                 static_cast<const float*>(W), m, n_loc, r, parts, counter,
+                                                 out_dev);
+  else {
+    set_error("bs_nmf_residual: unsupported dtype %d", dtype);
+    return BS_EINVAL;
+  }
+  return check_launch("bs_nmf_residual");
+}

@@ -1,0 +1,256 @@
+"""GPU: l1-Cox (solvers.py:337-450) against the reference's golden vectors and the oracle."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_2010_16114_b200 as bs
+from oracle import blockstat_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+COX_CASES = ["m40_n12_lam01", "m40_n12_powersigma", "m40_n12_f32", "m40_n12_breslow"]
+
+
+def _dist(comm, a):
+    return bs.distribute(a if comm.rank == 0 else None, comm)
+
+
+@pytest.mark.parametrize("name", COX_CASES)
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_cox_matches_reference_golden(golden, name, p):
+    x = golden[f"cox_{name}_x"]
+    y = golden[f"cox_{name}_y"]
+    delta = golden[f"cox_{name}_delta"]
+    lam, sigma, iters, breslow, _ = golden[f"cox_{name}_meta"]
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=lam, sigma=None if sigma < 0 else sigma,
+                         ties="breslow" if breslow else "none")
+        bs.cox_fit(st, int(iters))
+        return (np.asarray(st.trace), bs.gather_full(st.beta), bs.gather_full(st.grad), st.sigma,
+                st.w.cpu().numpy(), st.W.cpu().numpy(), st.pd.cpu().numpy())
+
+    tr, beta, grad, sig, w, W, pd = bs.run_inproc(p, fn)[0]
+    tol = 1e-10 if x.dtype == np.float64 else 1e-4
+    np.testing.assert_allclose(sig, golden[f"cox_{name}_sigma"][0], rtol=1e-12 if x.dtype == np.float64 else 1e-6)
+    np.testing.assert_allclose(tr, golden[f"cox_{name}_trace"], rtol=tol)
+    np.testing.assert_allclose(beta, golden[f"cox_{name}_beta"], rtol=tol * 10, atol=tol)
+    np.testing.assert_allclose(grad, golden[f"cox_{name}_grad"], rtol=tol * 10, atol=tol)
+    np.testing.assert_allclose(W, golden[f"cox_{name}_W"], rtol=tol)
+    np.testing.assert_allclose(pd, golden[f"cox_{name}_pd"], rtol=tol * 10, atol=tol)
+
+
+@pytest.mark.parametrize("m,n,p,breslow", [(500, 300, 1, False), (777, 129, 3, True), (1000, 2000, 2, False),
+                                          (64, 1500, 4, False), (2048, 8, 1, True)])
+def test_cox_matches_oracle(m, n, p, breslow):
+    bt = np.zeros(n)
+    bt[: min(5, n)] = 0.3
+    x, y, delta = orc.survival_data(900 + n, m, n, bt)
+    if breslow:
+        y = -np.sort(-np.round(y * 4) / 4)
+    cuts = orc.tie_cuts(y) if breslow else np.arange(m)
+    lam, sigma, iters = 0.02, 0.5 / (np.linalg.norm(x, 2) ** 2), 30
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=lam, sigma=sigma, ties="breslow" if breslow else "none")
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.beta), bs.gather_full(st.grad)
+
+    tr, beta, grad = bs.run_inproc(p, fn)[0]
+    ob, og, otr = orc.cox_fit(x, delta, cuts, lam, sigma, iters)
+    np.testing.assert_allclose(tr, otr, rtol=1e-10)
+    np.testing.assert_allclose(beta, ob, rtol=1e-8, atol=1e-12)
+    np.testing.assert_allclose(grad, og, rtol=1e-8, atol=1e-9)
+
+
+def test_cox_int8_genotypes_widen_exactly():
+    """int8 {0,1,2} storage computes the same iterates as float64 storage of the same values."""
+    gen = np.random.Generator(np.random.Philox(5))
+    m, n = 600, 400
+    maf = gen.uniform(0.05, 0.5, size=n)
+    g = gen.binomial(2, maf, size=(m, n)).astype(np.int8)
+    eta = g[:, :3].astype(np.float64) @ np.array([0.4, -0.3, 0.2])
+    t = gen.exponential(1.0 / np.exp(eta))
+    order = np.argsort(-t)
+    g, t = g[order], t[order]
+    delta = (gen.random(m) < 0.3).astype(np.float64)
+    sigma = 0.5 / np.linalg.norm(g.astype(np.float64), 2) ** 2
+
+    def fn(comm, arr):
+        st = bs.cox_init(_dist(comm, arr), t, delta, lam=0.01, sigma=sigma)
+        bs.cox_fit(st, 20)
+        return np.asarray(st.trace), bs.gather_full(st.beta)
+
+    for p in (1, 3):
+        tr8, b8 = bs.run_inproc(p, fn, g)[0]
+        tr64, b64 = bs.run_inproc(p, fn, g.astype(np.float64))[0]
+        np.testing.assert_allclose(tr8, tr64, rtol=1e-13)
+        np.testing.assert_allclose(b8, b64, rtol=1e-12, atol=1e-15)
+    ob, _, otr = orc.cox_fit(g.astype(np.float64), delta, np.arange(m), 0.01, sigma, 20)
+    np.testing.assert_allclose(tr8, otr, rtol=1e-10)
+
+
+def test_cox_loglik_zero_beta_and_single_subject():
+    x, y, delta = orc.survival_data(70, 8, 3)
+    want = -float(np.sum(delta * np.log(np.arange(1, 9))))
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.0, sigma=0.01)
+        one = bs.cox_init(_dist(comm, np.array([[1.5, -2.0]])), np.array([3.0]), np.array([1.0]), lam=0.0, sigma=0.01)
+        one.beta.local[...] = _dist(comm, np.array([0.3, 0.7])).local
+        return bs.cox_partial_loglik(st), bs.cox_partial_loglik(one)
+
+    for ll, single in bs.run_inproc(2, fn):
+        assert ll == pytest.approx(want, rel=1e-12)
+        assert single == pytest.approx(0.0, abs=1e-14)
+
+
+def test_pi_delta_examples_and_rank_partials(golden):
+    def two(comm):
+        out = np.empty(2)
+        bs.pi_delta(out, np.ones(2), np.cumsum(np.ones(2)), np.ones(2), comm.rank, comm.rank + 1, comm)
+        return out
+
+    for out in bs.run_inproc(2, two):
+        np.testing.assert_array_equal(out, [1.5, 0.5])
+
+    w, W, d, cuts = golden["pid_w"], golden["pid_W"], golden["pid_delta"], golden["pid_cuts"]
+    for p in (1, 3):
+        def fn(comm):
+            part = bs.partition_of(23, comm.size)
+            out = np.empty(23)
+            bs.pi_delta(out, w, W, d, part.lo(comm.rank), part.hi(comm.rank), comm, cuts=cuts)
+            return out
+
+        for out in bs.run_inproc(p, fn):
+            np.testing.assert_allclose(out, golden[f"pid_out_p{p}"], rtol=1e-13, atol=1e-15)
+
+    def zero_events(comm):
+        out = np.empty(4)
+        lo, hi = [(0, 2), (2, 4)][comm.rank]
+        bs.pi_delta(out, np.ones(4), np.cumsum(np.ones(4)), np.zeros(4), lo, hi, comm)
+        return out
+
+    for out in bs.run_inproc(2, zero_events):
+        np.testing.assert_array_equal(out, np.zeros(4))
+
+
+def test_cox_gradient_matches_dense_and_finite_differences():
+    x, y, delta = orc.survival_data(74, 12, 4)
+    beta_d = np.random.Generator(np.random.Philox(74)).standard_normal(4) * 0.2
+
+    def dense(b):
+        eta = x @ b
+        risk = y[:, None] >= y[None, :]
+        big_w = (risk * np.exp(eta)[:, None]).sum(axis=0)
+        ll = float(np.sum(delta * (eta - np.log(big_w))))
+        p_mat = risk * np.exp(eta)[:, None] / big_w[None, :]
+        return ll, x.T @ (delta - p_mat @ delta)
+
+    _, gwant = dense(beta_d)
+    h = 1e-6
+    fd = np.array([(dense(beta_d + h * e)[0] - dense(beta_d - h * e)[0]) / (2 * h) for e in np.eye(4)])
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.0, sigma=0.01)
+        st.beta.local[...] = _dist(comm, beta_d).local
+        bs.cox_fit(st, 1, trace_every=0)
+        return bs.gather_full(st.grad), bs.gather_full(st.beta)
+
+    for p in (1, 2, 3):
+        grad, beta = bs.run_inproc(p, fn)[0]
+        np.testing.assert_allclose(grad, gwant, rtol=1e-10)
+        np.testing.assert_allclose(grad, fd, rtol=1e-5)
+        np.testing.assert_allclose(beta, beta_d + 0.01 * gwant, rtol=1e-10)
+
+
+def test_cox_lambda_dominant_keeps_beta_exactly_zero():
+    x, y, delta = orc.survival_data(75, 10, 3)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e9, sigma=0.01)
+        bs.cox_fit(st, 5)
+        return bs.gather_full(st.beta)
+
+    for beta in bs.run_inproc(2, fn):
+        np.testing.assert_array_equal(beta, np.zeros(3))
+
+
+def test_cox_monitor_stops_early_like_reference():
+    x, y, delta = orc.survival_data(78, 10, 2, np.array([0.5, -0.5]))
+    sigma = 1.0 / (2.0 * orc.opnorm_l2_power(x) ** 2)
+    _, _, otr = orc.cox_fit(x, delta, np.arange(10), 0.1, sigma, 10_000, window=10)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.1)
+        mon = bs.ConvergenceMonitor()
+        bs.cox_fit(st, 10_000, monitor=mon)
+        return np.asarray(st.trace), len(mon.history)
+
+    tr, nh = bs.run_inproc(2, fn)[0]
+    assert len(tr) < 10_000 and len(tr) == len(otr) == nh
+    np.testing.assert_allclose(tr, otr, rtol=1e-9)
+
+
+def test_cox_overflow_clamps_with_warning():
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, np.array([[400.0], [-400.0]])), np.array([2.0, 1.0]), np.array([1.0, 1.0]),
+                         lam=0.0, sigma=1e-9)
+        st.beta.local[...] = _dist(comm, np.array([10.0])).local
+        with pytest.warns(RuntimeWarning):
+            val = bs.cox_partial_loglik(st)
+        return val
+
+    assert np.isfinite(bs.run_inproc(1, fn)[0])
+
+
+def test_cox_nonfinite_input_raises():
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, np.array([[np.nan], [0.0]])), np.array([2.0, 1.0]), np.array([1.0, 1.0]),
+                         lam=0.0, sigma=0.1)
+        bs.cox_partial_loglik(st)
+
+    with pytest.raises(bs.NumericError):
+        bs.run_inproc(1, fn)
+
+    def fit(comm):
+        st = bs.cox_init(_dist(comm, np.array([[np.nan], [0.0]])), np.array([2.0, 1.0]), np.array([1.0, 1.0]),
+                         lam=0.0, sigma=0.1)
+        try:
+            bs.cox_fit(st, 3)
+        except bs.NumericError:
+            return st.trace
+        return None
+
+    assert bs.run_inproc(1, fit)[0] == []
+
+
+def test_cox_init_validation():
+    bad = [
+        (np.array([1.0, 2.0, 3.0]), np.array([1.0, 0.0, 1.0]), "none"),    # unsorted
+        (np.array([3.0, 2.0, 1.0]), np.array([1.0, 0.5, 1.0]), "none"),    # bad delta
+        (np.array([2.0, 2.0, 1.0]), np.array([1.0, 0.0, 1.0]), "none"),    # ties need breslow
+        (np.array([3.0, 2.0, 1.0]), np.array([1.0, 0.0, 1.0]), "efron"),   # unknown mode
+    ]
+    for y, d, ties in bad:
+        def fn(comm):
+            bs.cox_init(bs.zeros((3, 2), comm), y, d, lam=0.0, sigma=0.1, ties=ties)
+
+        with pytest.raises(ValueError):
+            bs.run_inproc(2, fn)
+
+
+def test_cox_unpenalized_gradient_vanishes_at_optimum():
+    bt = np.array([0.8, -0.6, 0.0, 0.0, 0.4])
+    x, y, delta = orc.survival_data(76, 20, 5, bt)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.0)
+        bs.cox_fit(st, 800, trace_every=0)
+        bs.cox_fit(st, 1, trace_every=0)
+        return np.linalg.norm(bs.gather_full(st.grad))
+
+    for g in bs.run_inproc(2, fn):
+        assert g <= 1e-4
