@@ -43,6 +43,12 @@ inline int check_launch(const char* what, int n = 1) {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Most split-K slabs the tcgen05 GEMMs write (nmf_tc.cu).
+constexpr int TC_MAX_SPLITS = 16;
+
+// dst[e] = sum_s parts[s*len + e], slabs folded in order (nmf.cu).
+void launch_sum_slabs_f32(const float* parts, int S, int64_t len, float* dst, cudaStream_t st);
+
 // Workspace bump allocator over a caller-provided buffer (256-B aligned).
 struct Workspace {
   char* base;

@@ -29,7 +29,6 @@ int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, floa
            cudaStream_t st, bool* used);
 int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, float* C, int cap_slabs,
            int* splits, Workspace& ws, cudaStream_t st, bool* used);
-constexpr int TC_MAX_SPLITS = 16;
 int64_t tc_wxt_workspace(int64_t m, int64_t n_loc, int r);
 int64_t tc_vtx_workspace(int64_t m, int64_t n_loc, int r);
 }  // namespace bs
@@ -244,6 +243,13 @@ __global__ void sum_slabs_kernel(const T* __restrict__ parts, int S, int64_t len
     dst[e] = acc;
   }
 }
+
+namespace bs {
+void launch_sum_slabs_f32(const float* parts, int S, int64_t len, float* dst, cudaStream_t st) {
+  sum_slabs_kernel<float><<<int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(len, 256), 4096))), 256, 0, st>>>(
+      parts, S, len, dst);
+}
+}  // namespace bs
 
 static int pick_rp(int r) { return r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 128; }
 
