@@ -9,12 +9,13 @@ below turn torch tensors into those arguments.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import re
 import threading
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libbsb200.so"
+LIB_PATH = Path(os.environ.get("BS_LIB_PATH", str(PKG / "libbsb200.so")))
 HEADER = PKG.parent / "include" / "bsb200.h"
 
 # status codes (bsb200.h)

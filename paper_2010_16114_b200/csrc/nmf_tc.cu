@@ -3,21 +3,26 @@
 //   scn b  P[i][k] = sum_j X[j][i] W[j][k]    A = X MN-major (i contiguous), K = j   (distlinalg.py:246-252)
 //   scn a  C[j][k] = sum_i X[j][i] Vt[i][k]   A = X K-major  (i contiguous), K = i   (distlinalg.py:239-243)
 //
-// M = 128 rows per tile on the tensor cores, N = r padded to a multiple of 32
-// (the MN-major SW128 atom of B), K in blocks of 32.  Precision: float32 via
-// 3xTF32 — every operand x is split into hi = tf32(x) (mantissa truncated, an
-// exact tf32 value) and lo = x - hi (exact in fp32), and the accumulator in
-// TMEM collects hi*hi + hi*lo + lo*hi (the dropped lo*lo term is ~2^-22 relative).
+// M = 128 rows per tile on the tensor cores, N = r padded to a multiple of 32,
+// K in blocks of 32.  Precision: float32 via 3xTF32 — every operand x is split
+// into hi = tf32(x) (mantissa truncated: an exact tf32 value) and lo = x - hi
+// (exact in fp32); the products hi*hi + hi*lo + lo*hi are accumulated and the
+// dropped lo*lo term is ~2^-22 relative.
 //
-// Warp roles (192 threads, one CTA per SM, persistent over (tile, k-split) units):
-//   warp 0      TMA producer: X tile (16 KB) + B tile (r x 32) per stage, SWIZZLE_128B
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (3 MMAs per 8-wide k step)
-//   warps 2-5   converters: split each landed stage in place (hi) and into a
-//               parallel buffer (lo) with the same swizzled layout, then
-//               epilogue: tcgen05.ld the 128 x N accumulator and store the
-//               unit's partial rows into its split-K slab.
-// X is read exactly once per GEMM; the split-K slabs are folded (in order) by
-// the fused factor-update kernel that consumes them.
+// Data flow per k-block (one CTA per SM, persistent over (tile, k-split) units):
+//   warp 0       TMA producer: raw X tile (16 KB) + raw B tile (r x 32) into a
+//                6-deep smem ring (SWIZZLE_128B for K-major X, SWIZZLE_128B_ATOM_32B
+//                for MN-major operands — the only MN-major layout tf32 accepts)
+//   warps 6-13   two converter sets (alternate k-blocks): each thread takes one
+//                X row, splits it, tcgen05.st's hi|lo into TMEM (A operand, K-major),
+//                splits the B tile into hi|lo smem buffers, then frees the raw stage
+//   warp 1       tcgen05.mma issuer, one elected lane for the whole warp: per 8-wide
+//                k step D[:,0:2N] += A_hi [Bh|Bl] and D[:,0:N] += A_lo Bh (N <= 64)
+//   warps 2-5    epilogue: tcgen05.ld each finished accumulator group and fold it
+//                into fp32 registers (round-to-nearest), store the unit's rows
+// X is read exactly once per GEMM; split-K slabs are folded in order by the
+// consumer.  The TMEM accumulator is double-buffered and restarted every G
+// k-blocks because the tensor core's fp32 accumulation truncates (see below).
 #include "bsb200.cuh"
 
 #include <cuda.h>
@@ -30,10 +35,13 @@ using namespace bs;
 
 namespace {
 
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 448;  // producer, MMA, 4 epilogue warps, 2 x 4 converter warps
 constexpr int BM = 128;
 constexpr int BK = 32;
 constexpr int A_STAGE_BYTES = BM * BK * 4;  // 16 KB
+#ifndef BS_TC_CSTAGES
+#define BS_TC_CSTAGES 3
+#endif
 constexpr int SMEM_BUDGET = 220 * 1024;
 
 // ---------------------------------------------------------------------------
@@ -97,10 +105,10 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
 // SMEM matrix descriptor (tcgen05): start, LBO, SBO in 16-byte units, version 1, layout type.
-// Layout types: 2 = SWIZZLE_128B (K-major tiles, Swizzle<3,4,3>, 8-row atoms);
-// 1 = SWIZZLE_128B_BASE32B, the only MN-major layout tf32 accepts (Swizzle<2,5,2>,
-// 4-row x 128 B atoms) — the TMA produces it with CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.
-constexpr uint32_t LAYOUT_SW128 = 2, LAYOUT_SW128_32B = 1;
+// Layout type 1 = SWIZZLE_128B_BASE32B, the only MN-major layout tf32 accepts
+// (Swizzle<2,5,2>, 4-row x 128 B atoms); the TMA writes it with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.  (K-major tiles use SWIZZLE_128B.)
+constexpr uint32_t LAYOUT_SW128_32B = 1;
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
   uint64_t d = 0;
@@ -117,20 +125,6 @@ __device__ __forceinline__ uint64_t mn_desc(uint32_t base, int s) {
   return sdesc(base + uint32_t(s) * 1024u, 4096, 512, LAYOUT_SW128_32B);
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -143,30 +137,107 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// Splits 4 words in place: hi = tf32-truncated x (exact tf32), lo = x - hi (exact fp32).
-__device__ __forceinline__ void split4(uint4* hi_p, uint4* lo_p) {
-  uint4 v = *hi_p;
-  uint4 h, l;
-  h.x = v.x & 0xFFFFE000u;
-  h.y = v.y & 0xFFFFE000u;
-  h.z = v.z & 0xFFFFE000u;
-  h.w = v.w & 0xFFFFE000u;
-  l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
-  l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
-  l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
-  l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
-  *hi_p = h;
-  *lo_p = l;
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
 }
 
+// One k-block (4 k steps of 8) of the concatenated 3xTF32 product, issued by one elected
+// lane: D[:, 0:2NP] += A_hi [Bh|Bl] and D[:, 0:NP] += A_lo Bh per k step.  All operands
+// are warp-uniform; the k-step offsets are added inside the asm so ptxas keeps them in
+// uniform registers (a per-MMA elect/R2UR loop costs ~2x the MMA itself).
+// bdesc: descriptor of the Bh slab at k step 0; each k step advances 1024 B (desc lo + 64).
+__device__ __forceinline__ void mma_kblock_concat(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bdesc,
+                                                  uint32_t id_wide, uint32_t id_narrow, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "add.s64 b1, %3, 64;\n\tadd.s64 b2, %3, 128;\n\tadd.s64 b3, %3, 192;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, q;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+8], b1, %4, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+8], b1, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+16], b2, %4, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+16], b2, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], b3, %4, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+24], b3, %5, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bdesc), "r"(id_wide), "r"(id_narrow), "r"(acc0)
+      : "memory");
+}
+
+// Non-concatenated variant (NP > 64): three MMAs per k step, Bl slab at bdesc_lo.
+__device__ __forceinline__ void mma_kblock_3(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                             uint32_t id, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 h1, h2, h3, l1, l2, l3;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "add.s64 h1, %3, 64;\n\tadd.s64 h2, %3, 128;\n\tadd.s64 h3, %3, 192;\n\t"
+      "add.s64 l1, %4, 64;\n\tadd.s64 l2, %4, 128;\n\tadd.s64 l3, %4, 192;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, q;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+8], h1, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+8], l1, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+8], h1, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+16], h2, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+16], l2, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+16], h2, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+24], h3, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], l3, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], h3, %5, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(id), "r"(acc0)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+// Stage layout.  Raw ring (TMA targets): A raw (16 KB) + B raw (NP x 32 fp32).  Converted
+// ring: B hi | B lo in smem (MN-major, same swizzled layout as the raw tile) and the A
+// tile's tf32 hi | lo halves in TMEM (128 lanes x 64 columns, K-major: lane = row).
+// With NP <= 64 the MMA uses [B hi | B lo] as one N = 2*NP operand: per 8-wide k step
+// D[:, 0:2NP] += A_hi [Bh|Bl]  and  D[:, 0:NP] += A_lo Bh — two instructions instead of
+// three (an M=128 MMA costs ~45 cycles up to N = 64, measured).
 template <int NP>
 struct TcCfg {
-  static constexpr int B_BYTES = NP * BK * 4;                 // NP/32 MN-atoms of 32 rows x 128 B
-  static constexpr int STAGE = 2 * A_STAGE_BYTES + 2 * B_BYTES;  // A hi, A lo, B hi, B lo
-  static constexpr int STAGES = (SMEM_BUDGET - 2048) / STAGE > 6 ? 6 : (SMEM_BUDGET - 2048) / STAGE;
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align*/ + 512 /*barriers*/;
-  // two accumulator buffers of NP columns (power of two allocation)
-  static constexpr int TMEM_COLS = 2 * NP <= 64 ? 64 : 2 * NP <= 128 ? 128 : 256;
+  static constexpr bool CONCAT = NP <= 64;
+  static constexpr int ACC_COLS = CONCAT ? 2 * NP : NP;     // per accumulator buffer
+  static constexpr int B_BYTES = NP * BK * 4;                 // one of B raw / B hi / B lo
+  static constexpr int RAW = A_STAGE_BYTES + B_BYTES;
+  static constexpr int CONV = 2 * B_BYTES;
+  static constexpr int CSTAGES = BS_TC_CSTAGES;               // converted stages (TMEM A + smem B)
+  static constexpr int RSTAGES_FIT = (SMEM_BUDGET - 2048 - CSTAGES * CONV) / RAW;
+  static constexpr int RSTAGES = RSTAGES_FIT > 8 ? 8 : RSTAGES_FIT;
+  static constexpr int SMEM = RSTAGES * RAW + CSTAGES * CONV + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int TMEM_COLS = 512;                       // 2 accumulators + CSTAGES x 64 A columns
+  static constexpr int A_COL0 = 2 * ACC_COLS;                 // first TMEM column of the A stages
+  static_assert(2 * ACC_COLS + CSTAGES * 64 <= 512, "TMEM budget");
 };
 
 // ---------------------------------------------------------------------------
@@ -177,40 +248,44 @@ struct TcCfg {
 // 7e-6 relative after K = 320).  The K range of a unit is therefore cut into
 // groups of G k-blocks; each group accumulates into a fresh TMEM buffer (two
 // buffers alternate) and the epilogue warps fold the group partial into fp32
-// registers with round-to-nearest adds.  The error is then bounded by one group
-// (12*G MMAs) instead of the whole K extent.
+// registers with round-to-nearest adds.  The error is then bounded by one group.
 // ---------------------------------------------------------------------------
 
 template <bool A_MN, int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K, int r,
-               int tiles, int kb_per_split, int units, int G, float* __restrict__ out, int64_t slab) {
+               int tiles, int kb_per_split, int units, int G, float* __restrict__ out, int64_t slab, int mode) {
   using C = TcCfg<NP>;
-  constexpr int STAGES = C::STAGES;
+  constexpr int RS = C::RSTAGES, CS = C::CSTAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
-  // bars: full[STAGES], conv[STAGES], empty[STAGES], acc_full[2], acc_empty[2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * STAGES + 4);
+  uint8_t* conv_base = smem + RS * C::RAW;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(conv_base + CS * C::CONV);
+  // bars: raw_full[RS], raw_empty[RS], conv_full[CS], conv_empty[CS], acc_full[2], acc_empty[2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * CS + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb_total = (K + BK - 1) / BK;
 
-  auto stage_a = [&](int s) { return smem + s * C::STAGE; };
-  auto stage_al = [&](int s) { return smem + s * C::STAGE + A_STAGE_BYTES; };
-  auto stage_b = [&](int s) { return smem + s * C::STAGE + 2 * A_STAGE_BYTES; };
-  auto stage_bl = [&](int s) { return smem + s * C::STAGE + 2 * A_STAGE_BYTES + C::B_BYTES; };
-  auto full = [&](int s) { return smem_u32(bars + s); };
-  auto conv = [&](int s) { return smem_u32(bars + STAGES + s); };
-  auto empty = [&](int s) { return smem_u32(bars + 2 * STAGES + s); };
-  auto acc_full = [&](int b) { return smem_u32(bars + 3 * STAGES + b); };
-  auto acc_empty = [&](int b) { return smem_u32(bars + 3 * STAGES + 2 + b); };
+  auto raw_a = [&](int s) { return smem + s * C::RAW; };
+  auto raw_b = [&](int s) { return smem + s * C::RAW + A_STAGE_BYTES; };
+  auto conv_bh = [&](int c) { return conv_base + c * C::CONV; };
+  auto conv_bl = [&](int c) { return conv_base + c * C::CONV + C::B_BYTES; };
+  auto raw_full = [&](int s) { return smem_u32(bars + s); };
+  auto raw_empty = [&](int s) { return smem_u32(bars + RS + s); };
+  auto conv_full = [&](int c) { return smem_u32(bars + 2 * RS + c); };
+  auto conv_empty = [&](int c) { return smem_u32(bars + 2 * RS + CS + c); };
+  auto acc_full = [&](int b) { return smem_u32(bars + 2 * RS + 2 * CS + b); };
+  auto acc_empty = [&](int b) { return smem_u32(bars + 2 * RS + 2 * CS + 2 + b); };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), 1);
-      mbar_init(conv(s), 128);
-      mbar_init(empty(s), 1);
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(raw_full(s), 1);
+      mbar_init(raw_empty(s), 128);
+    }
+    for (int c = 0; c < CS; ++c) {
+      mbar_init(conv_full(c), 128);
+      mbar_init(conv_empty(c), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full(b), 1);
@@ -237,129 +312,195 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int stage = 0;
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int split = u / tiles, tile = u % tiles;
+        const int split = u / tiles, tile = u - split * tiles;
         const int kb0 = split * kb_per_split;
         const int kb1 = min(kb_total, kb0 + kb_per_split);
         const int m0 = tile * BM;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(empty(stage), phase ^ 1);
-          const uint32_t fb = full(stage);
+          mbar_wait(raw_empty(stage), phase ^ 1);
+          const uint32_t fb = raw_full(stage);
           mbar_expect_tx(fb, A_STAGE_BYTES + C::B_BYTES);
           const int k0 = kb * BK;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int a = 0; a < BM / 32; ++a) tma_load_2d(smem_u32(stage_a(stage) + a * 4096), &tmA, m0 + 32 * a, k0, fb);
+            for (int a = 0; a < BM / 32; ++a) tma_load_2d(smem_u32(raw_a(stage) + a * 4096), &tmA, m0 + 32 * a, k0, fb);
           } else {
-            tma_load_2d(smem_u32(stage_a(stage)), &tmA, k0, m0, fb);
+            tma_load_2d(smem_u32(raw_a(stage)), &tmA, k0, m0, fb);
           }
 #pragma unroll
-          for (int b = 0; b < NP / 32; ++b) tma_load_2d(smem_u32(stage_b(stage) + b * 4096), &tmB, 32 * b, k0, fb);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int b = 0; b < NP / 32; ++b) tma_load_2d(smem_u32(raw_b(stage) + b * 4096), &tmB, 32 * b, k0, fb);
+          if (++stage == RS) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    // idesc: D f32, A/B tf32, A major (MN for scn b), B MN-major, N = NP, M = 128
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) | (1u << 16) |
-                           (uint32_t(NP >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-    int stage = 0;
-    uint32_t phase = 0;
-    uint32_t gi = 0;  // global group counter (shared sequence with the epilogue)
+    // idesc: D f32, A/B tf32, A K-major (TMEM), B MN-major; N per instruction set below, M = 128
+    const uint32_t idesc_base = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | (uint32_t(BM >> 4) << 24);
+    const uint32_t idesc_wide = idesc_base | (uint32_t(C::ACC_COLS >> 3) << 17);
+    const uint32_t idesc_narrow = idesc_base | (uint32_t(NP >> 3) << 17);
+    int cst = 0;
+    uint32_t cphase = 0;
+    uint32_t gi = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int split = u / tiles;
       const int kb0 = split * kb_per_split;
       const int kb1 = min(kb_total, kb0 + kb_per_split);
+      int in_group = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
-        const int in_group = (kb - kb0) % G;
         const uint32_t buf = gi & 1;
         if (in_group == 0) {
           mbar_wait(acc_empty(buf), ((gi >> 1) & 1) ^ 1);
           tc_fence_after();
         }
-        mbar_wait(conv(stage), phase);
+        mbar_wait(conv_full(cst), cphase);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t d = tmem + buf * NP;
-          const uint32_t a = smem_u32(stage_a(stage)), al = smem_u32(stage_al(stage));
-          const uint32_t b = smem_u32(stage_b(stage)), bl = smem_u32(stage_bl(stage));
-#pragma unroll
-          for (int s = 0; s < BK / 8; ++s) {
-            uint64_t da, dal;
-            if constexpr (A_MN) {
-              da = mn_desc(a, s);
-              dal = mn_desc(al, s);
+        const bool last = (in_group == G - 1) || (kb == kb1 - 1);
+        {
+          // warp-uniform operands (broadcast so ptxas can use uniform registers)
+          const uint32_t d = __shfl_sync(0xffffffffu, tmem + buf * C::ACC_COLS, 0);
+          const uint32_t a_hi = __shfl_sync(0xffffffffu, tmem + C::A_COL0 + cst * 64, 0);
+          const uint32_t bh = __shfl_sync(0xffffffffu, smem_u32(conv_bh(cst)), 0);
+          const uint32_t acc0 = in_group > 0 ? 1u : 0u;
+          if (!(mode & 2)) {
+            if constexpr (C::CONCAT) {
+              mma_kblock_concat(d, a_hi, a_hi + 32, mn_desc(bh, 0), idesc_wide, idesc_narrow, acc0);
             } else {
-              da = sdesc(a + s * 32, 16, 1024, LAYOUT_SW128);
-              dal = sdesc(al + s * 32, 16, 1024, LAYOUT_SW128);
+              const uint32_t bl = __shfl_sync(0xffffffffu, smem_u32(conv_bl(cst)), 0);
+              mma_kblock_3(d, a_hi, a_hi + 32, mn_desc(bh, 0), mn_desc(bl, 0), idesc_narrow, acc0);
             }
-            const uint64_t db = mn_desc(b, s);
-            const uint64_t dbl = mn_desc(bl, s);
-            const uint32_t acc = (in_group > 0 || s > 0) ? 1u : 0u;
-            mma_tf32(d, dal, db, idesc, acc);  // lo * hi (small terms first)
-            mma_tf32(d, da, dbl, idesc, 1u);   // hi * lo
-            mma_tf32(d, da, db, idesc, 1u);    // hi * hi
           }
-          mma_commit(empty(stage));
-          if (in_group == G - 1 || kb == kb1 - 1) mma_commit(acc_full(buf));
+          mma_commit_elect(conv_empty(cst));
+          if (last) mma_commit_elect(acc_full(buf));
         }
         __syncwarp();
-        if (in_group == G - 1 || kb == kb1 - 1) ++gi;
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (last) {
+          ++gi;
+          in_group = 0;
+        } else {
+          ++in_group;
+        }
+        if (++cst == CS) { cst = 0; cphase ^= 1; }
       }
     }
-  } else {
-    // ---------------- converters + epilogue (warps 2..5) ----------------
-    const int ct = threadIdx.x - 64;  // 0..127
-    const int q = warp & 3;           // TMEM lane quarter this warp may access
-    int stage = 0;
-    uint32_t phase = 0;
+  } else if (warp < 6) {
+    // ---------------- epilogue (warps 2..5): fold TMEM group partials in fp32 RN ----------------
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t lane_addr = uint32_t(q * 32) << 16;
     uint32_t gi = 0;
     float acc[NP];
-    // folds group `g` (buffer g & 1) of TMEM into acc[] and releases the buffer
-    auto drain = [&](uint32_t g) {
-      const uint32_t buf = g & 1;
-      mbar_wait(acc_full(buf), (g >> 1) & 1);
-      tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < NP; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + (uint32_t(q * 32) << 16) + buf * NP + uint32_t(c0), v);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[c0 + i] = __fadd_rn(acc[c0 + i], v[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(acc_empty(buf));
-    };
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int split = u / tiles, tile = u % tiles;
+      const int split = u / tiles, tile = u - split * tiles;
       const int kb0 = split * kb_per_split;
       const int kb1 = min(kb_total, kb0 + kb_per_split);
+      const int groups = (kb1 - kb0 + G - 1) / G;
 #pragma unroll
       for (int i = 0; i < NP; ++i) acc[i] = 0.f;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        mbar_wait(full(stage), phase);
-        uint4* a = reinterpret_cast<uint4*>(stage_a(stage));
-        uint4* al = reinterpret_cast<uint4*>(stage_al(stage));
+      for (int g = 0; g < groups; ++g, ++gi) {
+        const uint32_t buf = gi & 1;
+        mbar_wait(acc_full(buf), (gi >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-        for (int e = ct; e < A_STAGE_BYTES / 16; e += 128) split4(a + e, al + e);
-        uint4* b = reinterpret_cast<uint4*>(stage_b(stage));
-        uint4* bl = reinterpret_cast<uint4*>(stage_bl(stage));
+        for (int c0 = 0; c0 < NP; c0 += 16) {
+          float v[16];
+          tmem_ld16(tmem + lane_addr + buf * C::ACC_COLS + uint32_t(c0), v);
+          if constexpr (C::CONCAT) {
+            float w[16];
+            tmem_ld16(tmem + lane_addr + buf * C::ACC_COLS + uint32_t(NP + c0), w);
 #pragma unroll
-        for (int e = ct; e < C::B_BYTES / 16; e += 128) split4(b + e, bl + e);
-        fence_proxy_async_smem();
-        mbar_arrive(conv(stage));
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        // the previous group finished while this stage was converted: fold it
-        if ((kb - kb0) % G == 0 && kb > kb0) drain(gi++);
+            for (int i = 0; i < 16; ++i) acc[c0 + i] = __fadd_rn(acc[c0 + i], __fadd_rn(v[i], w[i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[c0 + i] = __fadd_rn(acc[c0 + i], v[i]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(acc_empty(buf));
       }
-      drain(gi++);  // last group of the unit
-      const int row = tile * BM + q * 32 + lane;
-      if (row < M) {
-        float* dst = out + int64_t(split) * slab + int64_t(row) * r;
+      if (tile * BM + row_in_tile < M) {
+        float* dst = out + int64_t(split) * slab + int64_t(tile * BM + row_in_tile) * r;
 #pragma unroll
         for (int i = 0; i < NP; ++i)
           if (i < r) dst[i] = acc[i];
+      }
+    }
+  } else {
+    // ---------------- converters (warps 6..13): two sets alternate k-blocks ----------------
+    const int set = (warp - 6) >> 2;
+    const int ct = threadIdx.x - 192 - set * 128;  // 0..127 within the set
+    const int q = warp & 3;
+    const int row_in_tile = q * 32 + lane;
+    const uint32_t lane_addr = uint32_t(q * 32) << 16;
+    uint32_t j = 0;  // CTA-local block sequence number
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int split = u / tiles;
+      const int kb0 = split * kb_per_split;
+      const int kb1 = min(kb_total, kb0 + kb_per_split);
+      for (int kb = kb0; kb < kb1; ++kb, ++j) {
+        if (int(j & 1) != set) continue;
+        const int rst = int(j % RS), cst = int(j % CS);
+        const uint32_t rphase = (j / RS) & 1, cphase = (j / CS) & 1;
+        mbar_wait(raw_full(rst), rphase);
+        mbar_wait(conv_empty(cst), cphase ^ 1);
+        tc_fence_after();
+        // ---- A: this thread's row (32 K values) -> hi/lo -> TMEM ----
+        uint32_t hi[32], lo[32];
+        const uint32_t a_base = smem_u32(raw_a(rst));
+        if (!(mode & 1)) {
+          if constexpr (A_MN) {
+            // MN-major, Swizzle<2,5,2> atoms of 32 rows x 128 B (one atom per 32 M rows)
+            const uint32_t atom = a_base + uint32_t(row_in_tile >> 5) * 4096u;
+            const uint32_t mb = uint32_t(row_in_tile & 31) * 4u;
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const uint32_t off = uint32_t(k) * 128u + mb;
+              hi[k] = ld_shared_u32(atom + (off ^ (((off >> 7) & 3u) << 5)));
+            }
+          } else {
+            // K-major SW128: row at row*128 B, 16 B chunk c stored at c ^ (row & 7)
+            const uint32_t rowb = a_base + uint32_t(row_in_tile) * 128u;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const uint4 v = ld_shared_v4(rowb + (uint32_t(c ^ (row_in_tile & 7)) << 4));
+              hi[4 * c] = v.x; hi[4 * c + 1] = v.y; hi[4 * c + 2] = v.z; hi[4 * c + 3] = v.w;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 32; ++k) {
+            const uint32_t h = hi[k] & 0xFFFFE000u;
+            lo[k] = __float_as_uint(__uint_as_float(hi[k]) - __uint_as_float(h));
+            hi[k] = h;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 32; ++k) hi[k] = lo[k] = 0u;
+        }
+        const uint32_t a_col = tmem + lane_addr + uint32_t(C::A_COL0 + cst * 64);
+        tmem_st32(a_col, hi);
+        tmem_st32(a_col + 32, lo);
+        // ---- B: elementwise split into the converted buffers (same swizzled layout) ----
+        {
+          const uint32_t bsrc = smem_u32(raw_b(rst));
+          const uint32_t bh = smem_u32(conv_bh(cst)), bl = smem_u32(conv_bl(cst));
+#pragma unroll
+          for (int e = ct; e < C::B_BYTES / 16; e += 128) {
+            const uint4 v = ld_shared_v4(bsrc + 16u * e);
+            uint4 h, l;
+            h.x = v.x & 0xFFFFE000u; h.y = v.y & 0xFFFFE000u; h.z = v.z & 0xFFFFE000u; h.w = v.w & 0xFFFFE000u;
+            l.x = __float_as_uint(__uint_as_float(v.x) - __uint_as_float(h.x));
+            l.y = __float_as_uint(__uint_as_float(v.y) - __uint_as_float(h.y));
+            l.z = __float_as_uint(__uint_as_float(v.z) - __uint_as_float(h.z));
+            l.w = __float_as_uint(__uint_as_float(v.w) - __uint_as_float(h.w));
+            st_shared_v4(bh + 16u * e, h);
+            st_shared_v4(bl + 16u * e, l);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(raw_empty(rst));  // the raw stage is free again: TMA can refill it
+        mbar_arrive(conv_full(cst));
       }
     }
   }
@@ -436,9 +577,15 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r,
   static std::once_flag g_once;
   std::call_once(g_once, [] {
     const char* e = getenv("BS_TC_GROUP");
-    group = (e && atoi(e) > 0) ? atoi(e) : 2;
+    group = (e && atoi(e) > 0) ? atoi(e) : 4;
   });
-  tc_gemm_kernel<A_MN, NP><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, M, K, r, tiles, kb_per, units, group, out, slab);
+  static int mode = 0;
+  static std::once_flag m_once;
+  std::call_once(m_once, [] {
+    const char* e = getenv("BS_TC_MODE");
+    mode = e ? atoi(e) : 0;
+  });
+  tc_gemm_kernel<A_MN, NP><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, M, K, r, tiles, kb_per, units, group, out, slab, mode);
   return real_splits;
 }
 
