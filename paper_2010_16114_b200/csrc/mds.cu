@@ -15,92 +15,234 @@
 #include "bsb200.cuh"
 
 #include <algorithm>
+#include <mutex>
 
 using namespace bs;
 
 constexpr int MDS_THREADS = 256;
 constexpr int MDS_WARPS = MDS_THREADS / 32;
 
-// Pass kernel: each warp owns JB columns; lanes stride over the rows of the
-// CTA's row segment.  Partials per row segment s:
-//   zsum_part[s][jl], T_part[s][jl][k] (float64); stress/zero per CTA.
+// Pass kernel.  A CTA owns 8*JB columns (JB per warp) and one row segment.  The
+// segment is walked in chunks of CH rows; for every chunk the theta rows (CH x q,
+// contiguous in global memory) and the CTA's Y tile (CH rows of each of its
+// columns, contiguous per column) are copied into shared memory with cp.async,
+// double-buffered so chunk c+1 streams in while chunk c is computed.  Every lane
+// then walks rows i = lane, lane+32, ... of the chunk.  Per pair: g (q FMA), d,
+// stress, z, zsum and T_j += theta_i (1 - z) (q FMA); theta_j, the T partials and
+// zsum live in registers for the whole segment.  Arithmetic in the storage type
+// (the reference computes float32 data in float32); float32 uses one refined
+// rsqrt per pair, float64 IEEE sqrt/div (exact on exact inputs).
+//   Partials per row segment s: zsum_part[s][jl], T_part[s][jl][k] (float64);
+//   stress / zero count per CTA (float64).
+template <typename T>
+struct MdsChunk {
+  static constexpr int CH = sizeof(T) == 4 ? 128 : 64;  // rows per chunk
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+// one element of T
+template <typename T>
+__device__ __forceinline__ void cp_async_elem(T* smem, const T* gmem) {
+  if constexpr (sizeof(T) == 8) cp_async8(smem, gmem);
+  else cp_async4(smem, gmem);
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issues the async copies of chunk [c0, c0+rows) into buffer b.
+template <typename T, int QS, int JB>
+__device__ __forceinline__ void mds_stage(T* th_s, T* y_s, const T* __restrict__ theta, const T* __restrict__ Y,
+                                          int64_t n, int64_t jl0_cta, int64_t n_loc, int q, int64_t c0, int rows,
+                                          bool vec_th, bool vec) {
+  constexpr int CH = MdsChunk<T>::CH;
+  constexpr int VW = 16 / int(sizeof(T));
+  constexpr int NC = MDS_WARPS * JB;  // columns of the CTA
+  // theta rows: QS-strided rows in smem; global rows are q-strided
+  if (vec_th && QS == q) {
+    const int words = rows * QS / VW;
+    for (int e = threadIdx.x; e < words; e += MDS_THREADS) cp_async16(th_s + e * VW, theta + c0 * q + int64_t(e) * VW);
+  } else {
+    for (int e = threadIdx.x; e < rows * q; e += MDS_THREADS) {
+      const int rr = e / q, k = e - rr * q;
+      cp_async_elem(th_s + rr * QS + k, theta + (c0 + rr) * q + k);
+    }
+  }
+  // Y tile: column c of the CTA -> y_s[c * CH + rr]
+  if (vec) {
+    const int per_col = rows / VW;  // rows is a multiple of VW when vec
+    for (int e = threadIdx.x; e < NC * per_col; e += MDS_THREADS) {
+      const int c = e / per_col, w = e - c * per_col;
+      const int64_t jl = jl0_cta + c;
+      if (jl < n_loc) cp_async16(y_s + c * CH + w * VW, Y + jl * n + c0 + int64_t(w) * VW);
+    }
+  } else {
+    for (int e = threadIdx.x; e < NC * rows; e += MDS_THREADS) {
+      const int c = e / rows, rr = e - c * rows;
+      const int64_t jl = jl0_cta + c;
+      if (jl < n_loc) cp_async_elem(y_s + c * CH + rr, Y + jl * n + c0 + rr);
+    }
+  }
+  cp_async_commit();
+}
+
 template <typename T, int QM, int JB>
 __global__ void __launch_bounds__(MDS_THREADS)
 mds_pass_kernel(const T* __restrict__ Y, const T* __restrict__ theta, int64_t n, int64_t lo,
                 int64_t n_loc, int q, int perturb, int mode, int64_t rows_per_seg,
                 double* __restrict__ zsum_part, double* __restrict__ T_part,
                 double* __restrict__ parts, unsigned int* counter, double* __restrict__ red) {
+  constexpr int VW = 16 / int(sizeof(T));                       // elements per 16-byte word
+  constexpr int QS0 = (QM + VW - 1) / VW * VW;
+  constexpr int QS = ((QS0 / VW) % 2 == 0) ? QS0 + VW : QS0;    // odd number of 16-byte words
+  constexpr int CH = MdsChunk<T>::CH;
+  constexpr int NC = MDS_WARPS * JB;
+  extern __shared__ __align__(16) uint8_t mds_smem[];
+  T* th_buf[2] = {reinterpret_cast<T*>(mds_smem), reinterpret_cast<T*>(mds_smem) + CH * QS};
+  T* y_buf[2] = {reinterpret_cast<T*>(mds_smem) + 2 * CH * QS, reinterpret_cast<T*>(mds_smem) + 2 * CH * QS + NC * CH};
   __shared__ double sh_a[32], sh_b[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t jl0 = (int64_t(blockIdx.x) * MDS_WARPS + wid) * JB;
+  const int64_t jl0_cta = int64_t(blockIdx.x) * NC;
+  const int64_t jl0 = jl0_cta + int64_t(wid) * JB;
   const int64_t i_begin = int64_t(blockIdx.y) * rows_per_seg;
   const int64_t i_end = min(n, i_begin + rows_per_seg);
+  const bool vec = (n % VW == 0) && (i_begin % VW == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0);
+  const bool vec_th = (q % VW == 0) && (reinterpret_cast<uintptr_t>(theta) % 16 == 0);
 
-  double tj[JB][QM], nj[JB], Tacc[JB][QM], zs[JB];
+  T tj[JB][QM], Tacc[JB][QM], nj[JB], zs[JB];
   bool live[JB];
 #pragma unroll
   for (int c = 0; c < JB; ++c) {
     const int64_t jl = jl0 + c;
     live[c] = jl < n_loc;
     const int64_t jg = lo + (live[c] ? jl : 0);
-    double s = 0.0;
+    T s = T(0);
 #pragma unroll
     for (int k = 0; k < QM; ++k) {
-      tj[c][k] = (k < q && live[c]) ? double(theta[jg * q + k]) : 0.0;
+      tj[c][k] = (k < q && live[c]) ? theta[jg * q + k] : T(0);
       s = fma(tj[c][k], tj[c][k], s);
-      Tacc[c][k] = 0.0;
+      Tacc[c][k] = T(0);
     }
     nj[c] = s;
-    zs[c] = 0.0;
+    zs[c] = T(0);
   }
+  // zero the theta padding columns once (cp.async never writes them)
+  for (int e = threadIdx.x; e < 2 * CH * QS; e += MDS_THREADS)
+    if ((e % QS) >= q) th_buf[0][e] = T(0);
   double stress = 0.0, zeros = 0.0;
-  for (int64_t i = i_begin + lane; i < i_end; i += 32) {
-    double ti[QM];
-    double ni = 0.0;
-#pragma unroll
-    for (int k = 0; k < QM; ++k) {
-      ti[k] = k < q ? double(theta[i * q + k]) : 0.0;
-      ni = fma(ti[k], ti[k], ni);
+  const int64_t nchunks = (i_end - i_begin + CH - 1) / CH;
+  if (nchunks > 0)
+    mds_stage<T, QS, JB>(th_buf[0], y_buf[0], theta, Y, n, jl0_cta, n_loc, q, i_begin,
+                         int(i_end - i_begin < CH ? i_end - i_begin : CH), vec_th, vec);
+  for (int64_t ck = 0; ck < nchunks; ++ck) {
+    const int64_t c0 = i_begin + ck * CH;
+    const int rows = int(i_end - c0 < CH ? i_end - c0 : CH);
+    const int b = int(ck & 1);
+    if (ck + 1 < nchunks) {
+      const int64_t c1 = c0 + CH;
+      mds_stage<T, QS, JB>(th_buf[b ^ 1], y_buf[b ^ 1], theta, Y, n, jl0_cta, n_loc, q, c1,
+                           int(i_end - c1 < CH ? i_end - c1 : CH), vec_th, vec);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const T* th_s = th_buf[b];
+    const T* y_s = y_buf[b] + wid * JB * CH;
+    T st_chunk = T(0);
+    for (int rb = lane; rb < rows; rb += 64) {
+      // two rows per lane per iteration (rb, rb + 32): independent dependency chains
 #pragma unroll
-    for (int c = 0; c < JB; ++c) {
-      if (!live[c]) continue;
-      const int64_t jl = jl0 + c;
-      const double y = double(Y[jl * n + i]);
-      if (i == lo + jl) {  // diagonal: d_jj = 0 exactly (solvers.py:240-241), z_jj = y/inf = 0
-        stress = fma(y, y, stress);
-        continue;
-      }
-      double g = 0.0;
+      for (int h = 0; h < 2; ++h) {
+        const int rr = rb + 32 * h;
+        if (rr >= rows) break;
+        const int64_t i = c0 + rr;
+        T ti[QM];
+        const uint4* src = reinterpret_cast<const uint4*>(th_s + rr * QS);
 #pragma unroll
-      for (int k = 0; k < QM; ++k) g = fma(ti[k], tj[c][k], g);
-      // solvers.py:246: sqrt(max(dr + dc - 2g, 0)) evaluated in the storage type
-      const T d2 = T(ni) + T(nj[c]) - T(2.0) * T(g);
-      T d = sqrt(d2 > T(0) ? d2 : T(0));
-      const double e = y - double(d);
-      stress = fma(e, e, stress);
-      if (d == T(0)) {
-        zeros += 1.0;
-        if (perturb) d = T(1e-10);  // solvers.py:296
-      }
-      if (mode == 0) {
-        const T z = T(y) / d;  // solvers.py:297
-        zs[c] += double(z);
-        const double wz = double(T(1) - z);  // solvers.py:299
+        for (int v = 0; v < QM / VW; ++v) {
+          const uint4 w = src[v];
+          const T* wv = reinterpret_cast<const T*>(&w);
 #pragma unroll
-        for (int k = 0; k < QM; ++k) Tacc[c][k] = fma(ti[k], wz, Tacc[c][k]);
+          for (int u = 0; u < VW; ++u) ti[v * VW + u] = wv[u];
+        }
+        T ni = T(0);
+#pragma unroll
+        for (int k = 0; k < QM; ++k) ni = fma(ti[k], ti[k], ni);
+#pragma unroll
+        for (int c = 0; c < JB; ++c) {
+          if (!live[c]) continue;
+          const int64_t jl = jl0 + c;
+          const T y = y_s[c * CH + rr];
+          if (i == lo + jl) {  // diagonal: d_jj = 0 exactly (solvers.py:240-241), z_jj = y/inf = 0
+            st_chunk = fma(y, y, st_chunk);
+            continue;
+          }
+          // g = theta_i . theta_j with four independent partial sums
+          T g4[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+          for (int k = 0; k < QM; ++k) g4[k & 3] = fma(ti[k], tj[c][k], g4[k & 3]);
+          const T g = (g4[0] + g4[1]) + (g4[2] + g4[3]);
+          // solvers.py:246: sqrt(max(dr + dc - 2g, 0))
+          const T d2 = (ni + nj[c]) - T(2) * g;
+          T d, z;
+          if constexpr (sizeof(T) == 4) {
+            // one MUFU per pair: r = rsqrt(d2) refined by a Newton step; d = d2 r, z = y r
+            if (d2 > T(0)) {
+              float rs = rsqrtf(d2);
+              rs = rs * fmaf(-0.5f * d2 * rs, rs, 1.5f);
+              d = d2 * rs;
+              z = y * rs;
+            } else {
+              d = T(0);
+              z = perturb ? y * T(1e10) : y / T(0);
+            }
+          } else {
+            d = sqrt(d2 > T(0) ? d2 : T(0));
+            z = T(0);
+          }
+          const T e = y - d;
+          st_chunk = fma(e, e, st_chunk);
+          if (d == T(0)) {
+            zeros += 1.0;
+            if (perturb) d = T(1e-10);  // solvers.py:296
+          }
+          if (mode == 0) {
+            if constexpr (sizeof(T) == 8) z = y / d;  // solvers.py:297
+            zs[c] += z;
+            const T wz = T(1) - z;  // solvers.py:299
+#pragma unroll
+            for (int k = 0; k < QM; ++k) Tacc[c][k] = fma(ti[k], wz, Tacc[c][k]);
+          }
+        }
       }
     }
+    stress += double(st_chunk);
+    __syncthreads();  // buffer b is refilled two chunks later
   }
   // per-warp column partials
   if (mode == 0) {
     const int s = blockIdx.y;
 #pragma unroll
     for (int c = 0; c < JB; ++c) {
-      const double zsum = warp_sum(zs[c]);
+      const double zsum = warp_sum(double(zs[c]));
       double tk[QM];
 #pragma unroll
-      for (int k = 0; k < QM; ++k) tk[k] = warp_sum(Tacc[c][k]);
+      for (int k = 0; k < QM; ++k) tk[k] = warp_sum(double(Tacc[c][k]));
       const int64_t jl = jl0 + c;
       if (lane == 0 && live[c]) {
         zsum_part[int64_t(s) * n_loc + jl] = zsum;
@@ -129,29 +271,35 @@ mds_pass_kernel(const T* __restrict__ Y, const T* __restrict__ theta, int64_t n,
   }
 }
 
-static int mds_qm(int q) { return q <= 4 ? 4 : q <= 8 ? 8 : q <= 16 ? 16 : q <= 24 ? 24 : q <= 32 ? 32 : 64; }
+// columns per warp: keeps theta_j, the T partials and theta_i in registers
+static constexpr int mds_jb(int qm, int esize) {
+  return esize == 4 ? (qm <= 8 ? 8 : qm <= 12 ? 6 : qm <= 16 ? 4 : qm <= 20 ? 3 : qm <= 32 ? 2 : 1)
+                    : (qm <= 8 ? 4 : qm <= 16 ? 2 : 1);
+}
+
+static int mds_qm(int q) { return q <= 4 ? 4 : q <= 8 ? 8 : q <= 12 ? 12 : q <= 16 ? 16 : q <= 20 ? 20 : q <= 24 ? 24 : q <= 32 ? 32 : 64; }
 
 struct MdsGrid {
   int colblocks, segs;
   int64_t rows_per_seg;
 };
 
-static MdsGrid mds_grid(int64_t n, int64_t n_loc, int q) {
-  const int jb = mds_qm(q) <= 16 ? 2 : 1;
+static MdsGrid mds_grid(int64_t n, int64_t n_loc, int q, int dtype) {
+  const int jb = mds_jb(mds_qm(q), dtype == BS_F64 ? 8 : 4);
   MdsGrid g;
   g.colblocks = int(std::max<int64_t>(1, ceil_div(n_loc, int64_t(MDS_WARPS) * jb)));
   const int64_t want = int64_t(num_sms()) * 4;
   int64_t segs = std::max<int64_t>(1, ceil_div(want, g.colblocks));
   segs = std::min<int64_t>(segs, std::max<int64_t>(1, n / 256));
   segs = std::min<int64_t>(segs, 64);
-  g.rows_per_seg = ceil_div(std::max<int64_t>(n, 1), segs);
+  g.rows_per_seg = ceil_div(ceil_div(std::max<int64_t>(n, 1), segs), 128) * 128;
   g.segs = int(ceil_div(std::max<int64_t>(n, 1), g.rows_per_seg));
   return g;
 }
 
 extern "C" int64_t bs_mds_pass_workspace(int dtype, int64_t n, int64_t n_loc, int q) {
   (void)dtype;
-  MdsGrid g = mds_grid(n, n_loc, q);
+  MdsGrid g = mds_grid(n, n_loc, q, dtype);
   return ws_bytes<unsigned int>(1) + ws_bytes<double>(2 * int64_t(g.colblocks) * g.segs) +
          ws_bytes<double>(int64_t(g.segs) * n_loc) + ws_bytes<double>(int64_t(g.segs) * n_loc * q) +
          ws_bytes<int64_t>(2);
@@ -161,9 +309,18 @@ template <typename T, int QM>
 static void launch_pass(const T* Y, const T* th, int64_t n, int64_t lo, int64_t n_loc, int q, int perturb,
                         int mode, const MdsGrid& g, double* zp, double* tp, double* parts, unsigned int* ctr,
                         double* red, cudaStream_t st) {
-  constexpr int JB = QM <= 16 ? 2 : 1;
+  constexpr int JB = mds_jb(QM, int(sizeof(T)));
   dim3 grid(unsigned(g.colblocks), unsigned(g.segs));
-  mds_pass_kernel<T, QM, JB><<<grid, MDS_THREADS, 0, st>>>(Y, th, n, lo, n_loc, q, perturb, mode,
+  constexpr int VW = 16 / int(sizeof(T));
+  constexpr int QS0 = (QM + VW - 1) / VW * VW;
+  constexpr int QS = ((QS0 / VW) % 2 == 0) ? QS0 + VW : QS0;
+  constexpr int CH = MdsChunk<T>::CH;
+  const int smem = int(sizeof(T)) * (2 * CH * QS + 2 * MDS_WARPS * JB * CH);
+  static std::once_flag once;
+  std::call_once(once, [smem] {
+    cudaFuncSetAttribute(mds_pass_kernel<T, QM, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
+  mds_pass_kernel<T, QM, JB><<<grid, MDS_THREADS, smem, st>>>(Y, th, n, lo, n_loc, q, perturb, mode,
                                                            g.rows_per_seg, zp, tp, parts, ctr, red);
 }
 
@@ -174,7 +331,9 @@ static void dispatch_pass(const T* Y, const T* th, int64_t n, int64_t lo, int64_
   switch (mds_qm(q)) {
     case 4: launch_pass<T, 4>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
     case 8: launch_pass<T, 8>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
+    case 12: launch_pass<T, 12>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
     case 16: launch_pass<T, 16>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
+    case 20: launch_pass<T, 20>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
     case 24: launch_pass<T, 24>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
     case 32: launch_pass<T, 32>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
     default: launch_pass<T, 64>(Y, th, n, lo, n_loc, q, perturb, mode, g, zp, tp, parts, ctr, red, st); break;
@@ -213,7 +372,7 @@ extern "C" int bs_mds_pass(const void* Y, const void* theta_full, int dtype, int
   if (n_loc == 0 || n == 0)
     return cudaMemsetAsync(red, 0, 2 * sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
   Workspace ws(work, work_bytes);
-  MdsGrid g = mds_grid(n, n_loc, q);
+  MdsGrid g = mds_grid(n, n_loc, q, dtype);
   unsigned int* ctr = ws.take<unsigned int>(1);
   double* parts = ws.take<double>(2 * int64_t(g.colblocks) * g.segs);
   double* zp = ws.take<double>(int64_t(g.segs) * n_loc);
