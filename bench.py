@@ -284,6 +284,8 @@ def _run_b200(args, wl):
             out["e2e"] = {"value": None, "unit": "it/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
     if comm.rank == 0:
         print(json.dumps(out), flush=True)
+    comm.barrier()
+    comm.close()
 
 
 def _arith_dtype(wl):

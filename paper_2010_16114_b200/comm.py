@@ -485,7 +485,12 @@ class _TorchCommunicator(Communicator):
         self._dist = dist
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group(backend=backend_name)
+            kw = {}
+            if backend_name == "nccl":
+                local = int(os.environ.get("LOCAL_RANK", "0"))
+                torch.cuda.set_device(local)
+                kw["device_id"] = torch.device("cuda", local)
+            dist.init_process_group(backend=backend_name, **kw)
         self.rank = dist.get_rank()
         self.size = dist.get_world_size()
         self.backend = dist.get_backend()
@@ -499,7 +504,8 @@ class _TorchCommunicator(Communicator):
                      ReduceOp.MAX: dist.ReduceOp.MAX, ReduceOp.MIN: dist.ReduceOp.MIN}
 
     def close(self):
-        pass
+        if self._dist.is_initialized():
+            self._dist.destroy_process_group()
 
     def _to_dev(self, buf):
         """(device flat tensor, writeback fn)."""

@@ -1,0 +1,76 @@
+"""Multi-GPU parity under torchrun (one process per GPU, NCCL).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/nccl_parity.py
+
+Runs NMF (both algorithms, float32 tcgen05 path and float64), MDS and Cox through
+the 'nccl' Communicator on column-sharded data and checks every rank's result
+against the CPU oracle.  Exits non-zero on a mismatch.
+"""
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import paper_2010_16114_b200 as bs  # noqa: E402
+from oracle import blockstat_oracle as orc  # noqa: E402
+
+
+def check(name, got, want, tol):
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    err = np.abs(got - want).max() / max(np.abs(want).max(), 1e-300)
+    ok = err <= tol
+    print(f"[rank {os.environ.get('RANK')}] {name}: rel err {err:.2e} (tol {tol:.0e}) {'OK' if ok else 'FAIL'}",
+          flush=True)
+    return ok
+
+
+def main():
+    comm = bs.init("nccl")
+    ok = True
+    for dt, tol, (m, n, r) in ((np.float64, 1e-9, (300, 257, 7)), (np.float32, 2e-5, (2048, 1501, 60))):
+        x = orc.rand_fill_common((m, n), 5, dt)
+        vt0, w0 = orc.nmf_init(x, r, 6)
+        for algo, fn, ofn in ((0, bs.nmf_multiplicative, orc.nmf_multiplicative), (1, bs.nmf_apg, orc.nmf_apg)):
+            xd = bs.empty((m, n), comm, dt)
+            bs.rand_fill(xd, seed=5, common_init=True)
+            st = bs.nmf_init(xd, r, seed=6)
+            fn(st, 15)
+            ovt, ow, otr = ofn(x.astype(np.float64), vt0.astype(np.float64), w0.astype(np.float64), 15)
+            ok &= check(f"nmf algo={algo} {np.dtype(dt).name} trace", st.trace, otr, tol)
+            ok &= check(f"nmf algo={algo} {np.dtype(dt).name} W", bs.gather_full(st.W), ow, tol * 10)
+    # MDS
+    pts = orc.rand_fill_common((6, 301), 7, np.float64)
+    y = orc.pairwise_euclidean(pts)
+    th0 = orc.mds_init(y, 3, 8)
+    yd = bs.empty((301, 301), comm)
+    pd = bs.empty((6, 301), comm)
+    bs.rand_fill(pd, seed=7, common_init=True)
+    bs.pairwise_euclidean(yd, pd)
+    st = bs.mds_init(yd, 3, seed=8)
+    bs.mds_fit(st, 12)
+    oth, otr = orc.mds_fit(y, th0, 12)
+    ok &= check("mds trace", st.trace, otr, 1e-9)
+    ok &= check("mds theta", bs.gather_full(st.theta), oth, 1e-8)
+    # Cox (float64 and int8 storage)
+    xs, ys, ds = orc.survival_data(9, 500, 301, np.r_[0.4, -0.3, np.zeros(299)])
+    sig = 0.5 / np.linalg.norm(xs, 2) ** 2
+    xd = bs.distribute(xs if comm.rank == 0 else None, comm)
+    st = bs.cox_init(xd, ys, ds, lam=0.01, sigma=sig)
+    bs.cox_fit(st, 20)
+    ob, og, otr = orc.cox_fit(xs, ds, np.arange(500), 0.01, sig, 20)
+    ok &= check("cox trace", st.trace, otr, 1e-10)
+    ok &= check("cox beta", bs.gather_full(st.beta), ob, 1e-8)
+    ok &= check("cox sigma (power iteration)", bs.opnorm(xd), orc.opnorm_l2_power(xs), 1e-12)
+    comm.barrier()
+    import torch.distributed as dist
+
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
