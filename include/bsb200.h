@@ -124,6 +124,15 @@ int bs_nmf_wxt(const void* X, const void* W, int dtype, int64_t m,
                int64_t n_loc, int r, void* P, void* work, int64_t work_bytes,
                void* stream);
 
+/* scn b fused with _nmf_check (solvers.py:139-141, 147): the same X pass also
+ * yields stats_dev = {min, sum X^2} (float64; with padded tcgen05 tiles the min
+ * is min(min X, 0), enough for the nonnegativity check).  The solver uses it for
+ * the first iteration of every call instead of a separate bs_nmf_scan pass. */
+int64_t bs_nmf_wxt_scan_workspace(int dtype, int64_t m, int64_t n_loc, int r);
+int bs_nmf_wxt_scan(const void* X, const void* W, int dtype, int64_t m,
+                    int64_t n_loc, int r, void* P, double* stats_dev,
+                    void* work, int64_t work_bytes, void* stream);
+
 /* Vt half-step, fused (solvers.py:151-156 MU, 172-178 APG):
  *   WWtVt = WWt Vt_loc (scn j), sigma = 1/(2 sum WWt^2 + eps) (APG),
  *   Vt <- Vt*WXt/(WWtVt+eps) | max(0, Vt - sigma (WWtVt - WXt)),

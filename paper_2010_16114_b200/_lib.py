@@ -51,6 +51,8 @@ SIGNATURES = {
     "bs_nmf_scan": (_i, [_p, _i, _i64, _p, _p, _i64, _p]),
     "bs_nmf_wxt_workspace": (_i64, [_i, _i64, _i64, _i]),
     "bs_nmf_wxt": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _i64, _p]),
+    "bs_nmf_wxt_scan_workspace": (_i64, [_i, _i64, _i64, _i]),
+    "bs_nmf_wxt_scan": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _p, _i64, _p]),
     "bs_nmf_vt_step_workspace": (_i64, [_i, _i64]),
     "bs_nmf_vt_step": (_i, [_i, _p, _p, _p, _i, _i, _i64, _d, _p, _p, _p, _i64, _p]),
     "bs_nmf_w_step_workspace": (_i64, [_i, _i64, _i64, _i]),

@@ -46,6 +46,9 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // Most split-K slabs the tcgen05 GEMMs write (nmf_tc.cu).
 constexpr int TC_MAX_SPLITS = 16;
 
+// out = {min, sum} folded in order from np (min, sum) partial pairs (nmf.cu).
+void launch_fold_minsq(const double* parts, int np, double* out, cudaStream_t st);
+
 // dst[e] = sum_s parts[s*len + e], slabs folded in order (nmf.cu).
 void launch_sum_slabs_f32(const float* parts, int S, int64_t len, float* dst, cudaStream_t st);
 
@@ -61,6 +64,13 @@ struct Workspace {
     if (base == nullptr || off + bytes > size) return Workspace(nullptr, 0);
     used = off + bytes;
     return Workspace(base + off, bytes);
+  }
+  // Everything not yet handed out, as its own workspace.
+  Workspace rest() {
+    int64_t off = (used + 255) & ~int64_t(255);
+    if (base == nullptr || off >= size) return Workspace(nullptr, 0);
+    used = size;
+    return Workspace(base + off, size - off);
   }
   template <typename T>
   T* take(int64_t count) {
@@ -133,11 +143,54 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
                : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
+}
+
+// Grid-stride walk over x[0..count) calling f(double) per element: 16-byte
+// streaming loads, four in flight per thread, scalar head/tail.  Every element is
+// visited exactly once by exactly one thread; the per-thread order is fixed for
+// a fixed grid, so folds built on it are deterministic.
+template <typename T, typename F>
+__device__ __forceinline__ void stream_elems(const T* __restrict__ x, int64_t count, F&& f) {
+  constexpr int V = 16 / int(sizeof(T));
+  const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  // scalar head up to 16-byte alignment
+  const int64_t mis = (reinterpret_cast<uintptr_t>(x) & 15) / sizeof(T);
+  const int64_t head = mis ? (count < V - mis ? count : V - mis) : 0;
+  for (int64_t i = tid; i < head; i += nth) f(double(x[i]));
+  const T* xa = x + head;
+  const int64_t nvec = (count - head) / V;
+  const uint4* xv = reinterpret_cast<const uint4*>(xa);
+  int64_t v = tid;
+  for (; v + 3 * nth < nvec; v += 4 * nth) {
+    uint4 w[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) w[u] = ld_stream(xv + v + u * nth);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T* e = reinterpret_cast<const T*>(&w[u]);
+#pragma unroll
+      for (int k = 0; k < V; ++k) f(double(e[k]));
+    }
+  }
+  for (; v < nvec; v += nth) {
+    const uint4 w = ld_stream(xv + v);
+    const T* e = reinterpret_cast<const T*>(&w);
+#pragma unroll
+    for (int k = 0; k < V; ++k) f(double(e[k]));
+  }
+  for (int64_t i = head + nvec * V + tid; i < count; i += nth) f(double(x[i]));
 }
 
 // ReduceOp semantics in float64 (comm.py:60-65 ufuncs; NaN-propagating like np.min/np.max).

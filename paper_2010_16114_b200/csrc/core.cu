@@ -132,11 +132,6 @@ extern "C" int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t fi
 // reduce_all (distarray.py:335-348) — deterministic two-level fold in float64.
 // ---------------------------------------------------------------------------
 
-template <typename T>
-__device__ __forceinline__ double load_as_double(const T* p, int64_t i) {
-  return double(p[i]);
-}
-
 constexpr int RED_THREADS = 256;
 
 template <typename T>
@@ -145,9 +140,7 @@ reduce_kernel(const T* __restrict__ x, int64_t count, int op, int transform,
               double* __restrict__ parts, unsigned int* counter, double* out) {
   __shared__ double sh[32];
   double acc = rop_neutral(op);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
-       i += int64_t(gridDim.x) * blockDim.x)
-    acc = rop_apply(op, acc, rtransform(transform, load_as_double(x, i)));
+  stream_elems(x, count, [&](double v) { acc = rop_apply(op, acc, rtransform(transform, v)); });
   // block tree in fixed order
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll

@@ -26,7 +26,7 @@ int launch_gram(const void* A, int dtype, int r, int64_t ncols, double* G, Works
                 cudaStream_t st);
 // tcgen05 path (nmf_tc.cu); returns BS_EINVAL when the shape is not supported.
 int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, float* P, Workspace& ws,
-           cudaStream_t st, bool* used);
+           cudaStream_t st, bool* used, double* stats);
 int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, float* C, int cap_slabs,
            int* splits, Workspace& ws, cudaStream_t st, bool* used);
 int64_t tc_wxt_workspace(int64_t m, int64_t n_loc, int r);
@@ -45,12 +45,10 @@ scan_kernel(const T* __restrict__ x, int64_t count, double* __restrict__ parts,
             unsigned int* counter, double* out) {
   __shared__ double shm[32], shs[32];
   double mn = CUDART_INF, sq = 0.0;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const double v = double(x[i]);
+  stream_elems(x, count, [&](double v) {
     mn = rop_apply(BS_MIN, mn, v);
     sq = fma(v, v, sq);
-  }
+  });
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -244,7 +242,23 @@ __global__ void sum_slabs_kernel(const T* __restrict__ parts, int S, int64_t len
   }
 }
 
+__global__ void fold_minsq_kernel(const double* __restrict__ parts, int np, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double a = parts[0], b = parts[1];
+    for (int k = 1; k < np; ++k) {
+      a = rop_apply(BS_MIN, a, parts[2 * k]);
+      b += parts[2 * k + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
 namespace bs {
+void launch_fold_minsq(const double* parts, int np, double* out, cudaStream_t st) {
+  fold_minsq_kernel<<<1, 32, 0, st>>>(parts, np, out);
+}
+
 void launch_sum_slabs_f32(const float* parts, int S, int64_t len, float* dst, cudaStream_t st) {
   sum_slabs_kernel<float><<<int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(len, 256), 4096))), 256, 0, st>>>(
       parts, S, len, dst);
@@ -296,24 +310,58 @@ extern "C" int64_t bs_nmf_wxt_workspace(int dtype, int64_t m, int64_t n_loc, int
   return core;
 }
 
+static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
+                        double* stats, void* work, int64_t work_bytes, void* stream);
+
 extern "C" int bs_nmf_wxt(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r,
                           void* P, void* work, int64_t work_bytes, void* stream) {
+  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, nullptr, work, work_bytes, stream);
+}
+
+extern "C" int64_t bs_nmf_wxt_scan_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
+  return bs_nmf_wxt_workspace(dtype, m, n_loc, r) + ws_bytes<char>(64 * 1024) + 512;
+}
+
+extern "C" int bs_nmf_wxt_scan(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
+                               double* stats_dev, void* work, int64_t work_bytes, void* stream) {
+  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, stats_dev, work, work_bytes, stream);
+}
+
+static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
+                        double* stats, void* work, int64_t work_bytes, void* stream) {
   clear_error();
   if (r < 1 || r > MAX_R || m < 0 || n_loc < 0) {
     set_error("bs_nmf_wxt: bad shape m=%lld n_loc=%lld r=%d", (long long)m, (long long)n_loc, r);
     return BS_EINVAL;
   }
   cudaStream_t st = as_stream(stream);
+  Workspace all(work, work_bytes);
+  Workspace sws(nullptr, 0);
+  if (stats) sws = all.split(ws_bytes<char>(64 * 1024));  // the scan's slice (fixed counter offset)
+  Workspace ws = all.rest();
+  bool scanned = false;
+  auto plain_scan = [&]() -> int {
+    scanned = true;
+    return bs_nmf_scan(X, dtype, m * n_loc, stats, sws.base, sws.size, stream);
+  };
+  if (stats && (m == 0 || n_loc == 0 || dtype != BS_F32)) {
+    const int rc = plain_scan();
+    if (rc != BS_OK) return rc;
+  }
   if (m == 0) return BS_OK;
   if (n_loc == 0) {
     return cudaMemsetAsync(P, 0, size_t(m) * r * dsize(dtype), st) == cudaSuccess ? BS_OK : BS_ECUDA;
   }
-  Workspace ws(work, work_bytes);
   if (dtype == BS_F32) {
     bool used = false;
     int rc = tc_wxt(static_cast<const float*>(X), static_cast<const float*>(W), m, n_loc, r,
-                    static_cast<float*>(P), ws, st, &used);
-    if (used || rc != BS_OK) return rc;
+                    static_cast<float*>(P), ws, st, &used, scanned ? nullptr : stats);
+    if (rc != BS_OK) return rc;
+    if (used) return BS_OK;
+    if (stats && !scanned) {  // tcgen05 path not taken: plain scan
+      rc = plain_scan();
+      if (rc != BS_OK) return rc;
+    }
   }
   const int S = wxt_splits(m, n_loc);
   const int64_t cps = ceil_div(ceil_div(n_loc, S), 32) * 32;

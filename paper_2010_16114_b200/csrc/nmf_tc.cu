@@ -254,7 +254,8 @@ struct TcCfg {
 template <bool A_MN, int NP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int K, int r,
-               int tiles, int kb_per_split, int units, int G, float* __restrict__ out, int64_t slab, int mode) {
+               int tiles, int kb_per_split, int units, int G, float* __restrict__ out, int64_t slab, int mode,
+               double* __restrict__ stats_part) {
   using C = TcCfg<NP>;
   constexpr int RS = C::RSTAGES, CS = C::CSTAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -433,6 +434,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int row_in_tile = q * 32 + lane;
     const uint32_t lane_addr = uint32_t(q * 32) << 16;
     uint32_t j = 0;  // CTA-local block sequence number
+    float xmin = CUDART_INF_F;
+    double xsq = 0.0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int split = u / tiles;
       const int kb0 = split * kb_per_split;
@@ -464,6 +467,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             for (int c = 0; c < 8; ++c) {
               const uint4 v = ld_shared_v4(rowb + (uint32_t(c ^ (row_in_tile & 7)) << 4));
               hi[4 * c] = v.x; hi[4 * c + 1] = v.y; hi[4 * c + 2] = v.z; hi[4 * c + 3] = v.w;
+            }
+          }
+          if (stats_part) {  // _nmf_check + ||X||^2 ride on this pass (solvers.py:139-141)
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              const float x = __uint_as_float(hi[k]);
+              xmin = fminf(xmin, x);
+              xsq = fma(double(x), double(x), xsq);
             }
           }
 #pragma unroll
@@ -501,6 +512,26 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         tc_fence_before();
         mbar_arrive(raw_empty(rst));  // the raw stage is free again: TMA can refill it
         mbar_arrive(conv_full(cst));
+      }
+    }
+    if (stats_part) {
+      // deterministic CTA fold of the converters' (min, sum x^2): warps in order
+      __shared__ float smin[8];
+      __shared__ double ssq[8];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        xmin = fminf(xmin, __shfl_xor_sync(0xffffffffu, xmin, o));
+        xsq += __shfl_xor_sync(0xffffffffu, xsq, o);
+      }
+      const int cw = warp - 6;
+      if (lane == 0) { smin[cw] = xmin; ssq[cw] = xsq; }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (cw == 0 && lane == 0) {
+        float a = smin[0];
+        double b = ssq[0];
+        for (int w2 = 1; w2 < 8; ++w2) { a = fminf(a, smin[w2]); b += ssq[w2]; }
+        stats_part[2 * blockIdx.x] = double(a);
+        stats_part[2 * blockIdx.x + 1] = b;
       }
     }
   }
@@ -561,7 +592,7 @@ bool tc_enabled() {
 
 template <bool A_MN, int NP>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r, int splits, float* out, int64_t slab,
-              cudaStream_t st) {
+              cudaStream_t st, double* stats_part = nullptr, int* grid_out = nullptr) {
   using C = TcCfg<NP>;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -585,7 +616,9 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r,
     const char* e = getenv("BS_TC_MODE");
     mode = e ? atoi(e) : 0;
   });
-  tc_gemm_kernel<A_MN, NP><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, M, K, r, tiles, kb_per, units, group, out, slab, mode);
+  if (grid_out) *grid_out = grid;
+  tc_gemm_kernel<A_MN, NP><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, M, K, r, tiles, kb_per, units, group, out, slab, mode,
+                                                               stats_part);
   return real_splits;
 }
 
@@ -612,7 +645,7 @@ namespace bs {
 
 int64_t tc_wxt_workspace(int64_t m, int64_t n_loc, int r) {
   (void)n_loc;
-  return ws_bytes<float>(int64_t(TC_MAX_SPLITS) * m * r);
+  return ws_bytes<float>(int64_t(TC_MAX_SPLITS) * m * r) + ws_bytes<double>(2 * int64_t(num_sms()));
 }
 int64_t tc_vtx_workspace(int64_t m, int64_t n_loc, int r) {
   (void)m; (void)n_loc; (void)r;
@@ -621,15 +654,16 @@ int64_t tc_vtx_workspace(int64_t m, int64_t n_loc, int r) {
 
 #define BS_TC_DISPATCH(AMN)                                                                            \
   switch (np) {                                                                                        \
-    case 32: S = launch_tc<AMN, 32>(ta, tb, M, K, r, nsplit, out, slab, st); break;                    \
-    case 64: S = launch_tc<AMN, 64>(ta, tb, M, K, r, nsplit, out, slab, st); break;                    \
-    case 96: S = launch_tc<AMN, 96>(ta, tb, M, K, r, nsplit, out, slab, st); break;                    \
-    default: S = launch_tc<AMN, 128>(ta, tb, M, K, r, nsplit, out, slab, st); break;                   \
+    case 32: S = launch_tc<AMN, 32>(ta, tb, M, K, r, nsplit, out, slab, st, sp, &gsz); break;          \
+    case 64: S = launch_tc<AMN, 64>(ta, tb, M, K, r, nsplit, out, slab, st, sp, &gsz); break;          \
+    case 96: S = launch_tc<AMN, 96>(ta, tb, M, K, r, nsplit, out, slab, st, sp, &gsz); break;          \
+    default: S = launch_tc<AMN, 128>(ta, tb, M, K, r, nsplit, out, slab, st, sp, &gsz); break;         \
   }
 
 // scn b: writes S partial slabs of P (r x m) into the workspace and folds them into P.
+// stats (nullable): {min, sum x^2} of X gathered during the same pass (float64, device).
 int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, float* P, Workspace& ws, cudaStream_t st,
-           bool* used) {
+           bool* used, double* stats) {
   *used = false;
   const int np = pick_np(r);
   if (!tc_enabled() || np == 0 || m % 4 || r % 4 || m > INT32_MAX || n_loc > INT32_MAX || m < 128 || n_loc < 32 ||
@@ -640,6 +674,12 @@ int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, floa
   if (!make_map(&tb, W, uint64_t(r), uint64_t(n_loc), 32, 32, true)) return BS_OK;
   const int M = int(m), K = int(n_loc);
   const int nsplit = tc_splits(M, K);
+  double* sp = nullptr;
+  int gsz = 0;
+  if (stats) {
+    sp = ws.take<double>(2 * int64_t(num_sms()));
+    if (!sp) { set_error("tc_wxt: workspace too small"); return BS_EWORK; }
+  }
   float* out = P;
   float* slabs = nullptr;
   if (nsplit > 1) {
@@ -652,6 +692,11 @@ int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, floa
   BS_TC_DISPATCH(true)
   int rc = check_launch("tc_wxt");
   if (rc != BS_OK) return rc;
+  if (stats) {
+    launch_fold_minsq(sp, gsz, stats, st);
+    rc = check_launch("tc_wxt stats");
+    if (rc != BS_OK) return rc;
+  }
   if (S > 1) {
     launch_sum_slabs_f32(slabs, S, m * r, P, st);
     rc = check_launch("tc_wxt fold");
@@ -679,6 +724,8 @@ int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, flo
   const int64_t slab = n_loc * r;
   int S = 1;
   const int nsplit = want;
+  double* sp = nullptr;
+  int gsz = 0;
   BS_TC_DISPATCH(false)
   int rc = check_launch("tc_vtx");
   if (rc != BS_OK) return rc;

@@ -207,12 +207,19 @@ def _gather_factor(a, out):
 def _nmf_check_and_norm(s):
     """_nmf_check (solvers.py:139-141) fused with ||X||^2 for the objective."""
     x = s.X
-    comm = x.comm
     flat = _flat_local(x)
     scan = s._dev["scan"]
     wp, wn = s._work.args("scan", 16 * 4096)
     _lib.call("bs_nmf_scan", _lib.ptr(flat), _lib.dtype_code(flat.dtype), flat.numel(), _lib.ptr(scan), wp, wn,
               _lib.stream_ptr())
+    _nmf_check_result(s)
+
+
+def _nmf_check_result(s):
+    """Reduces the (min, ||X||^2) scan over ranks and raises like solvers.py:139-141."""
+    x = s.X
+    comm = x.comm
+    scan = s._dev["scan"]
     if comm.size > 1:
         mn = scan[0:1].clone()
         comm.allreduce(mn, ReduceOp.MIN)
@@ -235,8 +242,8 @@ def _nmf_run(s, iters, trace_every, algo):
     code = _lib.dtype_code(x.dtype)
     m_loc = s.Vt.local.shape[1]
     n_loc = x.local.shape[1]
-    _nmf_check_and_norm(s)
     if iters <= 0:
+        _nmf_check_and_norm(s)
         return s
     st = _lib.stream_ptr()
     dev = comm.device
@@ -265,12 +272,20 @@ def _nmf_run(s, iters, trace_every, algo):
     WXt_loc = _flat_local(s.WXt)
     trace_dev = _dev_f64(iters, dev)
     xp, xn = s._work.args("wxt", _lib.query("bs_nmf_wxt_workspace", code, m, n_loc, r))
+    sp, sn = s._work.args("wxt_scan", _lib.query("bs_nmf_wxt_scan_workspace", code, m, n_loc, r))
+    scan = s._dev["scan"]
     vp, vn = s._work.args("vt", _lib.query("bs_nmf_vt_step_workspace", r, m_loc))
     wp, wn = s._work.args("w", _lib.query("bs_nmf_w_step_workspace", code, m, n_loc, r))
     eps = float(s.eps)
     for it in range(iters):
-        # WXt = W X^T (scn b) and its reduce-scatter (distlinalg.py:246-252)
-        _lib.call("bs_nmf_wxt", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), xp, xn, st)
+        # WXt = W X^T (scn b) and its reduce-scatter (distlinalg.py:246-252).  The first
+        # iteration's pass also performs the call's _nmf_check and ||X||^2 (solvers.py:147).
+        if it == 0:
+            _lib.call("bs_nmf_wxt_scan", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), _lib.ptr(scan),
+                      sp, sn, st)
+            _nmf_check_result(s)
+        else:
+            _lib.call("bs_nmf_wxt", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), xp, xn, st)
         if comm.size > 1:
             comm.reduce_scatterv(P[:r * m], WXt_loc, mcounts)
         # Vt half-step (solvers.py:152-156 / 173-176)
