@@ -269,7 +269,7 @@ def _run_b200(args, wl):
                                "exceed the 126 MB L2"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(dom), "bytes_per_launch": bytes_launch,
+                     "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
                      "avg_launch_ms": avg_ms,
                      "share_of_step": tot[dom] / ms},
         "gpu_launches": int(launches),
@@ -292,11 +292,12 @@ def _arith_dtype(wl):
     return {"float32": "f32", "float64": "f64", "int8": "int8->f32"}[wl["dtype"]]
 
 
-def _traffic(kernel):
+def _traffic(wl, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu capture for this
+    workload at N=1 (profiles/ncu_traffic.json), else None."""
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
-        d = json.loads(p.read_text())
-        v = d.get(kernel)
+        v = json.loads(p.read_text()).get(wl["key"], {}).get(kernel)
         return None if v is None else float(v)
     return None
 
@@ -431,7 +432,7 @@ def main(argv=None):
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    wl = WORKLOADS[args.workload]
+    wl = dict(WORKLOADS[args.workload], key=args.workload)
     if args.impl == "reference":
         _run_reference(args, wl)
     else:

@@ -275,10 +275,173 @@ static int pick_splits(int64_t tiles, int64_t K, int64_t min_k) {
   return int(std::min<int64_t>(s, 64));
 }
 
+// ---------------------------------------------------------------------------
+// Register-tiled CUDA-core GEMM used for float64 (no tcgen05 kind exists) and for
+// shapes the tcgen05 path does not take.  One CTA of 128 threads computes a
+// 128 x RP output tile (M rows x r padded): thread (tx, ty) owns TM = 8 rows x
+// TN = RP/8 columns, so every k step costs TM + TN operand loads (16-byte shared
+// loads) for TM*TN FMAs.  Tiles are double-buffered through registers.
+//   A_MN = true : scn b, A = X with M = i contiguous (tile rows kk are contiguous)
+//   A_MN = false: scn a, A = X with K = i contiguous (one X column per thread row)
+// ---------------------------------------------------------------------------
+
+// k-tile depth: keeps both double buffers under the 48 KB static shared limit
+template <typename T, int RP> struct CcCfg {
+  static constexpr int BK = sizeof(T) == 8 ? (RP >= 64 ? 8 : 16) : (RP >= 64 ? 16 : 32);
+};
+
+template <typename T, int RP, bool A_MN>
+__global__ void __launch_bounds__(128)
+cc_gemm_kernel(const T* __restrict__ X, const T* __restrict__ B, int64_t M, int64_t ldx, int r,
+               int64_t K, int64_t k_per_split, T* __restrict__ out) {
+  constexpr int BM = 128, BK = CcCfg<T, RP>::BK, TM = 8, TN = RP / 8, V = 16 / int(sizeof(T));
+  constexpr int PAD = V;  // keeps 16-byte alignment of the rows
+  __shared__ __align__(16) T As[2][BK][BM + PAD];
+  __shared__ __align__(16) T Bs[2][BK][RP];
+  const int tid = threadIdx.x, tx = tid & 7, ty = tid >> 3;
+  const int64_t m0 = int64_t(blockIdx.x) * BM;
+  const int64_t k_begin = int64_t(blockIdx.y) * k_per_split;
+  const int64_t k_end = min(K, k_begin + k_per_split);
+  // register staging of one tile
+  constexpr int A_PER = BM * BK / 128;          // elements per thread
+  constexpr int B_PER = (BK * RP + 127) / 128;
+  T ra[A_PER], rb[B_PER];
+  const bool vec_ok = (ldx % V) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  auto load_tile = [&](int64_t k0) {
+    if constexpr (A_MN) {
+      // rows kk of the tile are X[(k0+kk)*ldx + m0 .. +BM): V-wide vector loads
+#pragma unroll
+      for (int u = 0; u < A_PER / V; ++u) {
+        const int e = tid + 128 * u;  // vector index
+        const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
+        const int64_t k = k0 + kk, mrow = m0 + mv;
+        if (vec_ok && k < k_end && mrow + V <= M) {
+          if constexpr (sizeof(T) == 8) {
+            const double2 w = *reinterpret_cast<const double2*>(X + k * ldx + mrow);
+            ra[u * V] = w.x; ra[u * V + 1] = w.y;
+          } else {
+            const float4 w = *reinterpret_cast<const float4*>(X + k * ldx + mrow);
+            ra[u * V] = w.x; ra[u * V + 1] = w.y; ra[u * V + 2] = w.z; ra[u * V + 3] = w.w;
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) ra[u * V + v] = (k < k_end && mrow + v < M) ? X[k * ldx + mrow + v] : T(0);
+        }
+      }
+    } else {
+      // thread tid owns tile row m0+tid: X[(m0+tid)*ldx + k0 .. +BK)
+      const int64_t mrow = m0 + tid;
+      const T* src = X + mrow * ldx + k0;
+      if (mrow < M && k0 + A_PER <= k_end && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int u = 0; u < A_PER; u += V) {
+          if constexpr (sizeof(T) == 8) {
+            const double2 w = *reinterpret_cast<const double2*>(src + u);
+            ra[u] = w.x; ra[u + 1] = w.y;
+          } else {
+            const float4 w = *reinterpret_cast<const float4*>(src + u);
+            ra[u] = w.x; ra[u + 1] = w.y; ra[u + 2] = w.z; ra[u + 3] = w.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < A_PER; ++kk) {
+          const int64_t k = k0 + kk;
+          ra[kk] = (mrow < M && k < k_end) ? X[mrow * ldx + k] : T(0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER; ++u) {
+      const int e = tid + 128 * u;
+      const int kk = e / RP, c = e % RP;
+      const int64_t k = k0 + kk;
+      rb[u] = (e < BK * RP && k < k_end && c < r) ? B[k * r + c] : T(0);
+    }
+  };
+  auto store_tile = [&](int buf) {
+    if constexpr (A_MN) {
+#pragma unroll
+      for (int u = 0; u < A_PER / V; ++u) {
+        const int e = tid + 128 * u;
+        const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) As[buf][kk][mv + v] = ra[u * V + v];
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < A_PER; ++kk) As[buf][kk][tid] = ra[kk];
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER; ++u) {
+      const int e = tid + 128 * u;
+      if (e < BK * RP) Bs[buf][e / RP][e % RP] = rb[u];
+    }
+  };
+  T acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc[a][b] = T(0);
+  if (k_begin < k_end) {
+    load_tile(k_begin);
+    store_tile(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t k0 = k_begin; k0 < k_end; k0 += BK) {
+      const bool more = k0 + BK < k_end;
+      if (more) load_tile(k0 + BK);  // in flight while this tile is consumed
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        T a[TM], b[TN];
+#pragma unroll
+        for (int t = 0; t < TM; t += V) {
+          if constexpr (sizeof(T) == 8) {
+            const double2 w = *reinterpret_cast<const double2*>(&As[buf][kk][ty * TM + t]);
+            a[t] = w.x; a[t + 1] = w.y;
+          } else {
+            const float4 w = *reinterpret_cast<const float4*>(&As[buf][kk][ty * TM + t]);
+            a[t] = w.x; a[t + 1] = w.y; a[t + 2] = w.z; a[t + 3] = w.w;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < TN; ++t) b[t] = Bs[buf][kk][tx * TN + t];
+#pragma unroll
+        for (int u = 0; u < TM; ++u)
+#pragma unroll
+          for (int v = 0; v < TN; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+      }
+      if (more) {
+        store_tile(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+  T* dst = out + int64_t(blockIdx.y) * M * r;
+#pragma unroll
+  for (int u = 0; u < TM; ++u) {
+    const int64_t row = m0 + ty * TM + u;
+    if (row >= M) continue;
+#pragma unroll
+    for (int v = 0; v < TN; ++v) {
+      const int c = tx * TN + v;
+      if (c < r) dst[row * r + c] = acc[u][v];
+    }
+  }
+}
+
+// scn b through the register-tiled kernel (RP <= 64) or the legacy one (RP = 128).
 template <typename T>
 static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, int r, int64_t cps,
                             int S, T* out, cudaStream_t st) {
   dim3 grid(unsigned(ceil_div(m, 128)), unsigned(S));
+  switch (pick_rp(r)) {
+    case 16: cc_gemm_kernel<T, 16, true><<<grid, 128, 0, st>>>(X, W, m, m, r, n_loc, cps, out); return;
+    case 32: cc_gemm_kernel<T, 32, true><<<grid, 128, 0, st>>>(X, W, m, m, r, n_loc, cps, out); return;
+    case 64: cc_gemm_kernel<T, 64, true><<<grid, 128, 0, st>>>(X, W, m, m, r, n_loc, cps, out); return;
+    default: break;
+  }
   switch (pick_rp(r)) {
     case 16: gemm_wxt_kernel<T, 16><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
     case 32: gemm_wxt_kernel<T, 32><<<grid, 256, 0, st>>>(X, W, m, n_loc, r, cps, out); break;
@@ -290,6 +453,13 @@ static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, in
 template <typename T>
 static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, int r, int64_t rps,
                             int S, T* out, cudaStream_t st) {
+  dim3 grid128(unsigned(ceil_div(n_loc, 128)), unsigned(S));
+  switch (pick_rp(r)) {
+    case 16: cc_gemm_kernel<T, 16, false><<<grid128, 128, 0, st>>>(X, Vt, n_loc, m, r, m, rps, out); return;
+    case 32: cc_gemm_kernel<T, 32, false><<<grid128, 128, 0, st>>>(X, Vt, n_loc, m, r, m, rps, out); return;
+    case 64: cc_gemm_kernel<T, 64, false><<<grid128, 128, 0, st>>>(X, Vt, n_loc, m, r, m, rps, out); return;
+    default: break;
+  }
   dim3 grid(unsigned(ceil_div(n_loc, 64)), unsigned(S));
   switch (pick_rp(r)) {
     case 16: gemm_vtx_kernel<T, 16><<<grid, 256, 0, st>>>(X, Vt, m, n_loc, r, rps, out); break;
@@ -300,7 +470,7 @@ static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, i
 }
 
 static int wxt_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(m, 128), n_loc, 256); }
-static int vtx_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(n_loc, 64), m, 512); }
+static int vtx_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(n_loc, 128), m, 512); }
 
 static int dsize(int dtype) { return dtype == BS_F64 ? 8 : 4; }
 
