@@ -527,12 +527,21 @@ static MdsGrid mds_grid(int64_t n, int64_t n_loc, int q, int dtype) {
   return g;
 }
 
+namespace bs {
+bool mds_tc_eligible(int dtype, int64_t n, int64_t n_loc, int q, int mode, const void* Y, const void* theta);
+int64_t mds_tc_workspace(int64_t n, int64_t n_loc, int q);
+int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64_t n_loc, int q, int perturb,
+                double* red, Workspace& ws, cudaStream_t st, double** zp_out, double** tp_out, int* segs_out);
+}  // namespace bs
+
 extern "C" int64_t bs_mds_pass_workspace(int dtype, int64_t n, int64_t n_loc, int q) {
-  (void)dtype;
   MdsGrid g = mds_grid(n, n_loc, q, dtype);
-  return ws_bytes<unsigned int>(1) + ws_bytes<double>(2 * int64_t(g.colblocks) * g.segs) +
-         ws_bytes<double>(int64_t(g.segs) * n_loc) + ws_bytes<double>(int64_t(g.segs) * n_loc * q) +
-         ws_bytes<int64_t>(2) + ws_bytes<float>(n);
+  const int64_t core = ws_bytes<unsigned int>(1) + ws_bytes<double>(2 * int64_t(g.colblocks) * g.segs) +
+                       ws_bytes<double>(int64_t(g.segs) * n_loc) + ws_bytes<double>(int64_t(g.segs) * n_loc * q) +
+                       ws_bytes<int64_t>(2) + ws_bytes<float>(n);
+  // float32 passes may take the tcgen05 kernel (mds_tc.cu), which needs its own buffers
+  const int64_t tcw = (dtype == BS_F32 && q <= 32 && n > 0 && n_loc > 0) ? mds_tc_workspace(n, n_loc, q) : 0;
+  return std::max(core, tcw);
 }
 
 // ||theta_i||^2 for every row (float32 pass stages them with the theta chunk).
@@ -623,6 +632,17 @@ extern "C" int bs_mds_pass(const void* Y, const void* theta_full, int dtype, int
   if (n_loc == 0 || n == 0)
     return cudaMemsetAsync(red, 0, 2 * sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
   Workspace ws(work, work_bytes);
+  if (mds_tc_eligible(dtype, n, n_loc, q, mode, Y, theta_full)) {
+    double *zp = nullptr, *tp = nullptr;
+    int segs = 0;
+    int rc = mds_tc_pass(static_cast<const float*>(Y), static_cast<const float*>(theta_full), n, lo, n_loc, q, perturb,
+                         red, ws, st, &zp, &tp, &segs);
+    if (rc != BS_OK) return rc;
+    const int fg = int(std::min<int64_t>(ceil_div(n_loc * (q + 1), 256), 2048));
+    mds_fold_kernel<float><<<fg, 256, 0, st>>>(zp, tp, segs, n_loc, q, static_cast<float*>(zsum),
+                                               static_cast<float*>(T));
+    return check_launch("bs_mds_pass", 3);
+  }
   MdsGrid g = mds_grid(n, n_loc, q, dtype);
   unsigned int* ctr = ws.take<unsigned int>(1);
   double* parts = ws.take<double>(2 * int64_t(g.colblocks) * g.segs);

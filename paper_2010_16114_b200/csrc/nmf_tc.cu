@@ -23,10 +23,7 @@
 // X is read exactly once per GEMM; split-K slabs are folded in order by the
 // consumer.  The TMEM accumulator is double-buffered and restarted every G
 // k-blocks because the tensor core's fp32 accumulation truncates (see below).
-#include "bsb200.cuh"
-
-#include <cuda.h>
-#include <cudaTypedefs.h>
+#include "tc_common.cuh"
 
 #include <algorithm>
 #include <mutex>
@@ -34,6 +31,8 @@
 using namespace bs;
 
 namespace {
+
+using namespace tc;
 
 constexpr int TC_THREADS = 448;  // producer, MMA, 4 epilogue warps, 2 x 4 converter warps
 constexpr int BM = 128;
@@ -44,132 +43,9 @@ constexpr int A_STAGE_BYTES = BM * BK * 4;  // 16 KB
 #endif
 constexpr int SMEM_BUDGET = 220 * 1024;
 
-// ---------------------------------------------------------------------------
-// PTX helpers
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-
-// Waits for phase `parity` of the barrier; traps after ~10 s instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done = 0;
-  uint64_t t0 = 0;
-  for (uint32_t spin = 0;; ++spin) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (done) return;
-    if ((spin & 1023) == 1023) {
-      uint64_t now;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (t0 == 0) t0 = now;
-      else if (now - t0 > 10000000000ULL) __trap();
-    }
-  }
-}
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// SMEM matrix descriptor (tcgen05): start, LBO, SBO in 16-byte units, version 1, layout type.
-// Layout type 1 = SWIZZLE_128B_BASE32B, the only MN-major layout tf32 accepts
-// (Swizzle<2,5,2>, 4-row x 128 B atoms); the TMA writes it with
-// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B.  (K-major tiles use SWIZZLE_128B.)
-constexpr uint32_t LAYOUT_SW128_32B = 1;
-
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
-  uint64_t d = 0;
-  d |= uint64_t((addr >> 4) & 0x3FFF);
-  d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
-  d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
-  d |= uint64_t(1) << 46;  // version (Blackwell)
-  d |= uint64_t(layout) << 61;
-  return d;
-}
-
 // MN-major operand slab (32 MN x 32 K of a stage): k step s covers rows 8s..8s+7 = two 512 B atoms.
 __device__ __forceinline__ uint64_t mn_desc(uint32_t base, int s) {
   return sdesc(base + uint32_t(s) * 1024u, 4096, 512, LAYOUT_SW128_32B);
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* v) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
-      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
-      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-
-// One k-block (4 k steps of 8) of the concatenated 3xTF32 product, issued by one elected
-// lane: D[:, 0:2NP] += A_hi [Bh|Bl] and D[:, 0:NP] += A_lo Bh per k step.  All operands
-// are warp-uniform; the k-step offsets are added inside the asm so ptxas keeps them in
-// uniform registers (a per-MMA elect/R2UR loop costs ~2x the MMA itself).
-// bdesc: descriptor of the Bh slab at k step 0; each k step advances 1024 B (desc lo + 64).
-__device__ __forceinline__ void mma_kblock_concat(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bdesc,
-                                                  uint32_t id_wide, uint32_t id_narrow, uint32_t acc0) {
-  asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .b64 b1, b2, b3;\n\t"
-      "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.b32 q, %6, 0;\n\t"
-      "add.s64 b1, %3, 64;\n\tadd.s64 b2, %3, 128;\n\tadd.s64 b3, %3, 192;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %4, q;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+8], b1, %4, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+8], b1, %5, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+16], b2, %4, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+16], b2, %5, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], b3, %4, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2+24], b3, %5, 1;\n\t}" ::"r"(d),
-      "r"(a_hi), "r"(a_lo), "l"(bdesc), "r"(id_wide), "r"(id_narrow), "r"(acc0)
-      : "memory");
 }
 
 // Non-concatenated variant (NP > 64): three MMAs per k step, Bl slab at bdesc_lo.
@@ -195,27 +71,6 @@ __device__ __forceinline__ void mma_kblock_3(uint32_t d, uint32_t a_hi, uint32_t
       "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1+24], h3, %5, 1;\n\t}" ::"r"(d),
       "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(id), "r"(acc0)
       : "memory");
-}
-
-__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
-      "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-      : "memory");
-}
-
-__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
 }
 
 // Stage layout.  Raw ring (TMA targets): A raw (16 KB) + B raw (NP x 32 fp32).  Converted
@@ -546,49 +401,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 // host side: tensor maps and launch
 // ---------------------------------------------------------------------------
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 bool make_map(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1, bool mn_major) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {d0, d1};
-  cuuint64_t strides[1] = {d0 * sizeof(float)};
-  cuuint32_t box[2] = {b0, b1};
-  cuuint32_t es[2] = {1, 1};
-  CUresult rc = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return rc == CUDA_SUCCESS;
+  return make_map_f32(map, base, d0, d1, b0, b1,
+                      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 int pick_np(int r) { return r <= 32 ? 32 : r <= 64 ? 64 : r <= 96 ? 96 : r <= 128 ? 128 : 0; }
-
-bool tc_enabled() {
-  static int enabled = -1;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    const char* e = getenv("BS_DISABLE_TCGEN05");
-    int dev = 0, major = 0, minor = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-    enabled = (e && e[0] == '1') ? 0 : (major == 10 && minor == 0) ? 1 : 0;
-  });
-  return enabled == 1;
-}
 
 template <bool A_MN, int NP>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r, int splits, float* out, int64_t slab,

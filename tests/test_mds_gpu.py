@@ -72,6 +72,36 @@ def test_mds_f32_matches_oracle():
     assert np.abs(th - oth).max() <= 1e-4 * np.abs(oth).max()
 
 
+@pytest.mark.parametrize("n,q,p", [(400, 20, 1), (1000, 20, 3), (516, 8, 2), (300, 32, 1), (260, 3, 2),
+                                   (772, 17, 4)])
+def test_mds_f32_tensor_core_pass_matches_oracle(n, q, p):
+    """float32 with n % 4 == 0 and n >= 64 takes the tcgen05 pass (mds_tc.cu): 3xTF32 Gram and
+    T products, ragged 64-row chunk tails, uneven column blocks and ranks with lo > 0."""
+    x = orc.rand_fill_common((12, n), 80 + q, np.float32)
+    y = orc.pairwise_euclidean(x)
+    th0 = orc.mds_init(y, q, 90 + q)
+    tr, th = bs.run_inproc(p, _run, y, th0, 6)[0]
+    oth, otr = orc.mds_fit(y.astype(np.float64), th0.astype(np.float64), 6)
+    np.testing.assert_allclose(tr, otr, rtol=2e-5)
+    assert np.abs(th - oth).max() <= 2e-5 * np.abs(oth).max()
+
+
+def test_mds_f32_tensor_core_coincident_points():
+    """Exactly coincident embedding points give d = 0 exactly on the tcgen05 path too
+    (cancellation guard): the reference raises, or perturbs d to 1e-10 (solvers.py:290-296)."""
+    n, q = 128, 4
+    x = orc.rand_fill_common((6, n), 5, np.float32)
+    y = orc.pairwise_euclidean(x)
+    th0 = orc.mds_init(y, q, 6).astype(np.float32)
+    th0[:, 77] = th0[:, 3]
+    with pytest.raises(bs.DegenerateConfigError):
+        bs.run_inproc(2, _run, y, th0, 1, False)
+    for tr, th in bs.run_inproc(2, _run, y, th0, 2, True):
+        assert np.all(np.isfinite(tr))
+    tr1, _ = bs.run_inproc(1, _run, y, th0, 1, True)[0]
+    np.testing.assert_allclose(tr1[0], orc.mds_stress(th0.astype(np.float64), y.astype(np.float64)), rtol=1e-5)
+
+
 def test_mds_stress_examples_and_bruteforce():
     def fn(comm):
         theta = bs.distribute(np.array([[0.0, 1.0]]) if comm.rank == 0 else None, comm)
