@@ -1,32 +1,37 @@
 // tcgen05 MDS pass for float32 (solvers.py:269-305, mode 0 of bs_mds_pass).
 //
 // Per pair (i, j) of the rank's column block of Y the MM step needs
-//   g_ij = theta_i . theta_j,  d_ij = sqrt(|theta_i|^2 + |theta_j|^2 - 2 g_ij)   (solvers.py:237-247)
-//   stress += (y_ij - d_ij)^2,  zsum_j += y_ij / d_ij,  T_j += theta_i (1 - y_ij / d_ij)
-// (solvers.py:289-300).  Both q-long dot products are GEMM-shaped: for a tile of
-// 128 columns j x 64 rows i,
-//   MMA1  D1[j][i] = sum_k ThJ[j][k] ThI[i][k]       M = 128, N = 64, K = 32 (q padded)
-//   MMA2  D2[j][k] += sum_i WZ[j][i] ThI[i][k]       M = 128, N = 32, K = 64
-// and run on the tensor cores in 3xTF32 (hi*hi + hi*lo + lo*hi, fp32-level error);
-// the CUDA cores only do the per-pair elementwise chain between them.  Y is read
-// once, by TMA, exactly as in the CUDA-core pass (mds.cu).
+//   d2_ij = |theta_i|^2 + |theta_j|^2 - 2 theta_i . theta_j,  d = sqrt(d2)   (solvers.py:237-247)
+//   stress += (y - d)^2,  zsum_j += y / d,  T_j += theta_i (1 - y / d)       (solvers.py:289-300)
+// Both reductions over the q coordinates are GEMM-shaped.  With augmented rows
+//   I-side  u_i = [theta_i, 1, |theta_i|^2]      J-side  v_j = [-2 theta_j, |theta_j|^2, 1]
+// the Gram identity is one product, d2_ij = v_j . u_i, and with w_ij = 1 - z_ij
+//   T_aug[j] = sum_i w_ij u_i   gives T_j (first q entries) and sum_i w_ij (entry q),
+// so zsum_j = (#i) - T_aug[j][q].  For a tile of 128 columns j x 64 rows i:
+//   MMA1  D1[j][i]  = sum_k V[j][k] U[i][k]       M = 128, N = 64, K = 8 * ceil((q + 2) / 8)
+//   MMA2  D2[j][k] += sum_i W[j][i] U[i][k]       M = 128, N = 32, K = 64
+// both in 3xTF32 (hi*hi + hi*lo + lo*hi: fp32-level error).  Per pair the CUDA cores only
+// do rsqrt, d, z, (y - d)^2, 1 - z and the tf32 split (about 9 instructions).  Y is read
+// once, by TMA, like the CUDA-core pass (mds.cu).
 //
-// CTA (one per SM, persistent over (128-column block, row segment) units), 320 threads:
-//   warp 0     TMA producer: per 64-row chunk, Y tile (2 boxes of 32 i x 128 j, SWIZZLE_128B),
-//              theta_i hi/lo K-major (B of MMA1), theta_i hi/lo MN-major (B of MMA2), norms
-//   warp 1     MMA issuer (one elected lane): MMA1(c+1) is issued before MMA2(c)
-//   warps 2-9  epilogue, two warps per TMEM lane quarter (lane = column j), each owning
-//              32 of the chunk's 64 rows: tcgen05.ld g, elementwise chain, tcgen05.st
-//              the hi/lo split of (1 - z) as MMA2's A operand (TMEM, K-major)
-// TMEM (512 columns): D1 x2 [0,128), D2 [128,192), A1 = theta_J hi|lo [192,256),
-//                     A2 x2 = WZ hi|lo [256,512).
+// CTA (one per SM, persistent over (128-column block, row segment) units), 576 threads:
+//   warp 0      TMA producer
+//   warp 1      MMA issuer (one elected lane): MMA1 runs up to two chunks ahead of MMA2
+//   warps 2-17  epilogue: warp w owns TMEM lane quarter w % 4 (lane = column j) and one
+//               16-row slice of the chunk: tcgen05.ld d2, elementwise chain, tcgen05.st
+//               the hi/lo split of w as MMA2's A operand (TMEM, K-major)
+// Shared-memory rings, each released as soon as its consumer is done:
+//   Y  (2 boxes of 32 i x 128 j, SWIZZLE_128B)              freed by the epilogue once loaded
+//   B1 (U hi | lo, 64 i x 32 k, K-major SWIZZLE_128B)        freed by MMA1's commit
+//   B2 (U hi | lo, 2 x (32 i x 32 k) MN-major SW128_BASE32B) freed by MMA2's commit
+// TMEM (512 columns): D1 x2 [0,128), D2 [128,192), A1 = V_J hi|lo [192,256), A2 x2 [256,512).
 // D2 is restarted every G chunks and folded into fp32 registers (the tensor core's
 // accumulator add truncates, see nmf_tc.cu).
 //
-// Cancellation guard: where |theta_i|^2 + |theta_j|^2 - 2g loses more than 12 bits
-// (near-coincident points) the pair is recomputed from the coordinates,
-// sum_k (theta_ik - theta_jk)^2, so exactly coincident points give d = 0 exactly as
-// the reference's Gram identity does on its own input (solvers.py:246, 290-296).
+// Cancellation guard: where d2 <= 2^-12 (|theta_j|^2 + max_i |theta_i|^2) the pair is
+// recomputed from the coordinates, sum_k (theta_ik - theta_jk)^2, so exactly coincident
+// points give d = 0 exactly, as the reference's Gram identity does on its own input
+// (solvers.py:246, 290-296).
 #include "tc_common.cuh"
 
 #include <algorithm>
@@ -37,21 +42,19 @@ using namespace tc;
 
 namespace {
 
-constexpr int MT_THREADS = 320;
-constexpr int CHI = 64;   // rows i per chunk
-constexpr int BJ = 128;   // columns j per unit (MMA M)
-constexpr int KP = 32;    // q padded (one 128-byte row of fp32)
-constexpr int Y_BOX = 32 * 4 * BJ;              // 16 KB: 32 i x 128 j
-constexpr int OFF_Y = 0;                        // 2 boxes
-constexpr int OFF_B1H = 2 * Y_BOX;              // 64 i x 32 k, K-major SW128: 8 KB
-constexpr int OFF_B1L = OFF_B1H + 8192;
-constexpr int OFF_B2H = OFF_B1L + 8192;         // 2 boxes of 32 i x 32 k, MN-major SW128_32B: 8 KB
-constexpr int OFF_B2L = OFF_B2H + 8192;
-constexpr int OFF_NRM = OFF_B2L + 8192;         // 64 norms
-constexpr int STAGE = OFF_NRM + 1024;
-constexpr int NST = 3;
-constexpr uint32_t TX_BYTES = 2 * Y_BOX + 4 * 8192 + CHI * 4;
-constexpr int SMEM = NST * STAGE + 1024 /*align*/ + 256 /*barriers*/ + 2 * 2 * BJ * 8 /*zsum halves*/ + 512;
+constexpr int MT_THREADS = 576;  // TMA warp, MMA warp, 16 epilogue warps
+constexpr int NEPI = 512;        // epilogue threads
+constexpr int CHI = 64;          // rows i per chunk
+constexpr int BJ = 128;          // columns j per unit (MMA M)
+constexpr int KP = 32;           // augmented q padded (one 128-byte row of fp32)
+constexpr int Y_BOX = 32 * 4 * BJ;   // 16 KB
+constexpr int Y_STAGE = 2 * Y_BOX;
+constexpr int B_STAGE = 16384;       // hi at 0, lo at 8192
+constexpr int NY = 3, NB1 = 2, NB2 = 4;
+constexpr int OFF_B1 = NY * Y_STAGE;
+constexpr int OFF_B2 = OFF_B1 + NB1 * B_STAGE;
+constexpr int RINGS = OFF_B2 + NB2 * B_STAGE;
+constexpr int SMEM = RINGS + 1024 /*align*/ + 512 /*barriers*/ + 16 * 2 * 8 /*stress fold*/ + 512;
 constexpr uint32_t T_D1 = 0, T_D2 = 128, T_A1 = 192, T_A2 = 256;
 constexpr float CANCEL = 1.0f / 4096.0f;
 
@@ -69,10 +72,10 @@ __device__ __forceinline__ void mma3_kstep(uint32_t d, uint32_t a_hi, uint32_t a
       : "memory");
 }
 
-__device__ __forceinline__ float rsqrt_nr(float d2) {
+__device__ __forceinline__ float rsqrt_approx(float x) {
   float r;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d2));
-  return r * fmaf(-0.5f * d2 * r, r, 1.5f);
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // max rel. error 2^-22.9
+  return r;
 }
 
 // sum_k (theta_ik - theta_jk)^2 from the coordinates (cancellation path only).
@@ -85,13 +88,51 @@ __device__ __noinline__ float direct_d2(const float* ti, const float* tj, int q)
   return acc;
 }
 
+// The 16 pairs of one (column, row slice) with every special case of the MM step:
+// buf[0..16) = y, buf[16..32) = d2 from the tensor core; writes w = (W - Z)_ij to
+// buf[32..48) and returns the slice's stress.
+__device__ __noinline__ float careful_block(float* buf, int64_t ib, int64_t i_end, int64_t jg, bool live, float thr,
+                                           const float* theta, int q, int perturb, double& zeros) {
+  float st = 0.f;
+  for (int e = 0; e < 16; ++e) {
+    const int64_t i = ib + e;
+    const float y = buf[e];
+    float w = 0.f;
+    if (live && i < i_end) {
+      if (i == jg) {  // d_jj = 0 exactly, (W - Z)_jj = 0 (solvers.py:240-241, 299-300)
+        st = fmaf(y, y, st);
+      } else {
+        float d2 = buf[16 + e];
+        if (!(d2 > thr)) d2 = direct_d2(theta + i * q, theta + jg * q, q);
+        float d, z;
+        if (d2 > 0.f) {
+          const float r = rsqrt_approx(d2);
+          d = d2 * r;
+          z = y * r;  // solvers.py:297
+        } else {
+          d = 0.f;
+          zeros += 1.0;
+          z = perturb ? y * 1e10f : __fdiv_rn(y, 0.f);  // solvers.py:296
+        }
+        const float er = y - d;
+        st = fmaf(er, er, st);
+        w = 1.f - z;  // solvers.py:299
+      }
+    }
+    buf[32 + e] = w;
+  }
+  return st;
+}
+
 struct MdsTcArgs {
   const float* theta;   // q x n (theta_full, column-major)
-  const float* th_hi;   // n x 32 tf32 hi (rows padded with zeros)
-  const float* th_lo;   // n x 32 lo
+  const float* vj_hi;   // n x 32: [-2 theta_j, |theta_j|^2, 1, 0...] tf32 hi
+  const float* vj_lo;   //         ... lo
   const float* norms;   // n
+  const float* nmax;    // max_i |theta_i|^2 (1 float)
   int64_t n, lo, n_loc;
   int q, perturb, G;
+  int mode;             // debug (BS_MDS_TC_MODE): 1 skips the pair math, 2 the MMAs
   int jblocks, segs;
   int64_t rows_per_seg;
   double* zsum_part;    // [segs][n_loc]
@@ -105,48 +146,62 @@ template <int KS>
 __global__ void __launch_bounds__(MT_THREADS, 1)
 mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmKh,
               const __grid_constant__ CUtensorMap tmKl, const __grid_constant__ CUtensorMap tmMh,
-              const __grid_constant__ CUtensorMap tmMl, const __grid_constant__ CUtensorMap tmN, const MdsTcArgs a) {
+              const __grid_constant__ CUtensorMap tmMl, const MdsTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
-  // st_full[NST], st_empty[NST], d1_full[2], d1_empty[2], a2_full[2], a2_empty[2], d2_full, d2_empty,
-  // a1_full, a1_empty
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 12);
-  double* zsh = reinterpret_cast<double*>(smem + NST * STAGE + 256);       // [2][BJ]
-  double* red_sh = zsh + 2 * BJ;                                             // [8][2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RINGS);
+  // d1_full[2], d1_empty[2], a2_full[2], a2_empty[2], d2_full, d2_empty, a1_full, a1_empty,
+  // y_full[NY], y_empty[NY], b1_full[NB1], b1_empty[NB1], b2_full[NB2], b2_empty[NB2]
+  constexpr int NBAR = 12 + 2 * (NY + NB1 + NB2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + NBAR);
+  double* red_sh = reinterpret_cast<double*>(smem + RINGS + 512);  // [16][2]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto st_full = [&](int s) { return smem_u32(bars + s); };
-  auto st_empty = [&](int s) { return smem_u32(bars + NST + s); };
-  auto d1_full = [&](int b) { return smem_u32(bars + 2 * NST + b); };
-  auto d1_empty = [&](int b) { return smem_u32(bars + 2 * NST + 2 + b); };
-  auto a2_full = [&](int b) { return smem_u32(bars + 2 * NST + 4 + b); };
-  auto a2_empty = [&](int b) { return smem_u32(bars + 2 * NST + 6 + b); };
-  const uint32_t d2_full = smem_u32(bars + 2 * NST + 8), d2_empty = smem_u32(bars + 2 * NST + 9);
-  const uint32_t a1_full = smem_u32(bars + 2 * NST + 10), a1_empty = smem_u32(bars + 2 * NST + 11);
+  auto d1_full = [&](int b) { return smem_u32(bars + b); };
+  auto d1_empty = [&](int b) { return smem_u32(bars + 2 + b); };
+  auto a2_full = [&](int b) { return smem_u32(bars + 4 + b); };
+  auto a2_empty = [&](int b) { return smem_u32(bars + 6 + b); };
+  const uint32_t d2_full = smem_u32(bars + 8), d2_empty = smem_u32(bars + 9);
+  const uint32_t a1_full = smem_u32(bars + 10), a1_empty = smem_u32(bars + 11);
+  auto y_full = [&](int s) { return smem_u32(bars + 12 + s); };
+  auto y_empty = [&](int s) { return smem_u32(bars + 12 + NY + s); };
+  auto b1_full = [&](int s) { return smem_u32(bars + 12 + 2 * NY + s); };
+  auto b1_empty = [&](int s) { return smem_u32(bars + 12 + 2 * NY + NB1 + s); };
+  auto b2_full = [&](int s) { return smem_u32(bars + 12 + 2 * NY + 2 * NB1 + s); };
+  auto b2_empty = [&](int s) { return smem_u32(bars + 12 + 2 * NY + 2 * NB1 + NB2 + s); };
+  auto y_at = [&](uint32_t c) { return smem + (c % NY) * Y_STAGE; };
+  auto b1_at = [&](uint32_t c) { return smem + OFF_B1 + (c % NB1) * B_STAGE; };
+  auto b2_at = [&](uint32_t c) { return smem + OFF_B2 + (c % NB2) * B_STAGE; };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) {
-      mbar_init(st_full(s), 1);
-      mbar_init(st_empty(s), 1);
-    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(d1_full(b), 1);
-      mbar_init(d1_empty(b), 256);
-      mbar_init(a2_full(b), 256);
+      mbar_init(d1_empty(b), NEPI);
+      mbar_init(a2_full(b), NEPI);
       mbar_init(a2_empty(b), 1);
     }
     mbar_init(d2_full, 1);
-    mbar_init(d2_empty, 256);
-    mbar_init(a1_full, 256);
+    mbar_init(d2_empty, NEPI);
+    mbar_init(a1_full, NEPI);
     mbar_init(a1_empty, 1);
+    for (int s = 0; s < NY; ++s) {
+      mbar_init(y_full(s), 1);
+      mbar_init(y_empty(s), NEPI);
+    }
+    for (int s = 0; s < NB1; ++s) {
+      mbar_init(b1_full(s), 1);
+      mbar_init(b1_empty(s), 1);
+    }
+    for (int s = 0; s < NB2; ++s) {
+      mbar_init(b2_full(s), 1);
+      mbar_init(b2_empty(s), 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmY);
     prefetch_tmap(&tmKh);
     prefetch_tmap(&tmKl);
     prefetch_tmap(&tmMh);
     prefetch_tmap(&tmMl);
-    prefetch_tmap(&tmN);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
@@ -175,83 +230,116 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         int nch, seg;
         unit_range(u, j0, i0, nch, seg);
         for (int t = 0; t < nch; ++t, ++cc) {
-          const int s = int(cc % NST);
-          mbar_wait(st_empty(s), ((cc / NST) & 1) ^ 1);
-          const uint32_t fb = st_full(s);
-          mbar_expect_tx(fb, TX_BYTES);
-          const uint32_t base = smem_u32(smem + s * STAGE);
           const int ic = int(i0 + int64_t(t) * CHI);
-          tma_load_2d(base + OFF_Y, &tmY, ic, int(j0), fb);
-          tma_load_2d(base + OFF_Y + Y_BOX, &tmY, ic + 32, int(j0), fb);
-          tma_load_2d(base + OFF_B1H, &tmKh, 0, ic, fb);
-          tma_load_2d(base + OFF_B1L, &tmKl, 0, ic, fb);
-          tma_load_2d(base + OFF_B2H, &tmMh, 0, ic, fb);
-          tma_load_2d(base + OFF_B2H + 4096, &tmMh, 0, ic + 32, fb);
-          tma_load_2d(base + OFF_B2L, &tmMl, 0, ic, fb);
-          tma_load_2d(base + OFF_B2L + 4096, &tmMl, 0, ic + 32, fb);
-          tma_load_1d(base + OFF_NRM, &tmN, ic, fb);
+          {  // MMA1's B first: it gates the chunk's first MMA
+            const int s = int(cc % NB1);
+            mbar_wait_sleep(b1_empty(s), ((cc / NB1) & 1) ^ 1);
+            const uint32_t fb = b1_full(s), base = smem_u32(b1_at(cc));
+            mbar_expect_tx(fb, B_STAGE);
+            tma_load_2d(base, &tmKh, 0, ic, fb);
+            tma_load_2d(base + 8192, &tmKl, 0, ic, fb);
+          }
+          {
+            const int s = int(cc % NY);
+            mbar_wait_sleep(y_empty(s), ((cc / NY) & 1) ^ 1);
+            const uint32_t fb = y_full(s), base = smem_u32(y_at(cc));
+            mbar_expect_tx(fb, Y_STAGE);
+            tma_load_2d(base, &tmY, ic, int(j0), fb);
+            tma_load_2d(base + Y_BOX, &tmY, ic + 32, int(j0), fb);
+          }
+          {
+            const int s = int(cc % NB2);
+            mbar_wait_sleep(b2_empty(s), ((cc / NB2) & 1) ^ 1);
+            const uint32_t fb = b2_full(s), base = smem_u32(b2_at(cc));
+            mbar_expect_tx(fb, B_STAGE);
+            tma_load_2d(base, &tmMh, 0, ic, fb);
+            tma_load_2d(base + 4096, &tmMh, 0, ic + 32, fb);
+            tma_load_2d(base + 8192, &tmMl, 0, ic, fb);
+            tma_load_2d(base + 8192 + 4096, &tmMl, 0, ic + 32, fb);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // Event loop: MMA1 of the next chunk is issued as soon as its B1 stage has landed and
+    // its D1 buffer is free (up to two chunks ahead of MMA2), MMA2 of the oldest chunk as
+    // soon as the epilogue has written its A2; the tensor pipe executes in issue order.
     constexpr uint32_t id1 = idesc_tf32(128, CHI, false, false);
     constexpr uint32_t id2w = idesc_tf32(128, 2 * KP, false, true);
     constexpr uint32_t id2n = idesc_tf32(128, KP, false, true);
-    uint32_t cc = 0, gi = 0, ut = 0;
-    auto issue_mma2 = [&](uint32_t c, int t, int nch) {
-      const uint32_t b = c & 1;
-      mbar_wait(a2_full(b), (c >> 1) & 1);
-      const bool first = (t % a.G) == 0;
-      const bool last = ((t % a.G) == a.G - 1) || (t == nch - 1);
-      if (first) mbar_wait(d2_empty, (gi & 1) ^ 1);
-      tc_fence_after();
-      const int s = int(c % NST);
-      const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D2, 0);
-      const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A2 + b * 128, 0);
-      const uint32_t b2 = __shfl_sync(0xffffffffu, smem_u32(smem + s * STAGE + OFF_B2H), 0);
-      const uint64_t bd = sdesc(b2, 8192, 512, LAYOUT_SW128_32B);
-      mma_kblock_concat(d, ah, ah + 64, bd, id2w, id2n, first ? 0u : 1u);
-      mma_kblock_concat(d, ah + 32, ah + 96, bd + 256, id2w, id2n, 1u);
-      mma_commit_elect(a2_empty(b));
-      mma_commit_elect(st_empty(s));
-      if (last) {
-        mma_commit_elect(d2_full);
-        ++gi;
-      }
-      __syncwarp();
-    };
+    uint32_t cbase = 0, gi = 0, ut = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++ut) {
       int64_t j0, i0;
       int nch, seg;
       unit_range(u, j0, i0, nch, seg);
-      mbar_wait(a1_full, ut & 1);
+      mbar_wait_sleep(a1_full, ut & 1);
       tc_fence_after();
-      for (int t = 0; t < nch; ++t, ++cc) {
-        const int s = int(cc % NST);
-        const uint32_t b = cc & 1;
-        mbar_wait(st_full(s), (cc / NST) & 1);
-        mbar_wait(d1_empty(b), ((cc >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D1 + b * CHI, 0);
-        const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A1, 0);
-        const uint32_t bh = __shfl_sync(0xffffffffu, smem_u32(smem + s * STAGE + OFF_B1H), 0);
-        const uint64_t dh = sdesc(bh, 16, 1024, LAYOUT_SW128), dl = sdesc(bh + 8192, 16, 1024, LAYOUT_SW128);
+      int t1 = 0, t2 = 0;
+      while (t2 < nch) {
+        bool issued = false;
+        if (t1 < nch && t1 < t2 + 2) {
+          const uint32_t c = cbase + uint32_t(t1);
+          const int s = int(c % NB1);
+          const uint32_t b = c & 1;
+          if (mbar_test(b1_full(s), (c / NB1) & 1) && mbar_test(d1_empty(b), ((c >> 1) & 1) ^ 1)) {
+            tc_fence_after();
+            const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D1 + b * CHI, 0);
+            const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A1, 0);
+            const uint32_t bh = __shfl_sync(0xffffffffu, smem_u32(b1_at(c)), 0);
+            const uint64_t dh = sdesc(bh, 16, 1024, LAYOUT_SW128), dl = sdesc(bh + 8192, 16, 1024, LAYOUT_SW128);
 #pragma unroll
-        for (int k = 0; k < KS; ++k) mma3_kstep(d, ah + 8 * k, ah + 32 + 8 * k, dh + 2 * k, dl + 2 * k, id1, k > 0);
-        mma_commit_elect(d1_full(b));
-        if (t == nch - 1) mma_commit_elect(a1_empty);
-        __syncwarp();
-        if (t > 0) issue_mma2(cc - 1, t - 1, nch);
+            for (int k = 0; k < KS; ++k)
+              if (!(a.mode & 2)) mma3_kstep(d, ah + 8 * k, ah + 32 + 8 * k, dh + 2 * k, dl + 2 * k, id1, k > 0);
+            mma_commit_elect(d1_full(b));
+            mma_commit_elect(b1_empty(s));
+            if (t1 == nch - 1) mma_commit_elect(a1_empty);
+            __syncwarp();
+            ++t1;
+            issued = true;
+          }
+        }
+        if (t2 < t1) {
+          const uint32_t c = cbase + uint32_t(t2);
+          const uint32_t b = c & 1;
+          const int s = int(c % NB2);
+          const bool first = (t2 % a.G) == 0;
+          const bool last = ((t2 % a.G) == a.G - 1) || (t2 == nch - 1);
+          if (mbar_test(a2_full(b), (c >> 1) & 1) && (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
+              mbar_test(b2_full(s), (c / NB2) & 1)) {
+            tc_fence_after();
+            const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D2, 0);
+            const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A2 + b * 128, 0);
+            const uint32_t b2 = __shfl_sync(0xffffffffu, smem_u32(b2_at(c)), 0);
+            const uint64_t bd = sdesc(b2, 8192, 512, LAYOUT_SW128_32B);
+            if (!(a.mode & 2)) {
+              mma_kblock_concat(d, ah, ah + 64, bd, id2w, id2n, first ? 0u : 1u);
+              mma_kblock_concat(d, ah + 32, ah + 96, bd + 256, id2w, id2n, 1u);
+            }
+            mma_commit_elect(a2_empty(b));
+            mma_commit_elect(b2_empty(s));
+            if (last) {
+              mma_commit_elect(d2_full);
+              ++gi;
+            }
+            __syncwarp();
+            ++t2;
+            issued = true;
+          }
+        }
+        if (!issued) __nanosleep(64);
       }
-      issue_mma2(cc - 1, nch - 1, nch);
+      cbase += uint32_t(nch);
     }
   } else {
-    // ---------------- epilogue (warps 2..9) ----------------
-    const int qd = warp & 3, h = (warp - 2) >> 2;
+    // ---------------- epilogue (warps 2..17) ----------------
+    // warp w may touch TMEM lanes 32 (w % 4)..+31 (its column quarter); the four warps of a
+    // quarter split the chunk's 64 rows into 16-row slices (sub).
+    const int qd = warp & 3, sub = (warp - 2) >> 2, ew = warp - 2;
     const int jrow = qd * 32 + lane;
     const uint32_t lane_addr = uint32_t(qd * 32) << 16;
     const int q = a.q;
+    const float nmax = __ldg(a.nmax);
     uint32_t cc = 0, gi = 0, ut = 0;
     double stress = 0.0, zeros = 0.0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++ut) {
@@ -262,135 +350,117 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       const bool live = jl < a.n_loc;
       const int64_t jg = a.lo + (live ? jl : 0);
       const int64_t i_end = min(a.n, i0 + a.rows_per_seg);
-      // A1: this column's theta_j (hi for h = 0, lo for h = 1) into TMEM, K-major
+      // A1: v_j into TMEM (K-major): sub 0/1 write hi k 0-15/16-31, sub 2/3 the lo half
       mbar_wait(a1_empty, (ut & 1) ^ 1);
       tc_fence_after();
       {
-        uint32_t v[32];
-        const float4* src = reinterpret_cast<const float4*>((h ? a.th_lo : a.th_hi) + jg * KP);
+        uint32_t v[16];
+        const float4* src = reinterpret_cast<const float4*>((sub >= 2 ? a.vj_lo : a.vj_hi) + jg * KP + 16 * (sub & 1));
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           const float4 w = live ? __ldg(src + c) : make_float4(0.f, 0.f, 0.f, 0.f);
           v[4 * c] = __float_as_uint(w.x); v[4 * c + 1] = __float_as_uint(w.y);
           v[4 * c + 2] = __float_as_uint(w.z); v[4 * c + 3] = __float_as_uint(w.w);
         }
-        tmem_st32(tmem + lane_addr + T_A1 + 32 * h, v);
+        tmem_st16(tmem + lane_addr + T_A1 + 16 * sub, v);
         tmem_wait_st();
       }
       tc_fence_before();
       mbar_arrive(a1_full);
       const float nj = live ? __ldg(a.norms + jg) : 0.f;
-      float Tacc[16];
+      const float thr = CANCEL * (nj + nmax);
+      float Tacc[8];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) Tacc[k] = 0.f;
-      double zsum = 0.0;
+      for (int k = 0; k < 8; ++k) Tacc[k] = 0.f;
       bool fold_pending = false;
       auto fold = [&]() {
         mbar_wait(d2_full, gi & 1);
         tc_fence_after();
-        float v[16], w[16];
-        tmem_ld16(tmem + lane_addr + T_D2 + 16 * h, v);
-        tmem_ld16(tmem + lane_addr + T_D2 + KP + 16 * h, w);
+        float v[8], w[8];
+        tmem_ld8(tmem + lane_addr + T_D2 + 8 * sub, v);
+        tmem_ld8(tmem + lane_addr + T_D2 + KP + 8 * sub, w);
 #pragma unroll
-        for (int k = 0; k < 16; ++k) Tacc[k] = __fadd_rn(Tacc[k], __fadd_rn(v[k], w[k]));
+        for (int k = 0; k < 8; ++k) Tacc[k] = __fadd_rn(Tacc[k], __fadd_rn(v[k], w[k]));
         tc_fence_before();
         mbar_arrive(d2_empty);
         ++gi;
         fold_pending = false;
       };
       for (int t = 0; t < nch; ++t, ++cc) {
-        const int s = int(cc % NST);
+        const int s = int(cc % NY);
         const uint32_t b = cc & 1;
-        const int64_t ib = i0 + int64_t(t) * CHI + 32 * h;  // first row of this thread's 32
-        mbar_wait(st_full(s), (cc / NST) & 1);
+        const int64_t ib = i0 + int64_t(t) * CHI + 16 * sub;  // first row of this warp's 16
+        // Y tile: box sub/2 holds rows 32 (sub/2) .. +31; row jrow is 128 B of 16 B chunks
+        // stored at chunk ^ (jrow & 7) (SWIZZLE_128B)
+        uint4 yv[4];
+        {
+          mbar_wait(y_full(s), (cc / NY) & 1);
+          const uint32_t ybase = smem_u32(y_at(cc) + (sub >> 1) * Y_BOX) + uint32_t(jrow) * 128u;
+          const uint32_t c0 = uint32_t(sub & 1) * 4u;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) yv[c] = ld_shared_v4(ybase + (((c0 + uint32_t(c)) ^ uint32_t(jrow & 7)) << 4));
+          mbar_arrive(y_empty(s));  // in registers: the TMA may refill the stage
+        }
+        float y[16];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          y[4 * c] = __uint_as_float(yv[c].x); y[4 * c + 1] = __uint_as_float(yv[c].y);
+          y[4 * c + 2] = __uint_as_float(yv[c].z); y[4 * c + 3] = __uint_as_float(yv[c].w);
+        }
         mbar_wait(d1_full(b), (cc >> 1) & 1);
         tc_fence_after();
-        uint32_t g[32];
-        tmem_ld32_nowait(tmem + lane_addr + T_D1 + b * CHI + 32 * h, g);
-        tmem_wait_ld();
+        uint32_t g[16];
+        tmem_ld16_u(tmem + lane_addr + T_D1 + b * CHI + 16 * sub, g);
         tc_fence_before();
         mbar_arrive(d1_empty(b));
-        const uint32_t ybase = smem_u32(smem + s * STAGE + OFF_Y + h * Y_BOX) + uint32_t(jrow) * 128u;
-        const uint32_t nbase = smem_u32(smem + s * STAGE + OFF_NRM) + uint32_t(h) * 128u;
-        uint32_t wz[32];
-        float st_blk = 0.f, zs_blk = 0.f;
-        const float sn = nj;
-        bool bad = !live || (ib + 32 > i_end) || (jg >= ib && jg < ib + 32);
+        uint32_t wz[16], wl[16];
+        float st_blk = 0.f, dmin = 1e30f;
+        if (a.mode & 1) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint4 yv = ld_shared_v4(ybase + (uint32_t(c ^ (jrow & 7)) << 4));
-          const uint4 nv = ld_shared_v4(nbase + 16u * c);
-          const uint32_t ya[4] = {yv.x, yv.y, yv.z, yv.w};
-          const uint32_t na[4] = {nv.x, nv.y, nv.z, nv.w};
+          for (int e = 0; e < 16; ++e) wz[e] = wl[e] = g[e] ^ __float_as_uint(y[e]);
+        } else {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int t4 = 4 * c + e;
-            const float y = __uint_as_float(ya[e]);
-            const float sum = __uint_as_float(na[e]) + sn;
-            const float d2 = fmaf(-2.f, __uint_as_float(g[t4]), sum);
-            bad |= !(fmaf(-CANCEL, sum, d2) > 0.f);
-            const float rs = rsqrt_nr(d2);
-            const float d = d2 * rs;
-            const float z = y * rs;
-            const float er = y - d;
-            st_blk = fmaf(er, er, st_blk);
-            zs_blk += z;
-            wz[t4] = __float_as_uint(1.f - z);
-          }
+        for (int e = 0; e < 16; ++e) {
+          const float d2 = __uint_as_float(g[e]);  // |ti|^2 + |tj|^2 - 2 ti.tj  (solvers.py:246)
+          dmin = fminf(dmin, d2);
+          const float r = rsqrt_approx(d2);
+          const float d = d2 * r;
+          const float z = y[e] * r;               // solvers.py:297
+          const float er = y[e] - d;
+          st_blk = fmaf(er, er, st_blk);
+          const float w = 1.f - z;                // solvers.py:299
+          const uint32_t hw = tf32_hi(__float_as_uint(w));
+          wz[e] = hw;
+          wl[e] = __float_as_uint(w - __uint_as_float(hw));
         }
+        }
+        const bool bad = !(a.mode & 1) && (!(dmin > thr) || !live || (ib + 16 > i_end) || (jg >= ib && jg < ib + 16));
         if (bad) {
-          // careful path: tails, the diagonal, padding columns and cancellation
-          st_blk = 0.f;
-          zs_blk = 0.f;
+          // careful path (tails, the diagonal, padding columns, cancellation): out of line,
+          // through a local buffer so the fast path keeps everything in registers
+          float buf[48];
 #pragma unroll
-          for (int t4 = 0; t4 < 32; ++t4) {
-            const int64_t i = ib + t4;
-            const uint32_t c = uint32_t(t4 >> 2), e = uint32_t(t4 & 3);
-            const float y = __uint_as_float(ld_shared_u32(ybase + ((c ^ uint32_t(jrow & 7)) << 4) + 4u * e));
-            const float ni = __uint_as_float(ld_shared_u32(nbase + 4u * uint32_t(t4)));
-            float w = 0.f;
-            if (live && i < i_end) {
-              if (i == jg) {  // d_jj = 0 exactly, (W - Z)_jj = 0 (solvers.py:240-241, 299-300)
-                st_blk = fmaf(y, y, st_blk);
-              } else {
-                const float sum = ni + sn;
-                float d2 = fmaf(-2.f, __uint_as_float(g[t4]), sum);
-                if (!(fmaf(-CANCEL, sum, d2) > 0.f)) d2 = direct_d2(a.theta + i * q, a.theta + jg * q, q);
-                float d, z;
-                if (d2 > 0.f) {
-                  const float rs = rsqrt_nr(d2);
-                  d = d2 * rs;
-                  z = y * rs;  // solvers.py:297
-                } else {
-                  d = 0.f;
-                  zeros += 1.0;
-                  z = a.perturb ? y * 1e10f : __fdiv_rn(y, 0.f);  // solvers.py:296
-                }
-                const float er = y - d;
-                st_blk = fmaf(er, er, st_blk);
-                zs_blk += z;
-                w = 1.f - z;  // solvers.py:299
-              }
-            }
-            wz[t4] = __float_as_uint(w);
+          for (int e = 0; e < 16; ++e) {
+            buf[e] = y[e];
+            buf[16 + e] = __uint_as_float(g[e]);
+          }
+          st_blk = careful_block(buf, ib, i_end, jg, live, thr, a.theta, q, a.perturb, zeros);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const float w = buf[32 + e];
+            const uint32_t hw = tf32_hi(__float_as_uint(w));
+            wz[e] = hw;
+            wl[e] = __float_as_uint(w - __uint_as_float(hw));
           }
         }
         stress += double(st_blk);
-        zsum += double(zs_blk);
-        // A2 <- hi | lo of (W - Z) for this chunk
+        // A2 <- hi | lo of W for this chunk
         mbar_wait(a2_empty(b), ((cc >> 1) & 1) ^ 1);
         tc_fence_after();
         {
-          uint32_t lo[32];
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const uint32_t hi = tf32_hi(wz[k]);
-            lo[k] = __float_as_uint(__uint_as_float(wz[k]) - __uint_as_float(hi));
-            wz[k] = hi;
-          }
-          const uint32_t a2 = tmem + lane_addr + T_A2 + b * 128 + 32 * h;
-          tmem_st32(a2, wz);
-          tmem_st32(a2 + 64, lo);
+          const uint32_t a2 = tmem + lane_addr + T_A2 + b * 128 + 16 * sub;
+          tmem_st16(a2, wz);
+          tmem_st16(a2 + 64, wl);
           tmem_wait_st();
         }
         tc_fence_before();
@@ -399,18 +469,19 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         if ((t % a.G) == a.G - 1 || t == nch - 1) fold_pending = true;
       }
       if (fold_pending) fold();
-      // ---- unit outputs: zsum (two halves combined in order), T (each half owns 16 k) ----
-      double* zs_sh = zsh;  // reuse is ordered by the two named barriers
-      zs_sh[h * BJ + jrow] = zsum;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      // ---- unit outputs: T (each slice owns 8 of the augmented k) and zsum = #i - sum_i w ----
       if (live) {
-        if (h == 0) a.zsum_part[int64_t(seg) * a.n_loc + jl] = zs_sh[jrow] + zs_sh[BJ + jrow];
         double* tp = a.T_part + (int64_t(seg) * a.n_loc + jl) * q;
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-          if (16 * h + k < q) tp[16 * h + k] = double(Tacc[k]);
+        for (int k = 0; k < 8; ++k) {
+          const int kk = 8 * sub + k;
+          if (kk < q) tp[kk] = double(Tacc[k]);
+          if (kk == q) {
+            const int64_t cnt = (i_end - i0) - ((jg >= i0 && jg < i_end) ? 1 : 0);
+            a.zsum_part[int64_t(seg) * a.n_loc + jl] = double(cnt) - double(Tacc[k]);
+          }
+        }
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     // ---- CTA stress / zero-count partial: warps in order ----
 #pragma unroll
@@ -419,13 +490,13 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
     }
     if (lane == 0) {
-      red_sh[2 * (warp - 2)] = stress;
-      red_sh[2 * (warp - 2) + 1] = zeros;
+      red_sh[2 * ew] = stress;
+      red_sh[2 * ew + 1] = zeros;
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (warp == 2 && lane == 0) {
+    asm volatile("bar.sync 1, 512;" ::: "memory");
+    if (ew == 0 && lane == 0) {
       double s0 = 0.0, z0 = 0.0;
-      for (int w = 0; w < 8; ++w) {
+      for (int w = 0; w < 16; ++w) {
         s0 += red_sh[2 * w];
         z0 += red_sh[2 * w + 1];
       }
@@ -449,20 +520,31 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
   }
 }
 
-// theta (q x n) -> tf32 hi / lo rows padded to 32, and |theta_i|^2.
-__global__ void mds_tc_prep_kernel(const float* __restrict__ theta, int64_t n, int q, float* __restrict__ hi,
-                                   float* __restrict__ lo, float* __restrict__ norms) {
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * KP; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / KP;
-    const int k = int(e - i * KP);
-    const float x = k < q ? theta[i * q + k] : 0.f;
-    const uint32_t h = tf32_hi(__float_as_uint(x));
-    hi[e] = __uint_as_float(h);
-    lo[e] = x - __uint_as_float(h);
-    if (k == 0) {
-      float s = 0.f;
-      for (int kk = 0; kk < q; ++kk) s = fmaf(theta[i * q + kk], theta[i * q + kk], s);
-      norms[i] = s;
+// theta (q x n) -> augmented rows (tf32 hi / lo, padded to 32):
+//   U_i = [theta_i, 1, |theta_i|^2]   V_i = [-2 theta_i, |theta_i|^2, 1]
+// plus |theta_i|^2 and max_i |theta_i|^2 (nmax zeroed by the caller; norms are >= 0, so
+// their float bits order like integers).
+__global__ void mds_tc_prep_kernel(const float* __restrict__ theta, int64_t n, int q, float* __restrict__ uh,
+                                   float* __restrict__ ul, float* __restrict__ vh, float* __restrict__ vl,
+                                   float* __restrict__ norms, float* __restrict__ nmax) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float* t = theta + i * q;
+    float s = 0.f;
+    for (int k = 0; k < q; ++k) s = fmaf(t[k], t[k], s);
+    norms[i] = s;
+    atomicMax(reinterpret_cast<unsigned int*>(nmax), __float_as_uint(s));
+    float* uhr = uh + i * KP;
+    float* ulr = ul + i * KP;
+    float* vhr = vh + i * KP;
+    float* vlr = vl + i * KP;
+    for (int k = 0; k < KP; ++k) {
+      const float u = k < q ? t[k] : k == q ? 1.f : k == q + 1 ? s : 0.f;
+      const float v = k < q ? -2.f * t[k] : k == q ? s : k == q + 1 ? 1.f : 0.f;
+      const uint32_t hu = tf32_hi(__float_as_uint(u)), hv = tf32_hi(__float_as_uint(v));
+      uhr[k] = __uint_as_float(hu);
+      ulr[k] = u - __uint_as_float(hu);
+      vhr[k] = __uint_as_float(hv);
+      vlr[k] = v - __uint_as_float(hv);
     }
   }
 }
@@ -497,7 +579,7 @@ TcGrid tc_grid(int64_t n, int64_t n_loc) {
 namespace bs {
 
 bool mds_tc_eligible(int dtype, int64_t n, int64_t n_loc, int q, int mode, const void* Y, const void* theta) {
-  return dtype == BS_F32 && mode == 0 && q >= 1 && q <= KP && n % 4 == 0 && n >= CHI && n_loc >= 1 &&
+  return dtype == BS_F32 && mode == 0 && q >= 1 && q + 2 <= KP && n % 4 == 0 && n >= CHI && n_loc >= 1 &&
          n <= INT32_MAX && n_loc <= INT32_MAX && (reinterpret_cast<uintptr_t>(Y) & 15) == 0 &&
          (reinterpret_cast<uintptr_t>(theta) & 15) == 0 && tc::tc_enabled();
 }
@@ -505,7 +587,8 @@ bool mds_tc_eligible(int dtype, int64_t n, int64_t n_loc, int q, int mode, const
 int64_t mds_tc_workspace(int64_t n, int64_t n_loc, int q) {
   TcGrid g = tc_grid(n, n_loc);
   return ws_bytes<unsigned int>(1) + ws_bytes<double>(2 * int64_t(g.grid)) + ws_bytes<double>(int64_t(g.segs) * n_loc) +
-         ws_bytes<double>(int64_t(g.segs) * n_loc * q) + ws_bytes<float>(n) + 2 * ws_bytes<float>(n * KP);
+         ws_bytes<double>(int64_t(g.segs) * n_loc * q) + ws_bytes<float>(n) + ws_bytes<float>(1) +
+         4 * ws_bytes<float>(n * KP);
 }
 
 // Returns BS_OK with *segs_out / the partial pointers set for mds_fold_kernel.
@@ -517,41 +600,50 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
   double* zp = ws.take<double>(int64_t(g.segs) * n_loc);
   double* tp = ws.take<double>(int64_t(g.segs) * n_loc * q);
   float* norms = ws.take<float>(n);
-  float* hi = ws.take<float>(n * KP);
-  float* lo_ = ws.take<float>(n * KP);
-  if (!ctr || !parts || !zp || !tp || !norms || !hi || !lo_) {
+  float* nmax = ws.take<float>(1);
+  float* uh = ws.take<float>(n * KP);
+  float* ul = ws.take<float>(n * KP);
+  float* vh = ws.take<float>(n * KP);
+  float* vl = ws.take<float>(n * KP);
+  if (!ctr || !parts || !zp || !tp || !norms || !nmax || !uh || !ul || !vh || !vl) {
     set_error("bs_mds_pass: workspace too small");
     return BS_EWORK;
   }
-  CUtensorMap mY, mKh, mKl, mMh, mMl, mN;
+  CUtensorMap mY, mKh, mKl, mMh, mMl;
   bool ok = make_map_f32(&mY, Y, uint64_t(n), uint64_t(n_loc), 32, BJ, CU_TENSOR_MAP_SWIZZLE_128B) &&
-            make_map_f32(&mKh, hi, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
-            make_map_f32(&mKl, lo_, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
-            make_map_f32(&mMh, hi, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
-            make_map_f32(&mMl, lo_, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
-            make_map_f32(&mN, norms, uint64_t(n), 0, CHI, 0, CU_TENSOR_MAP_SWIZZLE_NONE);
+            make_map_f32(&mKh, uh, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
+            make_map_f32(&mKl, ul, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
+            make_map_f32(&mMh, uh, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+            make_map_f32(&mMl, ul, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok) {
     set_error("bs_mds_pass: cuTensorMapEncodeTiled failed");
     return BS_ECUDA;
   }
-  static int group = -1;
+  static int group = -1, mode = 0;
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = getenv("BS_MDS_TC_GROUP");
     group = (e && atoi(e) > 0) ? atoi(e) : 2;
+    const char* m = getenv("BS_MDS_TC_MODE");
+    mode = m ? atoi(m) : 0;
     cudaFuncSetAttribute(mds_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     cudaFuncSetAttribute(mds_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     cudaFuncSetAttribute(mds_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     cudaFuncSetAttribute(mds_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   });
-  mds_tc_prep_kernel<<<int(std::min<int64_t>(ceil_div(n * KP, 256), 4096)), 256, 0, st>>>(theta, n, q, hi, lo_, norms);
-  MdsTcArgs args{theta, hi, lo_, norms, n, lo, n_loc, q, perturb, group, g.jblocks, g.segs, g.rows_per_seg,
+  if (cudaMemsetAsync(nmax, 0, sizeof(float), st) != cudaSuccess) {
+    set_error("bs_mds_pass: cudaMemsetAsync failed");
+    return BS_ECUDA;
+  }
+  mds_tc_prep_kernel<<<int(std::min<int64_t>(ceil_div(n, 256), 2048)), 256, 0, st>>>(theta, n, q, uh, ul, vh, vl,
+                                                                                    norms, nmax);
+  MdsTcArgs args{theta, vh, vl, norms, nmax, n, lo, n_loc, q, perturb, group, mode, g.jblocks, g.segs, g.rows_per_seg,
                  zp, tp, parts, ctr, red};
-  switch ((q + 7) / 8) {
-    case 1: mds_tc_kernel<1><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mN, args); break;
-    case 2: mds_tc_kernel<2><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mN, args); break;
-    case 3: mds_tc_kernel<3><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mN, args); break;
-    default: mds_tc_kernel<4><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mN, args); break;
+  switch ((q + 2 + 7) / 8) {
+    case 1: mds_tc_kernel<1><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
+    case 2: mds_tc_kernel<2><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
+    case 3: mds_tc_kernel<3><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
+    default: mds_tc_kernel<4><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
   }
   *zp_out = zp;
   *tp_out = tp;

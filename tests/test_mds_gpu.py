@@ -72,7 +72,7 @@ def test_mds_f32_matches_oracle():
     assert np.abs(th - oth).max() <= 1e-4 * np.abs(oth).max()
 
 
-@pytest.mark.parametrize("n,q,p", [(400, 20, 1), (1000, 20, 3), (516, 8, 2), (300, 32, 1), (260, 3, 2),
+@pytest.mark.parametrize("n,q,p", [(400, 20, 1), (1000, 20, 3), (516, 8, 2), (300, 30, 1), (260, 3, 2), (200, 32, 1),
                                    (772, 17, 4)])
 def test_mds_f32_tensor_core_pass_matches_oracle(n, q, p):
     """float32 with n % 4 == 0 and n >= 64 takes the tcgen05 pass (mds_tc.cu): 3xTF32 Gram and
