@@ -431,11 +431,161 @@ cc_gemm_kernel(const T* __restrict__ X, const T* __restrict__ B, int64_t M, int6
   }
 }
 
+// ---------------------------------------------------------------------------
+// float64: the same 128 x RP tile on the FP64 tensor cores (mma.sync m8n8k4 DMMA).
+// Staging as in cc_gemm_kernel (register double buffering into As[k][m] / Bs[k][c]);
+// warp w owns rows 32w..32w+31 as 4 x (RP/8) 8x8 accumulator fragments.  Per 4-wide k
+// step a warp loads 4 A and RP/8 B fragments (one double per lane each) for 4 RP/8
+// DMMAs (256 FMAs each).  Row strides are padded to 64 B mod 128 so the 4 k rows a
+// fragment load touches fall in disjoint bank halves.  Every product and sum is an
+// IEEE float64 FMA, like the CUDA-core kernel (only the summation order differs).
+// ---------------------------------------------------------------------------
+
+template <int RP, bool A_MN>
+__global__ void __launch_bounds__(128)
+dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int64_t M, int64_t ldx, int r,
+                 int64_t K, int64_t k_per_split, double* __restrict__ out) {
+  constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, V = 2, NF = RP / 8;
+  constexpr int PA = 8, PB = 8;  // pads (doubles): row strides = 64 B mod 128
+  __shared__ __align__(16) double As[2][BK][BM + PA];
+  __shared__ __align__(16) double Bs[2][BK][RP + PB];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = int64_t(blockIdx.x) * BM;
+  const int64_t k_begin = int64_t(blockIdx.y) * k_per_split;
+  const int64_t k_end = min(K, k_begin + k_per_split);
+  constexpr int A_PER = BM * BK / 128;
+  constexpr int B_PER = (BK * RP + 127) / 128;
+  double ra[A_PER], rb[B_PER];
+  const bool vec_ok = (ldx % V) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  auto load_tile = [&](int64_t k0) {
+    if constexpr (A_MN) {
+#pragma unroll
+      for (int u = 0; u < A_PER / V; ++u) {
+        const int e = tid + 128 * u;
+        const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
+        const int64_t k = k0 + kk, mrow = m0 + mv;
+        if (vec_ok && k < k_end && mrow + V <= M) {
+          const double2 w = *reinterpret_cast<const double2*>(X + k * ldx + mrow);
+          ra[u * V] = w.x; ra[u * V + 1] = w.y;
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) ra[u * V + v] = (k < k_end && mrow + v < M) ? X[k * ldx + mrow + v] : 0.0;
+        }
+      }
+    } else {
+      const int64_t mrow = m0 + tid;
+      const double* src = X + mrow * ldx + k0;
+      if (mrow < M && k0 + A_PER <= k_end && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+        for (int u = 0; u < A_PER; u += V) {
+          const double2 w = *reinterpret_cast<const double2*>(src + u);
+          ra[u] = w.x; ra[u + 1] = w.y;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < A_PER; ++kk) {
+          const int64_t k = k0 + kk;
+          ra[kk] = (mrow < M && k < k_end) ? X[mrow * ldx + k] : 0.0;
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER; ++u) {
+      const int e = tid + 128 * u;
+      const int kk = e / RP, c = e % RP;
+      const int64_t k = k0 + kk;
+      rb[u] = (e < BK * RP && k < k_end && c < r) ? B[k * r + c] : 0.0;
+    }
+  };
+  auto store_tile = [&](int buf) {
+    if constexpr (A_MN) {
+#pragma unroll
+      for (int u = 0; u < A_PER / V; ++u) {
+        const int e = tid + 128 * u;
+        const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
+        *reinterpret_cast<double2*>(&As[buf][kk][mv]) = make_double2(ra[u * V], ra[u * V + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < A_PER; ++kk) As[buf][kk][tid] = ra[kk];
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER; ++u) {
+      const int e = tid + 128 * u;
+      if (e < BK * RP) Bs[buf][e / RP][e % RP] = rb[u];
+    }
+  };
+  double acc[4][NF][2];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int g = 0; g < NF; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k of this lane
+  if (k_begin < k_end) {
+    load_tile(k_begin);
+    store_tile(0);
+    __syncthreads();
+    int buf = 0;
+    for (int64_t k0 = k_begin; k0 < k_end; k0 += BK) {
+      const bool more = k0 + BK < k_end;
+      if (more) load_tile(k0 + BK);  // in flight while this tile is consumed
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 4) {
+        double a[4], b[NF];
+#pragma unroll
+        for (int f = 0; f < 4; ++f) a[f] = As[buf][ks + fk][32 * warp + 8 * f + fr];
+#pragma unroll
+        for (int g = 0; g < NF; ++g) b[g] = Bs[buf][ks + fk][8 * g + fr];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int g = 0; g < NF; ++g)
+            asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                : "+d"(acc[f][g][0]), "+d"(acc[f][g][1])
+                : "d"(a[f]), "d"(b[g]));
+      }
+      if (more) {
+        store_tile(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+  double* dst = out + int64_t(blockIdx.y) * M * r;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t row = m0 + 32 * warp + 8 * f + fr;
+    if (row >= M) continue;
+#pragma unroll
+    for (int g = 0; g < NF; ++g) {
+      const int c = 8 * g + 2 * fk;
+      if (c < r) dst[row * r + c] = acc[f][g][0];
+      if (c + 1 < r) dst[row * r + c + 1] = acc[f][g][1];
+    }
+  }
+}
+
+template <bool A_MN>
+static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx, int r, int64_t K, int64_t kps,
+                        dim3 grid, double* out, cudaStream_t st) {
+  static const bool disabled = getenv("BS_DISABLE_DMMA") != nullptr;  // A/B switch for benchmarks
+  if (disabled) return false;
+  switch (pick_rp(r)) {
+    case 16: dmma_gemm_kernel<16, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
+    case 32: dmma_gemm_kernel<32, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
+    case 64: dmma_gemm_kernel<64, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
+    default: return false;
+  }
+}
+
 // scn b through the register-tiled kernel (RP <= 64) or the legacy one (RP = 128).
 template <typename T>
 static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, int r, int64_t cps,
                             int S, T* out, cudaStream_t st) {
   dim3 grid(unsigned(ceil_div(m, 128)), unsigned(S));
+  if constexpr (sizeof(T) == 8) {
+    if (launch_dmma<true>(X, W, m, m, r, n_loc, cps, grid, out, st)) return;
+  }
   switch (pick_rp(r)) {
     case 16: cc_gemm_kernel<T, 16, true><<<grid, 128, 0, st>>>(X, W, m, m, r, n_loc, cps, out); return;
     case 32: cc_gemm_kernel<T, 32, true><<<grid, 128, 0, st>>>(X, W, m, m, r, n_loc, cps, out); return;
@@ -454,6 +604,9 @@ template <typename T>
 static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, int r, int64_t rps,
                             int S, T* out, cudaStream_t st) {
   dim3 grid128(unsigned(ceil_div(n_loc, 128)), unsigned(S));
+  if constexpr (sizeof(T) == 8) {
+    if (launch_dmma<false>(X, Vt, n_loc, m, r, m, rps, grid128, out, st)) return;
+  }
   switch (pick_rp(r)) {
     case 16: cc_gemm_kernel<T, 16, false><<<grid128, 128, 0, st>>>(X, Vt, n_loc, m, r, m, rps, out); return;
     case 32: cc_gemm_kernel<T, 32, false><<<grid128, 128, 0, st>>>(X, Vt, n_loc, m, r, m, rps, out); return;
