@@ -851,8 +851,9 @@ factor_update_kernel(int algo, T* __restrict__ F, const TN* __restrict__ num, in
   if (last_block_done(counter)) fold_parts_block(parts, gridDim.x, rr + 1, BS_SUM, red);
 }
 
+// >= 64 columns per block, at most 2 blocks per SM (the last block folds grid x (r^2 + 1) partials)
 static int upd_grid(int64_t ncols) {
-  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 256), int64_t(num_sms()) * 2)));
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 64), int64_t(num_sms()) * 2)));
 }
 
 static int64_t upd_workspace(int r, int64_t ncols) {
