@@ -24,8 +24,12 @@ place.  Two backends implement it here:
 reference all-reduces the r x m product of scenario b and then keeps only its
 own column slice (distlinalg.py:251-252); a reduce-scatter moves 1/p of the data.
 
-The reference's TCP hub backend (comm.py:360-578) is not part of this build:
-multi-process runs use torch.distributed.
+``tcp:<host:port>,...,rank=<r>``
+    The reference's multi-process descriptor (comm.py:12-15, 501-519).  Instead
+    of a hub that relays every payload over sockets (comm.py:360-578), the
+    first host:port serves a TCPStore rendezvous that bootstraps a
+    torch.distributed world (NCCL's unique id travels through the store); the
+    collectives then run as in the ``nccl`` / ``gloo`` backend.
 """
 
 from __future__ import annotations
@@ -477,17 +481,28 @@ def _fold_into(dst, srcs, redop):
 class _TorchCommunicator(Communicator):
     """Collectives over a torch.distributed process group (NCCL or gloo)."""
 
-    def __init__(self, backend_name):
+    def __init__(self, backend_name, rendezvous=None, timeout=30.0):
+        """``rendezvous`` = (host, port, rank, size) for the reference's tcp descriptor:
+        rank 0 hosts a TCPStore at host:port, the other ranks join it, and the store
+        carries NCCL's unique id (the bootstrap the reference's hub socket performed);
+        None joins the env:// world (torchrun)."""
         super().__init__()
         torch = _torch()
+        import datetime
+
         import torch.distributed as dist
 
         self._dist = dist
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             kw = {}
+            if rendezvous is not None:
+                host, port, rank, size = rendezvous
+                kw.update(init_method=f"tcp://{host}:{port}", rank=rank, world_size=size,
+                          timeout=datetime.timedelta(seconds=max(float(timeout), 30.0)))
             if backend_name == "nccl":
-                local = int(os.environ.get("LOCAL_RANK", "0"))
+                ndev = max(torch.cuda.device_count(), 1)
+                local = int(os.environ.get("LOCAL_RANK", str(rendezvous[2] % ndev if rendezvous else 0)))
                 torch.cuda.set_device(local)
                 kw["device_id"] = torch.device("cuda", local)
             dist.init_process_group(backend=backend_name, **kw)
@@ -591,8 +606,22 @@ def _parse_descriptor(descriptor):
     if descriptor in ("nccl", "gloo", "torch"):
         return "torch", descriptor
     if descriptor.startswith("tcp:"):
-        raise CommInitError("the tcp hub backend is not part of the B200 build; launch one process per "
-                            "GPU with torchrun and use the 'nccl' descriptor")
+        # tcp:host:port,...,rank=<r> (comm.py:501-519): one process per rank; here the
+        # first entry is the TCPStore that bootstraps NCCL (gloo without a GPU).
+        parts = descriptor[4:].split(",")
+        if len(parts) < 2 or not parts[-1].startswith("rank="):
+            raise CommInitError(f"bad tcp descriptor {descriptor!r}; expected tcp:host:port,...,rank=<r>")
+        try:
+            rank = int(parts[-1][5:])
+            hosts = []
+            for entry in parts[:-1]:
+                host, port = entry.rsplit(":", 1)
+                hosts.append((host, int(port)))
+        except ValueError:
+            raise CommInitError(f"bad tcp descriptor {descriptor!r}") from None
+        if not 0 <= rank < len(hosts):
+            raise CommInitError(f"rank {rank} out of range for {len(hosts)} hosts")
+        return "tcp", (hosts, rank)
     raise CommInitError(f"unknown backend descriptor {descriptor!r}")
 
 
@@ -602,11 +631,21 @@ def init(descriptor, timeout=30.0):
     ``inproc:<P>`` returns a list of P endpoints sharing one world (one per
     rank thread).  ``nccl`` / ``gloo`` join the torch.distributed world of this
     process (env:// rendezvous, e.g. under torchrun) and return its endpoint.
+    ``tcp:host:port,...,rank=<r>`` (the reference's multi-process descriptor)
+    rendezvouses at the first host:port and returns this process's endpoint.
     """
     kind, arg = _parse_descriptor(descriptor)
     if kind == "inproc":
         world = _InProcWorld(arg)
         return [_InProcCommunicator(world, r) for r in range(arg)]
+    if kind == "tcp":
+        hosts, rank = arg
+        backend = "nccl" if _torch().cuda.is_available() else "gloo"
+        try:
+            return _TorchCommunicator(backend, rendezvous=(hosts[0][0], hosts[0][1], rank, len(hosts)),
+                                      timeout=timeout)
+        except Exception as exc:  # noqa: BLE001
+            raise CommInitError(f"tcp rendezvous at {hosts[0][0]}:{hosts[0][1]} failed: {exc}") from exc
     backend = arg
     if backend == "torch":
         backend = "nccl" if _torch().cuda.is_available() else "gloo"

@@ -130,3 +130,46 @@ def test_abi_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert set(syms) == set(_lib.SIGNATURES)
     assert lib.bs_abi_version() == 1
+
+
+def _tcp_worker(rank, port, q):
+    """One rank of the reference's multi-process descriptor (comm.py:12-15)."""
+    try:
+        desc = f"tcp:127.0.0.1:{port},127.0.0.1:{port + 1},rank={rank}"
+
+        def fn(comm):
+            a = np.array([1.0, 2.0]) * (comm.rank + 1)
+            comm.allreduce(a)
+            recv = torch.empty(3, dtype=torch.float64)
+            comm.allgatherv(torch.arange(2 - comm.rank, dtype=torch.float64) + 10 * comm.rank, recv, [2, 1])
+            return comm.rank, comm.size, a.tolist(), recv.tolist()
+
+        q.put((rank, bs.launch(desc, fn)))
+    except Exception as exc:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(exc)))
+
+
+def test_tcp_descriptor_world2():
+    """tcp:host:port,...,rank=<r> rendezvouses at the first entry and runs the collectives
+    (NCCL on a GPU box, gloo here); launch returns the local rank's result only."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tcp_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert isinstance(res[r], list) and len(res[r]) == 1, res[r]
+        rank, size, a, ag = res[r][0]
+        assert (rank, size) == (r, 2)
+        assert a == [3.0, 6.0]
+        assert ag == [0.0, 1.0, 10.0]
+
+
+def test_tcp_descriptor_validation():
+    for bad in ("tcp:", "tcp:127.0.0.1:1", "tcp:127.0.0.1:x,rank=0", "tcp:127.0.0.1:1,rank=3", "bogus"):
+        with pytest.raises(bs.CommInitError):
+            bs.init(bad)
