@@ -156,6 +156,19 @@ def main():
     g["opnorm_a"] = a
     g["opnorm_l2"] = np.array([bs.run_inproc(2, lambda c: bs.opnorm(bs.distribute(a if c.rank == 0 else None, c)))[0]])
 
+    # .dsta matrix files written by the reference's own writer (cli.py:63-78)
+    import tempfile
+
+    from blockstat.cli import write_matrix
+
+    for dt, tag in ((np.float32, "f32"), (np.float64, "f64"), (np.int64, "i64")):
+        data = (np.random.Generator(np.random.Philox(4100)).random((3, 7)) * 10).astype(dt)
+        with tempfile.TemporaryDirectory() as d:
+            path = Path(d) / "m.dsta"
+            write_matrix(path, data)
+            g[f"dsta_{tag}_bytes"] = np.frombuffer(path.read_bytes(), dtype=np.uint8).copy()
+        g[f"dsta_{tag}_data"] = data
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({len(g)} arrays)")
 
