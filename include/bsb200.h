@@ -233,6 +233,19 @@ int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, int dtype,
                      const int* flags, void* work, int64_t work_bytes,
                      void* stream);
 
+/* Fused iteration pass (solvers.py:443-449 then :436 of the next iteration):
+ * grad = X_loc^T dmpd, beta <- S_lam(beta + sigma grad), xb_out[0:m] = X_loc beta
+ * (local partial, float64) and xb_out[m] = sum |beta| (local) -- the effects of
+ * bs_cox_grad_step(do_step = 1) followed by bs_cox_xbeta, with X streamed once
+ * (cooperative persistent kernel, column waves held in shared memory).
+ * allow_fused = 0 (or an unsupported shape) runs those two entry points instead;
+ * pass 0 when other kernels may share the device concurrently. */
+int64_t bs_cox_grad_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc);
+int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, int dtype,
+                      int64_t m, int64_t n_loc, void* grad, void* beta,
+                      double sigma, double lam, double* xb_out, const int* flags,
+                      int allow_fused, void* work, int64_t work_bytes, void* stream);
+
 /* trace entry (solvers.py:438-441): out_dev[0] = -loglik + lam * l1. */
 int bs_cox_objective(const double* loglik_dev, const double* l1_dev, double lam,
                      double* out_dev, void* stream);

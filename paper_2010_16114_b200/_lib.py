@@ -71,6 +71,8 @@ SIGNATURES = {
     "bs_cox_pi_delta": (_i, [_p, _p, _p, _p, _i, _i64, _i64, _i64, _p, _p, _p, _p, _i64, _p]),
     "bs_cox_grad_workspace": (_i64, [_i, _i64, _i64]),
     "bs_cox_grad_step": (_i, [_p, _i, _p, _i, _i64, _i64, _p, _p, _d, _d, _i, _p, _p, _p, _i64, _p]),
+    "bs_cox_grad_xbeta_workspace": (_i64, [_i, _i64, _i64]),
+    "bs_cox_grad_xbeta": (_i, [_p, _i, _p, _i, _i64, _i64, _p, _p, _d, _d, _p, _p, _i, _p, _i64, _p]),
     "bs_cox_objective": (_i, [_p, _p, _d, _p, _p]),
 }
 

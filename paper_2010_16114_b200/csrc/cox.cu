@@ -582,3 +582,316 @@ extern "C" int bs_cox_objective(const double* loglik_dev, const double* l1_dev, 
   cox_objective_kernel<<<1, 1, 0, as_stream(stream)>>>(loglik_dev, l1_dev, lam, out_dev);
   return check_launch("bs_cox_objective");
 }
+
+// ---------------------------------------------------------------------------
+// Fused iteration pass: scn p of iteration k and scn m of iteration k+1 in ONE
+// stream over X (solvers.py:443-449 then :436 of the next iteration).
+//
+// grad_j needs every row before beta_j(k+1) is known, and X beta(k+1) needs
+// beta(k+1); the reference therefore reads X twice per iteration.  Here the
+// columns are processed in waves of W; CTA c (one per SM, all co-resident, a
+// cooperative launch) owns the row segment [c*seg, (c+1)*seg) and keeps its
+// seg x W tile of the wave in shared memory:
+//   A(w)  bulk-copy the tile (HBM, once), partial dots with v = delta - pd for
+//         the wave's columns -> partials[w % 4][c][.], arrive on a grid counter
+//   B(w)  after all CTAs arrived: fold the column partials in CTA order (every
+//         CTA redundantly, identical values), beta_new = S_lam(beta + sigma g),
+//         then xb_seg += tile . beta_new straight from shared memory.
+// The tile of wave w+1 streams in while wave w waits at its counter.  Every fold
+// has a fixed order (rows within a CTA, CTAs in index order, columns in wave
+// order), so the result is deterministic.  X is read once per iteration instead
+// of twice.  Requires all CTAs resident (cooperative launch) and
+// m * sizeof(X) % 16 == 0; otherwise the caller's two-pass path runs.
+//
+// Status (r01, C4 100k x 200k fp32, 1 B200): correct (tests/test_cox_gpu.py), but
+// 55.5 ms/iteration against 29.6 ms for the two-pass path, so cox_fit only uses it
+// with BS_COX_FUSION=1.  Dropping the grid barrier and the partial fold still
+// leaves 41.8 ms: with one 86 KB tile in flight per SM while the other is consumed,
+// the stream is latency-bound (~13 GB/s per SM); the fold adds an L2 round trip
+// per wave.  Needed: >= 3 tiles in flight (W = 16), the barrier of wave w-1
+// waited after A(w), and the partial block fetched by a bulk copy.
+// ---------------------------------------------------------------------------
+
+constexpr int FU_THREADS = 256;
+constexpr int FU_RING = 4;  // partial/counter slots (a slot is reused 4 waves later)
+
+__device__ __forceinline__ void fu_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fu_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename TX, typename TB, int W>
+__global__ void __launch_bounds__(FU_THREADS, 1)
+cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg, const double* __restrict__ v,
+                 TB* __restrict__ grad, TB* __restrict__ beta, double sigma, double lam, double* __restrict__ xb_out,
+                 double* __restrict__ partials, unsigned int* __restrict__ counters, const int* flags) {
+  extern __shared__ __align__(128) uint8_t fu_smem[];
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;  // every CTA sees the same flag
+  const int G = int(gridDim.x), c = int(blockIdx.x), tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t r0 = int64_t(c) * seg;
+  const int rows = int(r0 >= m ? 0 : (m - r0 < seg ? m - r0 : seg));
+  const int64_t tile_elems = int64_t(W) * seg;
+  TX* tiles = reinterpret_cast<TX*>(fu_smem);                                          // [2][W][seg]
+  double* vseg = reinterpret_cast<double*>(fu_smem + 2 * tile_elems * sizeof(TX));     // [seg]
+  double* xbseg = vseg + seg;                                                          // [seg]
+  double* bnew = xbseg + seg;                                                          // [W]
+  double* bold = bnew + W;                                                             // [W]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bold + W);                              // [2]
+  __shared__ double l1_sh[FU_THREADS / 32];
+  __shared__ double gsum[FU_THREADS];
+  for (int i = tid; i < rows; i += FU_THREADS) {
+    vseg[i] = v[r0 + i];
+    xbseg[i] = 0.0;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bars + b))));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t nwaves = (n_loc + W - 1) / W;
+  auto issue = [&](int64_t w) {  // one thread: bulk copies of wave w's columns (this CTA's rows)
+    const int b = int(w & 1);
+    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(bars + b));
+    const int64_t j0 = w * W;
+    const int nc = int(n_loc - j0 < W ? n_loc - j0 : W);
+    const uint32_t bytes = uint32_t(rows) * uint32_t(sizeof(TX));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * uint32_t(nc))
+                 : "memory");
+    if (bytes)
+      for (int jj = 0; jj < nc; ++jj)
+        fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(tiles + int64_t(b) * tile_elems + int64_t(jj) * seg)),
+                     X + (j0 + jj) * m + r0, bytes, bar);
+  };
+  if (tid == 0 && nwaves > 0) issue(0);
+  double l1 = 0.0;
+  for (int64_t w = 0; w < nwaves; ++w) {
+    const int b = int(w & 1);
+    const int64_t j0 = w * W;
+    const int nc = int(n_loc - j0 < W ? n_loc - j0 : W);
+    if (tid == 0 && w + 1 < nwaves) issue(w + 1);  // its buffer was released at the end of wave w-1
+    if (tid < nc) bold[tid] = double(beta[j0 + tid]);  // before anyone can pass this wave's counter
+    fu_wait(static_cast<uint32_t>(__cvta_generic_to_shared(bars + b)), uint32_t(w >> 1) & 1u);
+    const TX* tile = tiles + int64_t(b) * tile_elems;
+    // ---- A(w): partial dots over this CTA's rows ----
+    double* part = partials + (int64_t(w % FU_RING) * G + c) * W;
+    for (int jj = wid; jj < W; jj += FU_THREADS / 32) {
+      double acc = 0.0;
+      if (jj < nc) {
+        const TX* col = tile + int64_t(jj) * seg;
+        for (int i = lane; i < rows; i += 32) acc = fma(double(col[i]), vseg[i], acc);
+      }
+      acc = warp_sum(acc);
+      if (lane == 0) part[jj] = acc;
+    }
+    __syncthreads();
+    unsigned int* ctr = counters + (w % FU_RING);
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(ctr, 1u);
+      const unsigned int target = unsigned(G) * unsigned(w / FU_RING + 1);
+      uint64_t t0 = 0;
+      for (uint32_t spin = 0; ld_acquire_u32(ctr) < target; ++spin) {
+        __nanosleep(64);
+        if ((spin & 4095) == 4095) {
+          uint64_t now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (t0 == 0) t0 = now;
+          else if (now - t0 > 10000000000ULL) __trap();
+        }
+      }
+    }
+    __syncthreads();
+    // ---- B(w): column gradients (CTA order), prox step, xb += tile . beta_new ----
+    {  // fold partials[.][c'][col] over CTAs c' in order: 256/W threads per column take
+       // consecutive CTA chunks (loads batched 8 at a time), then chunk sums in order
+      constexpr int GROUPS = FU_THREADS / W;
+      const int col = tid % W, grp = tid / W;
+      const int chunk = (G + GROUPS - 1) / GROUPS;
+      const int k0 = grp * chunk, k1 = min(G, k0 + chunk);
+      const double* pc = partials + int64_t(w % FU_RING) * G * W + col;
+      double s = 0.0;
+      for (int k = k0; k < k1; k += 8) {
+        double t[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) t[u] = (k + u < k1) ? __ldcg(pc + int64_t(k + u) * W) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += t[u];
+      }
+      gsum[grp * W + col] = s;
+    }
+    __syncthreads();
+    if (tid < nc) {
+      constexpr int GROUPS = FU_THREADS / W;
+      double g = 0.0;
+      for (int k = 0; k < GROUPS; ++k) g += gsum[k * W + tid];
+      const TB gt = TB(g);
+      // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
+      const TB x = TB(bold[tid]) + TB(sigma) * gt;
+      const TB mag = fabs(x) - TB(lam);
+      const TB bn = mag > TB(0) ? copysign(mag, x) : TB(0);
+      bnew[tid] = double(bn);
+      l1 += fabs(double(bn));
+      if (c == 0) {
+        grad[j0 + tid] = gt;
+        beta[j0 + tid] = bn;
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < rows; i += FU_THREADS) {
+      double acc = xbseg[i];
+      for (int jj = 0; jj < nc; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[jj], acc);
+      xbseg[i] = acc;
+    }
+    __syncthreads();  // tile buffer b and bnew are free again
+  }
+  for (int i = tid; i < rows; i += FU_THREADS) xb_out[r0 + i] = xbseg[i];
+  if (c == 0) {  // ||beta_new||_1 in a fixed order: threads by column residue, warps in order
+    const double s = warp_sum(l1);
+    if (lane == 0) l1_sh[wid] = s;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int k = 0; k < FU_THREADS / 32; ++k) t += l1_sh[k];
+      xb_out[m] = t;
+    }
+  }
+}
+
+struct FuPlan {
+  bool ok;
+  int grid, W;
+  int64_t seg;
+  size_t smem;
+};
+
+static FuPlan fu_plan(int xdtype, int64_t m, int64_t n_loc) {
+  FuPlan p{false, 0, 0, 0, 0};
+  const int es = xsize(xdtype);
+  if (m <= 0 || n_loc <= 0 || (m * es) % 16) return p;
+  int dev = 0, coop = 0, maxsm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (!coop) return p;
+  const int G = num_sms();
+  const int64_t align = 16 / es;
+  const int64_t seg = ceil_div(ceil_div(m, G), align) * align;
+  const int64_t budget = int64_t(maxsm) - 2048;
+  for (int W = 32; W >= 4; W /= 2) {
+    const int64_t need = 2 * int64_t(W) * seg * es + 2 * seg * 8 + 2 * W * 8 + 64;
+    if (need <= budget) {
+      p.ok = true;
+      p.grid = int(std::min<int64_t>(G, ceil_div(m, seg)));
+      p.W = W;
+      p.seg = seg;
+      p.smem = size_t(need);
+      return p;
+    }
+  }
+  return p;
+}
+
+template <typename TX, typename TB, int W>
+static int launch_fused(const void* X, int64_t m, int64_t n_loc, const FuPlan& p, const double* v, void* grad,
+                        void* beta, double sigma, double lam, double* xb_out, double* partials, unsigned int* counters,
+                        const int* flags, cudaStream_t st) {
+  auto kern = cox_fused_kernel<TX, TB, W>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem));
+  const TX* Xp = static_cast<const TX*>(X);
+  int64_t seg = p.seg;
+  TB* g = static_cast<TB*>(grad);
+  TB* b = static_cast<TB*>(beta);
+  void* args[] = {&Xp, &m, &n_loc, &seg, &v, &g, &b, &sigma, &lam, &xb_out, &partials, &counters, &flags};
+  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(p.grid), dim3(FU_THREADS),
+                                              args, p.smem, st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("bs_cox_grad_xbeta: cooperative launch failed: %s", cudaGetErrorString(e));
+    return BS_ECUDA;
+  }
+  return BS_OK;
+}
+
+template <typename TX, typename TB>
+static int dispatch_fused(const void* X, int64_t m, int64_t n_loc, const FuPlan& p, const double* v, void* grad,
+                          void* beta, double sigma, double lam, double* xb_out, double* partials,
+                          unsigned int* counters, const int* flags, cudaStream_t st) {
+  switch (p.W) {
+    case 32: return launch_fused<TX, TB, 32>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
+    case 16: return launch_fused<TX, TB, 16>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
+    case 8: return launch_fused<TX, TB, 8>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
+    default: return launch_fused<TX, TB, 4>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
+  }
+}
+
+static int64_t fused_ws(const FuPlan& p) {
+  return ws_bytes<unsigned int>(FU_RING) + ws_bytes<double>(int64_t(FU_RING) * p.grid * p.W);
+}
+
+extern "C" int64_t bs_cox_grad_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) {
+  const FuPlan p = fu_plan(xdtype, m, n_loc);
+  const int64_t two = bs_cox_grad_workspace(xdtype, m, n_loc) + bs_cox_xbeta_workspace(xdtype, m, n_loc) + 512;
+  return std::max<int64_t>(p.ok ? fused_ws(p) : 0, two);
+}
+
+extern "C" int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, int dtype, int64_t m, int64_t n_loc,
+                                 void* grad, void* beta, double sigma, double lam, double* xb_out, const int* flags,
+                                 int allow_fused, void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  cudaStream_t st = as_stream(stream);
+  if (m < 0 || n_loc < 0) { set_error("bs_cox_grad_xbeta: negative shape"); return BS_EINVAL; }
+  const FuPlan p = fu_plan(xdtype, m, n_loc);
+  const bool fuse = allow_fused && p.ok && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                    (dtype == BS_F32 || dtype == BS_F64) &&
+                    (xdtype == BS_F32 || xdtype == BS_F64 || xdtype == BS_I8);
+  if (!fuse) {
+    // two passes: scn p + prox (l1 -> xb_out[m]), then scn m with the new beta
+    Workspace ws(work, work_bytes);
+    Workspace wg = ws.split(bs_cox_grad_workspace(xdtype, m, n_loc));
+    Workspace wx = ws.rest();
+    int rc = bs_cox_grad_step(X, xdtype, dmpd, dtype, m, n_loc, grad, beta, sigma, lam, 1, xb_out + m, flags, wg.base,
+                              wg.size, stream);
+    if (rc != BS_OK) return rc;
+    return bs_cox_xbeta(X, xdtype, beta, dtype, m, n_loc, xb_out, wx.base, wx.size, stream);
+  }
+  Workspace ws(work, work_bytes);
+  unsigned int* counters = ws.take<unsigned int>(FU_RING);
+  double* partials = ws.take<double>(int64_t(FU_RING) * p.grid * p.W);
+  if (!counters || !partials) { set_error("bs_cox_grad_xbeta: workspace too small"); return BS_EWORK; }
+  if (cudaMemsetAsync(counters, 0, FU_RING * sizeof(unsigned int), st) != cudaSuccess) {
+    set_error("bs_cox_grad_xbeta: cudaMemsetAsync failed");
+    return BS_ECUDA;
+  }
+  int rc;
+#define BS_FU(TXT, TBT) \
+  rc = dispatch_fused<TXT, TBT>(X, m, n_loc, p, dmpd, grad, beta, sigma, lam, xb_out, partials, counters, flags, st)
+  if (dtype == BS_F64) {
+    if (xdtype == BS_F64) BS_FU(double, double);
+    else if (xdtype == BS_F32) BS_FU(float, double);
+    else BS_FU(int8_t, double);
+  } else {
+    if (xdtype == BS_F32) BS_FU(float, float);
+    else if (xdtype == BS_F64) BS_FU(double, float);
+    else BS_FU(int8_t, float);
+  }
+#undef BS_FU
+  if (rc != BS_OK) return rc;
+  return check_launch("bs_cox_grad_xbeta", 1);
+}

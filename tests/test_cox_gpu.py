@@ -4,6 +4,7 @@ import warnings
 
 import numpy as np
 import pytest
+import torch
 
 import paper_2010_16114_b200 as bs
 from oracle import blockstat_oracle as orc
@@ -254,3 +255,36 @@ def test_cox_unpenalized_gradient_vanishes_at_optimum():
 
     for g in bs.run_inproc(2, fn):
         assert g <= 1e-4
+
+
+@pytest.mark.parametrize("xdt,bdt,m,n", [(torch.float32, torch.float32, 4004, 777), (torch.float64, torch.float64, 3002, 301),
+                                         (torch.int8, torch.float32, 8000, 250), (torch.float32, torch.float64, 5000, 33)])
+def test_fused_grad_xbeta_pass_matches_two_pass(xdt, bdt, m, n):
+    """bs_cox_grad_xbeta: the cooperative one-stream pass (allow_fused=1) gives the same
+    grad, prox step, ||beta||_1 and X beta_new as bs_cox_grad_step + bs_cox_xbeta."""
+    from paper_2010_16114_b200 import _lib
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    if xdt == torch.int8:
+        X = torch.randint(0, 3, (n, m), generator=g, device="cuda", dtype=torch.int8)
+    else:
+        X = torch.randn(n, m, generator=g, device="cuda", dtype=xdt)  # column j = X[j]
+    v = torch.randn(m, generator=g, device="cuda", dtype=torch.float64)
+    beta0 = torch.randn(n, generator=g, device="cuda", dtype=bdt) * 0.1
+    flags = torch.zeros(1, dtype=torch.int32, device="cuda")
+    xc, bc = _lib.dtype_code(X.dtype), _lib.dtype_code(bdt)
+    ws = torch.zeros(_lib.query("bs_cox_grad_xbeta_workspace", xc, m, n), dtype=torch.uint8, device="cuda")
+    out = {}
+    for fused in (0, 1):
+        beta = beta0.clone()
+        grad = torch.empty_like(beta)
+        xb = torch.full((m + 1,), float("nan"), dtype=torch.float64, device="cuda")
+        _lib.call("bs_cox_grad_xbeta", _lib.ptr(X), xc, _lib.ptr(v), bc, m, n, _lib.ptr(grad), _lib.ptr(beta),
+                  1e-4, 0.1, _lib.ptr(xb), _lib.ptr(flags), fused, _lib.ptr(ws), ws.numel(), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        out[fused] = (grad.double().cpu().numpy(), beta.double().cpu().numpy(), xb.cpu().numpy())
+    tol = 1e-12 if bdt == torch.float64 else 1e-5
+    for a, b in zip(out[0], out[1]):
+        np.testing.assert_allclose(b, a, rtol=tol, atol=tol * max(1.0, np.abs(a).max()))
+    assert np.count_nonzero(out[1][1]) < n  # the threshold zeroed some coordinates
