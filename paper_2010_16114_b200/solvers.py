@@ -699,18 +699,23 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
     grad = _flat_local(s.grad)
     Xf = _flat_local(x)
     pp, pn = s._work.args("pd", _lib.query("bs_cox_pi_delta_workspace", m))
-    gp, gn = s._work.args("grad_xbeta", _lib.query("bs_cox_grad_xbeta_workspace", xcode, m, n_loc))
+    gp, gn = s._work.args("grad", _lib.query("bs_cox_grad_workspace", xcode, m, n_loc))
     comm = x.comm
     # The fused pass (one X stream per iteration) is opt-in until it beats the two-pass
     # path (see cox.cu); it spins on grid-wide counters, so never with other ranks'
     # kernels sharing this GPU.
     fuse = int(os.environ.get("BS_COX_FUSION") == "1" and dev.type == "cuda"
                and (comm.backend != "inproc" or comm.size <= torch.cuda.device_count()))
+    if fuse:
+        fp, fn_ = s._work.args("grad_xbeta", _lib.query("bs_cox_grad_xbeta_workspace", xcode, m, n_loc))
     host_trace = []
     ran = iters
-    _xbeta(s, beta)                                             # scn m + ||beta||_1 of the entering iterate
+    if fuse:
+        _xbeta(s, beta)                                         # the fused pass supplies the later ones
     for it in range(iters):
-        if it > 0 and comm.size > 1:
+        if not fuse:
+            _xbeta(s, beta)                                     # scn m + ||beta||_1 (solvers.py:436)
+        elif it > 0 and comm.size > 1:
             comm.allreduce(xb, ReduceOp.SUM)                    # X beta partials of the fused pass
         _risk(s)                                                # solvers.py:437
         fhist[it:it + 1].copy_(flags)
@@ -728,9 +733,12 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
                     break
         _lib.call("bs_cox_pi_delta", _lib.ptr(s.w), _lib.ptr(s.W), _lib.ptr(s.delta), _cuts_ptr(s), code, m, 0, m,
                   _lib.ptr(s.pd), _lib.ptr(dmpd), _lib.ptr(flags), pp, pn, st)
-        # scn p + prox step, and scn m of the next iteration, in one pass over X
-        _lib.call("bs_cox_grad_xbeta", _lib.ptr(Xf), xcode, _lib.ptr(dmpd), code, m, n_loc, _lib.ptr(grad),
-                  _lib.ptr(beta), sigma, lam, _lib.ptr(xb), _lib.ptr(flags), fuse, gp, gn, st)
+        if fuse:  # scn p + prox step and scn m of the next iteration in one pass over X
+            _lib.call("bs_cox_grad_xbeta", _lib.ptr(Xf), xcode, _lib.ptr(dmpd), code, m, n_loc, _lib.ptr(grad),
+                      _lib.ptr(beta), sigma, lam, _lib.ptr(xb), _lib.ptr(flags), 1, fp, fn_, st)
+        else:     # scn p + prox (solvers.py:443-449)
+            _lib.call("bs_cox_grad_step", _lib.ptr(Xf), xcode, _lib.ptr(dmpd), code, m, n_loc, _lib.ptr(grad),
+                      _lib.ptr(beta), sigma, lam, 1, _at(xb, m), _lib.ptr(flags), gp, gn, st)
     fl_all = fhist[:max(ran, 1)].cpu().numpy() if ran else np.zeros(0, dtype=np.int32)
     bad = np.nonzero(fl_all & _lib.BS_FLAG_NONFINITE)[0] if fl_all.size else []
     stop = int(bad[0]) if len(bad) else ran
