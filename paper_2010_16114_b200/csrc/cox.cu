@@ -620,14 +620,21 @@ __device__ __forceinline__ void fu_bulk_load(uint32_t dst, const void* src, uint
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
-__device__ __forceinline__ void fu_wait(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ void fu_wait(uint32_t bar, uint32_t parity) {  // traps after ~10 s
   uint32_t done = 0;
-  while (!done) {
+  uint64_t t0 = 0;
+  for (uint32_t spin = 0; !done; ++spin) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+    if (!done && (spin & 1023) == 1023) {
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 10000000000ULL) __trap();
+    }
   }
 }
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
@@ -641,125 +648,136 @@ __global__ void __launch_bounds__(FU_THREADS, 1)
 cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg, const double* __restrict__ v,
                  TB* __restrict__ grad, TB* __restrict__ beta, double sigma, double lam, double* __restrict__ xb_out,
                  double* __restrict__ partials, unsigned int* __restrict__ counters, const int* flags) {
+  constexpr int NB = 3;  // tile buffers: wave w in A, wave w-1 in B, wave w+1 streaming in
   extern __shared__ __align__(128) uint8_t fu_smem[];
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;  // every CTA sees the same flag
   const int G = int(gridDim.x), c = int(blockIdx.x), tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t r0 = int64_t(c) * seg;
   const int rows = int(r0 >= m ? 0 : (m - r0 < seg ? m - r0 : seg));
   const int64_t tile_elems = int64_t(W) * seg;
-  TX* tiles = reinterpret_cast<TX*>(fu_smem);                                          // [2][W][seg]
-  double* vseg = reinterpret_cast<double*>(fu_smem + 2 * tile_elems * sizeof(TX));     // [seg]
-  double* xbseg = vseg + seg;                                                          // [seg]
-  double* bnew = xbseg + seg;                                                          // [W]
-  double* bold = bnew + W;                                                             // [W]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(bold + W);                              // [2]
+  TX* tiles = reinterpret_cast<TX*>(fu_smem);                                           // [NB][W][seg]
+  double* pbuf = reinterpret_cast<double*>(fu_smem + NB * tile_elems * sizeof(TX));     // [2][G][W]
+  double* vseg = pbuf + 2 * G * W;                                                      // [seg]
+  double* xbseg = vseg + seg;                                                           // [seg]
+  double* bold = xbseg + seg;                                                           // [NB][W]
+  double* bnew = bold + NB * W;                                                         // [W]
+  double* gsum = bnew + W;                                                              // [FU_THREADS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gsum + FU_THREADS);                      // tile[NB], part[2]
   __shared__ double l1_sh[FU_THREADS / 32];
-  __shared__ double gsum[FU_THREADS];
+  auto bar_u32 = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(bars + i)); };
   for (int i = tid; i < rows; i += FU_THREADS) {
     vseg[i] = v[r0 + i];
     xbseg[i] = 0.0;
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bars + b))));
+    for (int i = 0; i < NB + 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_u32(i)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int64_t nwaves = (n_loc + W - 1) / W;
-  auto issue = [&](int64_t w) {  // one thread: bulk copies of wave w's columns (this CTA's rows)
-    const int b = int(w & 1);
-    const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(bars + b));
-    const int64_t j0 = w * W;
-    const int nc = int(n_loc - j0 < W ? n_loc - j0 : W);
+  auto ncols = [&](int64_t w) { return int(n_loc - w * W < W ? n_loc - w * W : W); };
+  auto issue_tile = [&](int64_t w) {  // one thread: bulk copies of wave w's columns (this CTA's rows)
+    const int b = int(w % NB);
+    const int nc = ncols(w);
     const uint32_t bytes = uint32_t(rows) * uint32_t(sizeof(TX));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes * uint32_t(nc))
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_u32(b)), "r"(bytes * uint32_t(nc))
                  : "memory");
     if (bytes)
       for (int jj = 0; jj < nc; ++jj)
-        fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(tiles + int64_t(b) * tile_elems + int64_t(jj) * seg)),
-                     X + (j0 + jj) * m + r0, bytes, bar);
+        fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(tiles + b * tile_elems + int64_t(jj) * seg)),
+                     X + (w * W + jj) * m + r0, bytes, bar_u32(b));
   };
-  if (tid == 0 && nwaves > 0) issue(0);
-  double l1 = 0.0;
-  for (int64_t w = 0; w < nwaves; ++w) {
-    const int b = int(w & 1);
-    const int64_t j0 = w * W;
-    const int nc = int(n_loc - j0 < W ? n_loc - j0 : W);
-    if (tid == 0 && w + 1 < nwaves) issue(w + 1);  // its buffer was released at the end of wave w-1
-    if (tid < nc) bold[tid] = double(beta[j0 + tid]);  // before anyone can pass this wave's counter
-    fu_wait(static_cast<uint32_t>(__cvta_generic_to_shared(bars + b)), uint32_t(w >> 1) & 1u);
-    const TX* tile = tiles + int64_t(b) * tile_elems;
-    // ---- A(w): partial dots over this CTA's rows ----
-    double* part = partials + (int64_t(w % FU_RING) * G + c) * W;
-    for (int jj = wid; jj < W; jj += FU_THREADS / 32) {
-      double acc = 0.0;
-      if (jj < nc) {
-        const TX* col = tile + int64_t(jj) * seg;
-        for (int i = lane; i < rows; i += 32) acc = fma(double(col[i]), vseg[i], acc);
+  auto fetch_partials = [&](int64_t u) {  // one thread: wait for wave u's grid counter, copy its partial block
+    unsigned int* ctr = counters + (u % FU_RING);
+    const unsigned int target = unsigned(G) * unsigned(u / FU_RING + 1);
+    uint64_t t0 = 0;
+    for (uint32_t spin = 0; ld_acquire_u32(ctr) < target; ++spin) {
+      __nanosleep(32);
+      if ((spin & 4095) == 4095) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        else if (now - t0 > 10000000000ULL) __trap();
       }
-      acc = warp_sum(acc);
-      if (lane == 0) part[jj] = acc;
     }
-    __syncthreads();
-    unsigned int* ctr = counters + (w % FU_RING);
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(ctr, 1u);
-      const unsigned int target = unsigned(G) * unsigned(w / FU_RING + 1);
-      uint64_t t0 = 0;
-      for (uint32_t spin = 0; ld_acquire_u32(ctr) < target; ++spin) {
-        __nanosleep(64);
-        if ((spin & 4095) == 4095) {
-          uint64_t now;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-          if (t0 == 0) t0 = now;
-          else if (now - t0 > 10000000000ULL) __trap();
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk-copy reads
+    const uint32_t bytes = uint32_t(G) * W * 8u;
+    const int pb = int(u & 1);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_u32(NB + pb)), "r"(bytes)
+                 : "memory");
+    fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(pbuf + int64_t(pb) * G * W)),
+                 partials + int64_t(u % FU_RING) * G * W, bytes, bar_u32(NB + pb));
+  };
+  double l1 = 0.0;
+  if (tid == 0)
+    for (int64_t w = 0; w < nwaves && w < NB; ++w) issue_tile(w);
+  for (int64_t w = 0; w <= nwaves; ++w) {
+    const int64_t u = w - 1;  // the wave finished (B) in this iteration
+    if (tid == 0 && u >= 0) fetch_partials(u);
+    if (w < nwaves) {
+      // ---- A(w): partial dots of the wave's columns over this CTA's rows ----
+      const int b = int(w % NB), nc = ncols(w);
+      if (tid < nc) bold[b * W + tid] = double(beta[w * W + tid]);  // before this wave's counter can complete
+      fu_wait(bar_u32(b), uint32_t((w / NB) & 1));
+      const TX* tile = tiles + b * tile_elems;
+      double* part = partials + (int64_t(w % FU_RING) * G + c) * W;
+      for (int jj = wid; jj < W; jj += FU_THREADS / 32) {
+        double acc = 0.0;
+        if (jj < nc) {
+          const TX* col = tile + int64_t(jj) * seg;
+          for (int i = lane; i < rows; i += 32) acc = fma(double(col[i]), vseg[i], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) part[jj] = acc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(counters + (w % FU_RING), 1u);
+      }
+    }
+    if (u >= 0) {
+      // ---- B(u): fold the column partials in CTA order, prox step, xb += tile . beta_new ----
+      const int b = int(u % NB), nc = ncols(u);
+      fu_wait(bar_u32(NB + int(u & 1)), uint32_t((u >> 1) & 1));
+      const double* pb = pbuf + int64_t(u & 1) * G * W;
+      {
+        constexpr int GROUPS = FU_THREADS / W;
+        const int col = tid % W, grp = tid / W;
+        const int chunk = (G + GROUPS - 1) / GROUPS;
+        const int k0 = grp * chunk, k1 = min(G, k0 + chunk);
+        double s = 0.0;
+        for (int k = k0; k < k1; ++k) s += pb[k * W + col];
+        gsum[grp * W + col] = s;
+      }
+      __syncthreads();
+      if (tid < nc) {
+        constexpr int GROUPS = FU_THREADS / W;
+        double g = 0.0;
+        for (int k = 0; k < GROUPS; ++k) g += gsum[k * W + tid];
+        const TB gt = TB(g);
+        // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
+        const TB x = TB(bold[b * W + tid]) + TB(sigma) * gt;
+        const TB mag = fabs(x) - TB(lam);
+        const TB bn = mag > TB(0) ? copysign(mag, x) : TB(0);
+        bnew[tid] = double(bn);
+        l1 += fabs(double(bn));
+        if (c == 0) {
+          grad[u * W + tid] = gt;
+          beta[u * W + tid] = bn;
         }
       }
-    }
-    __syncthreads();
-    // ---- B(w): column gradients (CTA order), prox step, xb += tile . beta_new ----
-    {  // fold partials[.][c'][col] over CTAs c' in order: 256/W threads per column take
-       // consecutive CTA chunks (loads batched 8 at a time), then chunk sums in order
-      constexpr int GROUPS = FU_THREADS / W;
-      const int col = tid % W, grp = tid / W;
-      const int chunk = (G + GROUPS - 1) / GROUPS;
-      const int k0 = grp * chunk, k1 = min(G, k0 + chunk);
-      const double* pc = partials + int64_t(w % FU_RING) * G * W + col;
-      double s = 0.0;
-      for (int k = k0; k < k1; k += 8) {
-        double t[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) t[u] = (k + u < k1) ? __ldcg(pc + int64_t(k + u) * W) : 0.0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s += t[u];
+      __syncthreads();
+      const TX* tile = tiles + b * tile_elems;
+      for (int i = tid; i < rows; i += FU_THREADS) {
+        double acc = xbseg[i];
+#pragma unroll 4
+        for (int jj = 0; jj < nc; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[jj], acc);
+        xbseg[i] = acc;
       }
-      gsum[grp * W + col] = s;
+      __syncthreads();  // tile buffer b, bnew and gsum are free again
+      if (tid == 0 && u + NB < nwaves) issue_tile(u + NB);
     }
-    __syncthreads();
-    if (tid < nc) {
-      constexpr int GROUPS = FU_THREADS / W;
-      double g = 0.0;
-      for (int k = 0; k < GROUPS; ++k) g += gsum[k * W + tid];
-      const TB gt = TB(g);
-      // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
-      const TB x = TB(bold[tid]) + TB(sigma) * gt;
-      const TB mag = fabs(x) - TB(lam);
-      const TB bn = mag > TB(0) ? copysign(mag, x) : TB(0);
-      bnew[tid] = double(bn);
-      l1 += fabs(double(bn));
-      if (c == 0) {
-        grad[j0 + tid] = gt;
-        beta[j0 + tid] = bn;
-      }
-    }
-    __syncthreads();
-    for (int i = tid; i < rows; i += FU_THREADS) {
-      double acc = xbseg[i];
-      for (int jj = 0; jj < nc; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[jj], acc);
-      xbseg[i] = acc;
-    }
-    __syncthreads();  // tile buffer b and bnew are free again
   }
   for (int i = tid; i < rows; i += FU_THREADS) xb_out[r0 + i] = xbseg[i];
   if (c == 0) {  // ||beta_new||_1 in a fixed order: threads by column residue, warps in order
@@ -794,8 +812,9 @@ static FuPlan fu_plan(int xdtype, int64_t m, int64_t n_loc) {
   const int64_t align = 16 / es;
   const int64_t seg = ceil_div(ceil_div(m, G), align) * align;
   const int64_t budget = int64_t(maxsm) - 2048;
-  for (int W = 32; W >= 4; W /= 2) {
-    const int64_t need = 2 * int64_t(W) * seg * es + 2 * seg * 8 + 2 * W * 8 + 64;
+  for (int W = 16; W >= 4; W /= 2) {
+    const int64_t need = 3 * int64_t(W) * seg * es + 2 * int64_t(G) * W * 8 + 2 * seg * 8 + 4 * W * 8 +
+                         FU_THREADS * 8 + 64;
     if (need <= budget) {
       p.ok = true;
       p.grid = int(std::min<int64_t>(G, ceil_div(m, seg)));
@@ -834,7 +853,6 @@ static int dispatch_fused(const void* X, int64_t m, int64_t n_loc, const FuPlan&
                           void* beta, double sigma, double lam, double* xb_out, double* partials,
                           unsigned int* counters, const int* flags, cudaStream_t st) {
   switch (p.W) {
-    case 32: return launch_fused<TX, TB, 32>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
     case 16: return launch_fused<TX, TB, 16>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
     case 8: return launch_fused<TX, TB, 8>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
     default: return launch_fused<TX, TB, 4>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
