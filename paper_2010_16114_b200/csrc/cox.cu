@@ -584,41 +584,49 @@ extern "C" int bs_cox_objective(const double* loglik_dev, const double* l1_dev, 
 }
 
 // ---------------------------------------------------------------------------
-// Fused iteration pass: scn p of iteration k and scn m of iteration k+1 in ONE
-// stream over X (solvers.py:443-449 then :436 of the next iteration).
+// Fused iteration pass: scn p of iteration k and scn m of iteration k+1 with ONE
+// stream of X from HBM (solvers.py:443-449 then :436 of the next iteration).
 //
 // grad_j needs every row before beta_j(k+1) is known, and X beta(k+1) needs
 // beta(k+1); the reference therefore reads X twice per iteration.  Here the
-// columns are processed in waves of W; CTA c (one per SM, all co-resident, a
-// cooperative launch) owns the row segment [c*seg, (c+1)*seg) and keeps its
-// seg x W tile of the wave in shared memory:
-//   A(w)  bulk-copy the tile (HBM, once), partial dots with v = delta - pd for
-//         the wave's columns -> partials[w % 4][c][.], arrive on a grid counter
-//   B(w)  after all CTAs arrived: fold the column partials in CTA order (every
-//         CTA redundantly, identical values), beta_new = S_lam(beta + sigma g),
-//         then xb_seg += tile . beta_new straight from shared memory.
-// The tile of wave w+1 streams in while wave w waits at its counter.  Every fold
-// has a fixed order (rows within a CTA, CTAs in index order, columns in wave
-// order), so the result is deterministic.  X is read once per iteration instead
-// of twice.  Requires all CTAs resident (cooperative launch) and
+// columns are processed in waves of W; CTA c (one per SM, all co-resident: a
+// cooperative launch) owns the row segment [c*seg, (c+1)*seg):
+//   A(w)  a producer warp streams the wave's columns (this CTA's rows) from HBM
+//         through a shared-memory ring (bulk copies, L2 evict_last); eight
+//         consumer warps form the partial dots with v = delta - pd ->
+//         partials[w % R][c][.], then arrive on the wave's grid counter
+//   B(w-L) L = 2 waves later (the counter is long complete, so no one waits):
+//         fold the column partials in CTA order (every CTA, identical values),
+//         beta_new = S_lam(beta + sigma g), and xb_seg += X[seg, wave] beta_new
+//         with the wave re-read from L2 by the same producer into a second ring
+//         (3 waves x 148 CTAs x seg x W bytes stay resident: 38 MB at C4).
+// HBM is read once per iteration; every fold has a fixed order (rows in a CTA,
+// CTAs by index, columns in wave order), so results are deterministic.  Needs
 // m * sizeof(X) % 16 == 0; otherwise the caller's two-pass path runs.
 //
-// Status (r01, C4 100k x 200k fp32, 1 B200): correct (tests/test_cox_gpu.py), but
-// 55.5 ms/iteration against 29.6 ms for the two-pass path, so cox_fit only uses it
-// with BS_COX_FUSION=1.  Dropping the grid barrier and the partial fold still
-// leaves 41.8 ms: with one 86 KB tile in flight per SM while the other is consumed,
-// the stream is latency-bound (~13 GB/s per SM); the fold adds an L2 round trip
-// per wave.  Needed: >= 3 tiles in flight (W = 16), the barrier of wave w-1
-// waited after A(w), and the partial block fetched by a bulk copy.
+// Status (r01): correct (tests/test_cox_gpu.py, NCCL parity at 4 GPUs) but slower
+// than the two-pass path at C4 (58 ms vs 28 ms per iteration), so cox_fit uses it
+// only with BS_COX_FUSION=1.  ncu (profiles/r01_ncu_cox_fused_summary.txt): 27
+// instructions per X element against ~3 DFMA/F2F/LDS of real work -- loop and
+// address overhead of the runtime-bounded row/column loops with 8 consumer warps
+// per SM; issue slots 27% busy.  Next: compile-time stage loops, v in registers,
+// more consumer warps.
 // ---------------------------------------------------------------------------
 
-constexpr int FU_THREADS = 256;
-constexpr int FU_RING = 4;  // partial/counter slots (a slot is reused 4 waves later)
+constexpr int FU_THREADS = 288;     // warp 0 producer, warps 1..8 consumers
+constexpr int FU_CONS = 256;
+constexpr int FU_RING = 8;          // partial / counter slots (>= 2L + 2)
+constexpr int FU_LAG = 2;           // waves between A(w) and B(w)
+constexpr int FU_CW = 8;            // columns per ring stage (one per consumer warp)
+constexpr int FU_STAGES = 3;        // A ring (HBM stream)
+constexpr int FU_BSTAGES = 2;       // B ring (L2 re-read of wave w - LAG)
 
-__device__ __forceinline__ void fu_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+__device__ __forceinline__ void fu_bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                             uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
 }
 __device__ __forceinline__ void fu_wait(uint32_t bar, uint32_t parity) {  // traps after ~10 s
   uint32_t done = 0;
@@ -642,151 +650,216 @@ __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
 template <typename TX, typename TB, int W>
 __global__ void __launch_bounds__(FU_THREADS, 1)
 cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg, const double* __restrict__ v,
                  TB* __restrict__ grad, TB* __restrict__ beta, double sigma, double lam, double* __restrict__ xb_out,
                  double* __restrict__ partials, unsigned int* __restrict__ counters, const int* flags) {
-  constexpr int NB = 3;  // tile buffers: wave w in A, wave w-1 in B, wave w+1 streaming in
+  static_assert(W % FU_CW == 0, "a wave is whole ring stages");
+  constexpr int QPW = W / FU_CW;  // ring stages per wave
   extern __shared__ __align__(128) uint8_t fu_smem[];
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;  // every CTA sees the same flag
-  const int G = int(gridDim.x), c = int(blockIdx.x), tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = int(gridDim.x), c = int(blockIdx.x), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r0 = int64_t(c) * seg;
   const int rows = int(r0 >= m ? 0 : (m - r0 < seg ? m - r0 : seg));
-  const int64_t tile_elems = int64_t(W) * seg;
-  TX* tiles = reinterpret_cast<TX*>(fu_smem);                                           // [NB][W][seg]
-  double* pbuf = reinterpret_cast<double*>(fu_smem + NB * tile_elems * sizeof(TX));     // [2][G][W]
-  double* vseg = pbuf + 2 * G * W;                                                      // [seg]
-  double* xbseg = vseg + seg;                                                           // [seg]
-  double* bold = xbseg + seg;                                                           // [NB][W]
-  double* bnew = bold + NB * W;                                                         // [W]
-  double* gsum = bnew + W;                                                              // [FU_THREADS]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(gsum + FU_THREADS);                      // tile[NB], part[2]
-  __shared__ double l1_sh[FU_THREADS / 32];
+  const int64_t stage_elems = int64_t(FU_CW) * seg;
+  TX* ring = reinterpret_cast<TX*>(fu_smem);                                               // [STAGES][CW][seg]
+  TX* bring = ring + FU_STAGES * stage_elems;                                               // [BSTAGES][CW][seg]
+  double* pbuf = reinterpret_cast<double*>(fu_smem + (FU_STAGES + FU_BSTAGES) * stage_elems * sizeof(TX));  // [2][G][W]
+  double* vseg = pbuf + 2 * int64_t(G) * W;                                                 // [seg]
+  double* xbseg = vseg + seg;                                                               // [seg]
+  double* bold = xbseg + seg;                                                               // [LAG+1][W]
+  double* bnew = bold + (FU_LAG + 1) * W;                                                   // [W]
+  double* gsum = bnew + W;                                                                  // [FU_CONS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gsum + FU_CONS);  // full[S], empty[S], bfull[BS], bempty[BS], pfull[2], pempty[2]
+  constexpr int PB0 = 2 * FU_STAGES + 2 * FU_BSTAGES;
+  __shared__ double l1_sh[FU_CONS / 32];
   auto bar_u32 = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(bars + i)); };
+  const int64_t nwaves = (n_loc + W - 1) / W;
+  if (tid == 0) {
+    for (int i = 0; i < FU_STAGES; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_u32(i)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_u32(FU_STAGES + i)), "r"(FU_CONS / 32));
+    }
+    for (int i = 0; i < FU_BSTAGES; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_u32(2 * FU_STAGES + i)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_u32(2 * FU_STAGES + FU_BSTAGES + i)),
+                   "r"(FU_CONS / 32));
+    }
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_u32(PB0 + i)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_u32(PB0 + 2 + i)), "r"(FU_CONS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int i = tid; i < rows; i += FU_THREADS) {
     vseg[i] = v[r0 + i];
     xbseg[i] = 0.0;
   }
-  if (tid == 0) {
-    for (int i = 0; i < NB + 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_u32(i)));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
   __syncthreads();
-  const int64_t nwaves = (n_loc + W - 1) / W;
-  auto ncols = [&](int64_t w) { return int(n_loc - w * W < W ? n_loc - w * W : W); };
-  auto issue_tile = [&](int64_t w) {  // one thread: bulk copies of wave w's columns (this CTA's rows)
-    const int b = int(w % NB);
-    const int nc = ncols(w);
-    const uint32_t bytes = uint32_t(rows) * uint32_t(sizeof(TX));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_u32(b)), "r"(bytes * uint32_t(nc))
-                 : "memory");
-    if (bytes)
-      for (int jj = 0; jj < nc; ++jj)
-        fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(tiles + b * tile_elems + int64_t(jj) * seg)),
-                     X + (w * W + jj) * m + r0, bytes, bar_u32(b));
-  };
-  auto fetch_partials = [&](int64_t u) {  // one thread: wait for wave u's grid counter, copy its partial block
-    unsigned int* ctr = counters + (u % FU_RING);
-    const unsigned int target = unsigned(G) * unsigned(u / FU_RING + 1);
-    uint64_t t0 = 0;
-    for (uint32_t spin = 0; ld_acquire_u32(ctr) < target; ++spin) {
-      __nanosleep(32);
-      if ((spin & 4095) == 4095) {
-        uint64_t now;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-        if (t0 == 0) t0 = now;
-        else if (now - t0 > 10000000000ULL) __trap();
+
+  if (warp == 0) {
+    // ---------------- producer: every stage of every wave, in order ----------------
+    if (lane == 0) {
+      uint64_t keep, drop;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
+      const uint32_t bytes = uint32_t(rows) * uint32_t(sizeof(TX));
+      // one ring stage: columns j0 .. j0+CW of this CTA's rows into `dst`, completing on `full`
+      auto stage = [&](TX* dst, int64_t j0, uint32_t full, uint64_t pol) {
+        const int nc = int(n_loc - j0 <= 0 ? 0 : (n_loc - j0 < FU_CW ? n_loc - j0 : FU_CW));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"(bytes * uint32_t(nc))
+                     : "memory");
+        if (bytes)
+          for (int jj = 0; jj < nc; ++jj)
+            fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(dst + int64_t(jj) * seg)),
+                         X + (j0 + jj) * m + r0, bytes, full, pol);
+      };
+      int64_t k = 0, kb = 0;  // A / B stage sequences
+      for (int64_t w = 0; w < nwaves + FU_LAG; ++w) {
+        if (w < nwaves)
+          for (int q = 0; q < QPW; ++q, ++k) {  // A(w): from HBM, kept in L2 for B
+            const int s = int(k % FU_STAGES);
+            fu_wait(bar_u32(FU_STAGES + s), uint32_t((k / FU_STAGES) & 1) ^ 1u);
+            stage(ring + s * stage_elems, w * W + q * FU_CW, bar_u32(s), keep);
+          }
+        if (w >= FU_LAG) {
+          // wave u's grid counter (all CTAs' A(u) partials are out), then its partial block
+          const int64_t u = w - FU_LAG;
+          unsigned int* ctr = counters + (u % FU_RING);
+          const unsigned int target = unsigned(G) * unsigned(u / FU_RING + 1);
+          uint64_t t0 = 0;
+          for (uint32_t spin = 0; ld_acquire_u32(ctr) < target; ++spin) {
+            __nanosleep(32);
+            if ((spin & 4095) == 4095) {
+              uint64_t now;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+              if (t0 == 0) t0 = now;
+              else if (now - t0 > 10000000000ULL) __trap();
+            }
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          const int pb = int(u & 1);
+          fu_wait(bar_u32(PB0 + 2 + pb), uint32_t((u >> 1) & 1) ^ 1u);
+          const uint32_t pbytes = uint32_t(G) * W * 8u;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_u32(PB0 + pb)), "r"(pbytes)
+                       : "memory");
+          fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(pbuf + int64_t(pb) * G * W)),
+                       partials + int64_t(u % FU_RING) * G * W, pbytes, bar_u32(PB0 + pb), drop);
+        }
+        if (w >= FU_LAG)
+          for (int q = 0; q < QPW; ++q, ++kb) {  // B(w - LAG): the same columns again, from L2
+            const int s = int(kb % FU_BSTAGES);
+            fu_wait(bar_u32(2 * FU_STAGES + FU_BSTAGES + s), uint32_t((kb / FU_BSTAGES) & 1) ^ 1u);
+            stage(bring + s * stage_elems, (w - FU_LAG) * W + q * FU_CW, bar_u32(2 * FU_STAGES + s), drop);
+          }
       }
     }
-    asm volatile("fence.proxy.async.global;" ::: "memory");  // generic-proxy writes -> bulk-copy reads
-    const uint32_t bytes = uint32_t(G) * W * 8u;
-    const int pb = int(u & 1);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_u32(NB + pb)), "r"(bytes)
-                 : "memory");
-    fu_bulk_load(static_cast<uint32_t>(__cvta_generic_to_shared(pbuf + int64_t(pb) * G * W)),
-                 partials + int64_t(u % FU_RING) * G * W, bytes, bar_u32(NB + pb));
-  };
+    return;  // the consumers never sync with warp 0 again
+  }
+
+  // ---------------- consumers (warps 1..8) ----------------
+  const int ct = tid - 32, cw = warp - 1;  // consumer thread / warp index
   double l1 = 0.0;
-  if (tid == 0)
-    for (int64_t w = 0; w < nwaves && w < NB; ++w) issue_tile(w);
-  for (int64_t w = 0; w <= nwaves; ++w) {
-    const int64_t u = w - 1;  // the wave finished (B) in this iteration
-    if (tid == 0 && u >= 0) fetch_partials(u);
+  int64_t k = 0, kb = 0;
+  auto cons_sync = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+  for (int64_t w = 0; w < nwaves + FU_LAG; ++w) {
     if (w < nwaves) {
-      // ---- A(w): partial dots of the wave's columns over this CTA's rows ----
-      const int b = int(w % NB), nc = ncols(w);
-      if (tid < nc) bold[b * W + tid] = double(beta[w * W + tid]);  // before this wave's counter can complete
-      fu_wait(bar_u32(b), uint32_t((w / NB) & 1));
-      const TX* tile = tiles + b * tile_elems;
-      double* part = partials + (int64_t(w % FU_RING) * G + c) * W;
-      for (int jj = wid; jj < W; jj += FU_THREADS / 32) {
+      // ---- A(w) ----
+      const int slot = int(w % FU_RING);
+      if (ct < W && w * W + ct < n_loc) bold[int(w % (FU_LAG + 1)) * W + ct] = double(beta[w * W + ct]);
+      double* part = partials + (int64_t(slot) * G + c) * W;
+      for (int q = 0; q < QPW; ++q, ++k) {
+        const int s = int(k % FU_STAGES);
+        fu_wait(bar_u32(s), uint32_t((k / FU_STAGES) & 1));
+        const int64_t j = w * W + q * FU_CW + cw;
         double acc = 0.0;
-        if (jj < nc) {
-          const TX* col = tile + int64_t(jj) * seg;
-          for (int i = lane; i < rows; i += 32) acc = fma(double(col[i]), vseg[i], acc);
+        if (j < n_loc) {
+          const TX* col = ring + s * stage_elems + int64_t(cw) * seg;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int i = lane;
+          for (; i + 96 < rows; i += 128) {
+            a0 = fma(double(col[i]), vseg[i], a0);
+            a1 = fma(double(col[i + 32]), vseg[i + 32], a1);
+            a2 = fma(double(col[i + 64]), vseg[i + 64], a2);
+            a3 = fma(double(col[i + 96]), vseg[i + 96], a3);
+          }
+          for (; i < rows; i += 32) a0 = fma(double(col[i]), vseg[i], a0);
+          acc = (a0 + a1) + (a2 + a3);
         }
         acc = warp_sum(acc);
-        if (lane == 0) part[jj] = acc;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        __threadfence();
-        atomicAdd(counters + (w % FU_RING), 1u);
-      }
-    }
-    if (u >= 0) {
-      // ---- B(u): fold the column partials in CTA order, prox step, xb += tile . beta_new ----
-      const int b = int(u % NB), nc = ncols(u);
-      fu_wait(bar_u32(NB + int(u & 1)), uint32_t((u >> 1) & 1));
-      const double* pb = pbuf + int64_t(u & 1) * G * W;
-      {
-        constexpr int GROUPS = FU_THREADS / W;
-        const int col = tid % W, grp = tid / W;
-        const int chunk = (G + GROUPS - 1) / GROUPS;
-        const int k0 = grp * chunk, k1 = min(G, k0 + chunk);
-        double s = 0.0;
-        for (int k = k0; k < k1; ++k) s += pb[k * W + col];
-        gsum[grp * W + col] = s;
-      }
-      __syncthreads();
-      if (tid < nc) {
-        constexpr int GROUPS = FU_THREADS / W;
-        double g = 0.0;
-        for (int k = 0; k < GROUPS; ++k) g += gsum[k * W + tid];
-        const TB gt = TB(g);
-        // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
-        const TB x = TB(bold[b * W + tid]) + TB(sigma) * gt;
-        const TB mag = fabs(x) - TB(lam);
-        const TB bn = mag > TB(0) ? copysign(mag, x) : TB(0);
-        bnew[tid] = double(bn);
-        l1 += fabs(double(bn));
-        if (c == 0) {
-          grad[u * W + tid] = gt;
-          beta[u * W + tid] = bn;
+        if (lane == 0) {
+          part[q * FU_CW + cw] = acc;
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_u32(FU_STAGES + s)) : "memory");
         }
       }
-      __syncthreads();
-      const TX* tile = tiles + b * tile_elems;
-      for (int i = tid; i < rows; i += FU_THREADS) {
-        double acc = xbseg[i];
-#pragma unroll 4
-        for (int jj = 0; jj < nc; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[jj], acc);
-        xbseg[i] = acc;
+      cons_sync();
+      if (ct == 0) {
+        __threadfence();
+        atomicAdd(counters + slot, 1u);
       }
-      __syncthreads();  // tile buffer b, bnew and gsum are free again
-      if (tid == 0 && u + NB < nwaves) issue_tile(u + NB);
+    }
+    const int64_t u = w - FU_LAG;
+    if (u >= 0) {
+      // ---- B(u): the producer fetched wave u's partial block once its counter completed ----
+      const int pb = int(u & 1);
+      fu_wait(bar_u32(PB0 + pb), uint32_t((u >> 1) & 1));
+      const double* pbu = pbuf + int64_t(pb) * G * W;
+      const int nc = int(n_loc - u * W < W ? n_loc - u * W : W);
+      {
+        constexpr int GROUPS = FU_CONS / W;
+        const int col = ct % W, grp = ct / W;
+        const int chunk = (G + GROUPS - 1) / GROUPS;
+        const int k0 = grp * chunk, k1 = min(G, k0 + chunk);
+        double sacc = 0.0;
+        for (int kk = k0; kk < k1; ++kk) sacc += pbu[kk * W + col];
+        gsum[grp * W + col] = sacc;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_u32(PB0 + 2 + pb)) : "memory");
+      cons_sync();
+      if (ct < nc) {
+        constexpr int GROUPS = FU_CONS / W;
+        double g = 0.0;
+        for (int kk = 0; kk < GROUPS; ++kk) g += gsum[kk * W + ct];
+        const TB gt = TB(g);
+        // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
+        const TB x = TB(bold[int(u % (FU_LAG + 1)) * W + ct]) + TB(sigma) * gt;
+        const TB mag = fabs(x) - TB(lam);
+        const TB bn = mag > TB(0) ? copysign(mag, x) : TB(0);
+        bnew[ct] = double(bn);
+        l1 += fabs(double(bn));
+        if (c == 0) {
+          grad[u * W + ct] = gt;
+          beta[u * W + ct] = bn;
+        }
+      }
+      cons_sync();
+      for (int q = 0; q < QPW; ++q, ++kb) {
+        const int s = int(kb % FU_BSTAGES);
+        fu_wait(bar_u32(2 * FU_STAGES + s), uint32_t((kb / FU_BSTAGES) & 1));
+        const TX* tile = bring + s * stage_elems;
+        const int ncq = min(FU_CW, nc - q * FU_CW);
+        for (int i = ct; i < rows; i += FU_CONS) {
+          double acc = xbseg[i];
+          for (int jj = 0; jj < ncq; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[q * FU_CW + jj], acc);
+          xbseg[i] = acc;
+        }
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_u32(2 * FU_STAGES + FU_BSTAGES + s)) : "memory");
+      }
+      cons_sync();  // bnew / gsum / pbuf reusable
     }
   }
-  for (int i = tid; i < rows; i += FU_THREADS) xb_out[r0 + i] = xbseg[i];
-  if (c == 0) {  // ||beta_new||_1 in a fixed order: threads by column residue, warps in order
-    const double s = warp_sum(l1);
-    if (lane == 0) l1_sh[wid] = s;
-    __syncthreads();
-    if (tid == 0) {
+  for (int i = ct; i < rows; i += FU_CONS) xb_out[r0 + i] = xbseg[i];
+  if (c == 0) {  // ||beta_new||_1 in a fixed order: consumer threads by column residue, warps in order
+    const double sm = warp_sum(l1);
+    if (lane == 0) l1_sh[cw] = sm;
+    cons_sync();
+    if (ct == 0) {
       double t = 0.0;
-      for (int k = 0; k < FU_THREADS / 32; ++k) t += l1_sh[k];
+      for (int kk = 0; kk < FU_CONS / 32; ++kk) t += l1_sh[kk];
       xb_out[m] = t;
     }
   }
@@ -812,18 +885,15 @@ static FuPlan fu_plan(int xdtype, int64_t m, int64_t n_loc) {
   const int64_t align = 16 / es;
   const int64_t seg = ceil_div(ceil_div(m, G), align) * align;
   const int64_t budget = int64_t(maxsm) - 2048;
-  for (int W = 16; W >= 4; W /= 2) {
-    const int64_t need = 3 * int64_t(W) * seg * es + 2 * int64_t(G) * W * 8 + 2 * seg * 8 + 4 * W * 8 +
-                         FU_THREADS * 8 + 64;
-    if (need <= budget) {
-      p.ok = true;
-      p.grid = int(std::min<int64_t>(G, ceil_div(m, seg)));
-      p.W = W;
-      p.seg = seg;
-      p.smem = size_t(need);
-      return p;
-    }
-  }
+  const int W = 32;
+  const int64_t need = int64_t(FU_STAGES + FU_BSTAGES) * FU_CW * seg * es + 2 * int64_t(G) * W * 8 + 2 * seg * 8 +
+                       (FU_LAG + 2) * W * 8 + FU_CONS * 8 + (2 * (FU_STAGES + FU_BSTAGES) + 4) * 8 + 64;
+  if (need > budget) return p;
+  p.ok = true;
+  p.grid = int(std::min<int64_t>(G, ceil_div(m, seg)));
+  p.W = W;
+  p.seg = seg;
+  p.smem = size_t(need);
   return p;
 }
 
@@ -852,11 +922,7 @@ template <typename TX, typename TB>
 static int dispatch_fused(const void* X, int64_t m, int64_t n_loc, const FuPlan& p, const double* v, void* grad,
                           void* beta, double sigma, double lam, double* xb_out, double* partials,
                           unsigned int* counters, const int* flags, cudaStream_t st) {
-  switch (p.W) {
-    case 16: return launch_fused<TX, TB, 16>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
-    case 8: return launch_fused<TX, TB, 8>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
-    default: return launch_fused<TX, TB, 4>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
-  }
+  return launch_fused<TX, TB, 32>(X, m, n_loc, p, v, grad, beta, sigma, lam, xb_out, partials, counters, flags, st);
 }
 
 static int64_t fused_ws(const FuPlan& p) {
