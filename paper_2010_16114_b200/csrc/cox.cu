@@ -778,7 +778,9 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
           const TX* col = ring + s * stage_elems + int64_t(cw) * seg;
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int i = lane;
-          for (; i + 96 < rows; i += 128) {
+          const int full = rows - 96;
+#pragma unroll 2
+          for (; i < full; i += 128) {
             a0 = fma(double(col[i]), vseg[i], a0);
             a1 = fma(double(col[i + 32]), vseg[i + 32], a1);
             a2 = fma(double(col[i + 64]), vseg[i + 64], a2);
@@ -840,10 +842,23 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
         fu_wait(bar_u32(2 * FU_STAGES + s), uint32_t((kb / FU_BSTAGES) & 1));
         const TX* tile = bring + s * stage_elems;
         const int ncq = min(FU_CW, nc - q * FU_CW);
-        for (int i = ct; i < rows; i += FU_CONS) {
-          double acc = xbseg[i];
-          for (int jj = 0; jj < ncq; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[q * FU_CW + jj], acc);
-          xbseg[i] = acc;
+        if (ncq == FU_CW) {  // full stage: the 8 coefficients in registers, compile-time column loop
+          double bq[FU_CW];
+#pragma unroll
+          for (int jj = 0; jj < FU_CW; ++jj) bq[jj] = bnew[q * FU_CW + jj];
+          const int sg = int(seg);
+          for (int i = ct; i < rows; i += FU_CONS) {
+            double acc = xbseg[i];
+#pragma unroll
+            for (int jj = 0; jj < FU_CW; ++jj) acc = fma(double(tile[jj * sg + i]), bq[jj], acc);
+            xbseg[i] = acc;
+          }
+        } else {
+          for (int i = ct; i < rows; i += FU_CONS) {
+            double acc = xbseg[i];
+            for (int jj = 0; jj < ncq; ++jj) acc = fma(double(tile[int64_t(jj) * seg + i]), bnew[q * FU_CW + jj], acc);
+            xbseg[i] = acc;
+          }
         }
         __syncwarp();
         if (lane == 0)
