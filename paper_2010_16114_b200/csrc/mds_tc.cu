@@ -16,7 +16,7 @@
 //
 // CTA (one per SM, persistent over (128-column block, row segment) units), 576 threads:
 //   warp 0      TMA producer
-//   warp 1      MMA issuer (one elected lane): MMA1 runs up to two chunks ahead of MMA2
+//   warp 1      MMA issuer (one elected lane): MMA1 runs ahead of MMA2 (bounded by D1 buffers)
 //   warps 2-17  epilogue: warp w owns TMEM lane quarter w % 4 (lane = column j) and one
 //               16-row slice of the chunk: tcgen05.ld d2, elementwise chain, tcgen05.st
 //               the hi/lo split of w as MMA2's A operand (TMEM, K-major)
@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 using namespace bs;
 using namespace tc;
@@ -124,6 +125,15 @@ __device__ __noinline__ float careful_block(float* buf, int64_t ib, int64_t i_en
   return st;
 }
 
+constexpr int TR_CHUNKS = 4096;  // trace: first chunks of CTA 0
+__device__ __forceinline__ void tr_mark(unsigned long long* tr, int ev, uint32_t chunk) {
+  if (tr && blockIdx.x == 0 && chunk < TR_CHUNKS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[ev * TR_CHUNKS + chunk] = t;
+  }
+}
+
 struct MdsTcArgs {
   const float* theta;   // q x n (theta_full, column-major)
   const float* vj_hi;   // n x 32: [-2 theta_j, |theta_j|^2, 1, 0...] tf32 hi
@@ -133,6 +143,7 @@ struct MdsTcArgs {
   int64_t n, lo, n_loc;
   int q, perturb, G;
   int mode;             // debug (BS_MDS_TC_MODE): 1 skips the pair math, 2 the MMAs
+  unsigned long long* trace;  // debug (BS_MDS_TC_TRACE): CTA 0 event times, [event][chunk]
   int jblocks, segs;
   int64_t rows_per_seg;
   double* zsum_part;    // [segs][n_loc]
@@ -263,8 +274,10 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     // Event loop: MMA1 of the next chunk is issued as soon as its B1 stage has landed and
-    // its D1 buffer is free (up to two chunks ahead of MMA2), MMA2 of the oldest chunk as
-    // soon as the epilogue has written its A2; the tensor pipe executes in issue order.
+    // its D1 buffer is free (the epilogue has loaded D1 of chunk t1 - 2, early in its
+    // work on that chunk), so it overtakes MMA2 of the chunk the epilogue is finishing;
+    // MMA2 of the oldest chunk goes as soon as its A2 is written.  The tensor pipe
+    // executes in issue order.
     constexpr uint32_t id1 = idesc_tf32(128, CHI, false, false);
     constexpr uint32_t id2w = idesc_tf32(128, 2 * KP, false, true);
     constexpr uint32_t id2n = idesc_tf32(128, KP, false, true);
@@ -278,7 +291,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       int t1 = 0, t2 = 0;
       while (t2 < nch) {
         bool issued = false;
-        if (t1 < nch && t1 < t2 + 2) {
+        if (t1 < nch) {  // bounded by d1_empty: at most two chunks ahead of the epilogue's D1 reads
           const uint32_t c = cbase + uint32_t(t1);
           const int s = int(c % NB1);
           const uint32_t b = c & 1;
@@ -292,6 +305,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
             for (int k = 0; k < KS; ++k)
               if (!(a.mode & 2)) mma3_kstep(d, ah + 8 * k, ah + 32 + 8 * k, dh + 2 * k, dl + 2 * k, id1, k > 0);
             mma_commit_elect(d1_full(b));
+            if (lane == 0) tr_mark(a.trace, 0, c);  // MMA1 issued
             mma_commit_elect(b1_empty(s));
             if (t1 == nch - 1) mma_commit_elect(a1_empty);
             __syncwarp();
@@ -317,6 +331,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
               mma_kblock_concat(d, ah + 32, ah + 96, bd + 256, id2w, id2n, 1u);
             }
             mma_commit_elect(a2_empty(b));
+            if (lane == 0) tr_mark(a.trace, 1, c);  // MMA2 issued
             mma_commit_elect(b2_empty(s));
             if (last) {
               mma_commit_elect(d2_full);
@@ -395,6 +410,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         uint4 yv[4];
         {
           mbar_wait(y_full(s), (cc / NY) & 1);
+          if (warp == 2 && lane == 0) tr_mark(a.trace, 2, cc);  // Y landed
           const uint32_t ybase = smem_u32(y_at(cc) + (sub >> 1) * Y_BOX) + uint32_t(jrow) * 128u;
           const uint32_t c0 = uint32_t(sub & 1) * 4u;
 #pragma unroll
@@ -408,6 +424,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           y[4 * c + 2] = __uint_as_float(yv[c].z); y[4 * c + 3] = __uint_as_float(yv[c].w);
         }
         mbar_wait(d1_full(b), (cc >> 1) & 1);
+        if (warp == 2 && lane == 0) tr_mark(a.trace, 3, cc);  // D1 ready
         tc_fence_after();
         uint32_t g[16];
         tmem_ld16_u(tmem + lane_addr + T_D1 + b * CHI + 16 * sub, g);
@@ -465,6 +482,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         }
         tc_fence_before();
         mbar_arrive(a2_full(b));
+        if (warp == 2 && lane == 0) tr_mark(a.trace, 4, cc);  // A2 written (warp 2)
         if (fold_pending) fold();
         if ((t % a.G) == a.G - 1 || t == nch - 1) fold_pending = true;
       }
@@ -637,13 +655,29 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
   }
   mds_tc_prep_kernel<<<int(std::min<int64_t>(ceil_div(n, 256), 2048)), 256, 0, st>>>(theta, n, q, uh, ul, vh, vl,
                                                                                     norms, nmax);
-  MdsTcArgs args{theta, vh, vl, norms, nmax, n, lo, n_loc, q, perturb, group, mode, g.jblocks, g.segs, g.rows_per_seg,
+  static unsigned long long* trace = nullptr;
+  static const bool tracing = getenv("BS_MDS_TC_TRACE") != nullptr;
+  if (tracing && !trace) cudaMalloc(&trace, sizeof(unsigned long long) * 5 * TR_CHUNKS);
+  MdsTcArgs args{theta, vh, vl, norms, nmax, n, lo, n_loc, q, perturb, group, mode, trace, g.jblocks, g.segs, g.rows_per_seg,
                  zp, tp, parts, ctr, red};
   switch ((q + 2 + 7) / 8) {
     case 1: mds_tc_kernel<1><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
     case 2: mds_tc_kernel<2><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
     case 3: mds_tc_kernel<3><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
     default: mds_tc_kernel<4><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
+  }
+  if (tracing && trace) {  // debug: CTA 0 event intervals (ns), averaged over chunks 100..1100
+    std::vector<unsigned long long> h(5 * TR_CHUNKS);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+    const char* names[5] = {"MMA1 issued", "MMA2 issued", "Y landed", "D1 ready", "A2 written"};
+    double per[5] = {0};
+    for (int e = 0; e < 5; ++e) per[e] = double(h[e * TR_CHUNKS + 1100] - h[e * TR_CHUNKS + 100]) / 1000.0;
+    fprintf(stderr, "[mds_tc trace] ns per chunk:");
+    for (int e = 0; e < 5; ++e) fprintf(stderr, " %s %.0f;", names[e], per[e]);
+    fprintf(stderr, "\n[mds_tc trace] chunk 500 offsets vs D1 ready (ns):");
+    for (int e = 0; e < 5; ++e) fprintf(stderr, " %s %+lld;", names[e], (long long)(h[e * TR_CHUNKS + 500] - h[3 * TR_CHUNKS + 500]));
+    fprintf(stderr, "\n");
   }
   *zp_out = zp;
   *tp_out = tp;
