@@ -437,6 +437,24 @@ grad_kernel(const TX* __restrict__ X, const double* __restrict__ v, int64_t m, i
     const TX* col = X + j * m + r0;
     double acc0 = 0.0, acc1 = 0.0;
     int e = lane;
+    // four 16-byte loads in flight per lane (a warp streams one column)
+    for (; e + 96 < nvec; e += 128) {
+      double x0[VEC], x1[VEC], x2[VEC], x3[VEC];
+      VecLoad<TX, VEC>::load(col + e * VEC, x0);
+      VecLoad<TX, VEC>::load(col + (e + 32) * VEC, x1);
+      VecLoad<TX, VEC>::load(col + (e + 64) * VEC, x2);
+      VecLoad<TX, VEC>::load(col + (e + 96) * VEC, x3);
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        acc0 = fma(x0[u], vs[e * VEC + u], acc0);
+        acc1 = fma(x1[u], vs[(e + 32) * VEC + u], acc1);
+      }
+#pragma unroll
+      for (int u = 0; u < VEC; ++u) {
+        acc0 = fma(x2[u], vs[(e + 64) * VEC + u], acc0);
+        acc1 = fma(x3[u], vs[(e + 96) * VEC + u], acc1);
+      }
+    }
     for (; e + 32 < nvec; e += 64) {
       double x0[VEC], x1[VEC];
       VecLoad<TX, VEC>::load(col + e * VEC, x0);
