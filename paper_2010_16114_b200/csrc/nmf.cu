@@ -442,13 +442,24 @@ cc_gemm_kernel(const T* __restrict__ X, const T* __restrict__ B, int64_t M, int6
 // ---------------------------------------------------------------------------
 
 template <int RP, bool A_MN>
+struct DmmaCfg {
+  static constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, PB = 8;
+  // A tile: [k][m] (m contiguous) for scn b; [m][k] (k contiguous, +4 pad) for scn a
+  static constexpr int A_ELEMS = A_MN ? BK * (BM + 8) : BM * (BK + 4);
+  static constexpr int B_ELEMS = BK * (RP + PB);
+  static constexpr int SMEM = 2 * (A_ELEMS + B_ELEMS) * 8;
+};
+
+template <int RP, bool A_MN>
 __global__ void __launch_bounds__(128)
 dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int64_t M, int64_t ldx, int r,
                  int64_t K, int64_t k_per_split, double* __restrict__ out) {
-  constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, V = 2, NF = RP / 8;
-  constexpr int PA = 8, PB = 8;  // pads (doubles): row strides = 64 B mod 128
-  __shared__ __align__(16) double As[2][BK][BM + PA];
-  __shared__ __align__(16) double Bs[2][BK][RP + PB];
+  using C = DmmaCfg<RP, A_MN>;
+  constexpr int BM = C::BM, BK = C::BK, V = 2, NF = RP / 8, PB = C::PB;
+  constexpr int SA = A_MN ? BM + 8 : BK + 4;  // row stride of the A tile (doubles)
+  extern __shared__ __align__(16) double dm_smem[];
+  double* As = dm_smem;                  // [2][A_ELEMS]
+  double* Bs = dm_smem + 2 * C::A_ELEMS;  // [2][BK][RP + PB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t m0 = int64_t(blockIdx.x) * BM;
   const int64_t k_begin = int64_t(blockIdx.y) * k_per_split;
@@ -457,11 +468,13 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
   constexpr int B_PER = (BK * RP + 127) / 128;
   double ra[A_PER], rb[B_PER];
   const bool vec_ok = (ldx % V) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  // A_MN: vector e covers m [mv, mv+2) of k row kk.  !A_MN: BK/2 threads per m row, vector e
+  // covers k [2c, 2c+2) of row (e / (BK/2)) -- consecutive threads read consecutive 16 bytes.
   auto load_tile = [&](int64_t k0) {
-    if constexpr (A_MN) {
 #pragma unroll
-      for (int u = 0; u < A_PER / V; ++u) {
-        const int e = tid + 128 * u;
+    for (int u = 0; u < A_PER / V; ++u) {
+      const int e = tid + 128 * u;
+      if constexpr (A_MN) {
         const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
         const int64_t k = k0 + kk, mrow = m0 + mv;
         if (vec_ok && k < k_end && mrow + V <= M) {
@@ -471,21 +484,15 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
 #pragma unroll
           for (int v = 0; v < V; ++v) ra[u * V + v] = (k < k_end && mrow + v < M) ? X[k * ldx + mrow + v] : 0.0;
         }
-      }
-    } else {
-      const int64_t mrow = m0 + tid;
-      const double* src = X + mrow * ldx + k0;
-      if (mrow < M && k0 + A_PER <= k_end && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-#pragma unroll
-        for (int u = 0; u < A_PER; u += V) {
-          const double2 w = *reinterpret_cast<const double2*>(src + u);
-          ra[u] = w.x; ra[u + 1] = w.y;
-        }
       } else {
+        const int row = e / (BK / V), c = e % (BK / V);
+        const int64_t mrow = m0 + row, k = k0 + V * c;
+        if (vec_ok && mrow < M && k + V <= k_end) {
+          const double2 w = *reinterpret_cast<const double2*>(X + mrow * ldx + k);
+          ra[u * V] = w.x; ra[u * V + 1] = w.y;
+        } else {
 #pragma unroll
-        for (int kk = 0; kk < A_PER; ++kk) {
-          const int64_t k = k0 + kk;
-          ra[kk] = (mrow < M && k < k_end) ? X[mrow * ldx + k] : 0.0;
+          for (int v = 0; v < V; ++v) ra[u * V + v] = (mrow < M && k + v < k_end) ? X[mrow * ldx + k + v] : 0.0;
         }
       }
     }
@@ -498,21 +505,23 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
     }
   };
   auto store_tile = [&](int buf) {
-    if constexpr (A_MN) {
+    double* at = As + buf * C::A_ELEMS;
 #pragma unroll
-      for (int u = 0; u < A_PER / V; ++u) {
-        const int e = tid + 128 * u;
+    for (int u = 0; u < A_PER / V; ++u) {
+      const int e = tid + 128 * u;
+      if constexpr (A_MN) {
         const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
-        *reinterpret_cast<double2*>(&As[buf][kk][mv]) = make_double2(ra[u * V], ra[u * V + 1]);
+        *reinterpret_cast<double2*>(at + kk * SA + mv) = make_double2(ra[u * V], ra[u * V + 1]);
+      } else {
+        const int row = e / (BK / V), c = e % (BK / V);
+        *reinterpret_cast<double2*>(at + row * SA + V * c) = make_double2(ra[u * V], ra[u * V + 1]);
       }
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < A_PER; ++kk) As[buf][kk][tid] = ra[kk];
     }
+    double* bt = Bs + buf * C::B_ELEMS;
 #pragma unroll
     for (int u = 0; u < B_PER; ++u) {
       const int e = tid + 128 * u;
-      if (e < BK * RP) Bs[buf][e / RP][e % RP] = rb[u];
+      if (e < BK * RP) bt[(e / RP) * (RP + PB) + e % RP] = rb[u];
     }
   };
   double acc[4][NF][2];
@@ -529,13 +538,18 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
     for (int64_t k0 = k_begin; k0 < k_end; k0 += BK) {
       const bool more = k0 + BK < k_end;
       if (more) load_tile(k0 + BK);  // in flight while this tile is consumed
+      const double* at = As + buf * C::A_ELEMS;
+      const double* bt = Bs + buf * C::B_ELEMS;
 #pragma unroll
       for (int ks = 0; ks < BK; ks += 4) {
         double a[4], b[NF];
 #pragma unroll
-        for (int f = 0; f < 4; ++f) a[f] = As[buf][ks + fk][32 * warp + 8 * f + fr];
+        for (int f = 0; f < 4; ++f) {
+          const int row = 32 * warp + 8 * f + fr;
+          a[f] = A_MN ? at[(ks + fk) * SA + row] : at[row * SA + ks + fk];
+        }
 #pragma unroll
-        for (int g = 0; g < NF; ++g) b[g] = Bs[buf][ks + fk][8 * g + fr];
+        for (int g = 0; g < NF; ++g) b[g] = bt[(ks + fk) * (RP + PB) + 8 * g + fr];
 #pragma unroll
         for (int f = 0; f < 4; ++f)
 #pragma unroll
@@ -570,10 +584,25 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
                         dim3 grid, double* out, cudaStream_t st) {
   static const bool disabled = getenv("BS_DISABLE_DMMA") != nullptr;  // A/B switch for benchmarks
   if (disabled) return false;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaFuncSetAttribute(dmma_gemm_kernel<16, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DmmaCfg<16, A_MN>::SMEM);
+    cudaFuncSetAttribute(dmma_gemm_kernel<32, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DmmaCfg<32, A_MN>::SMEM);
+    cudaFuncSetAttribute(dmma_gemm_kernel<64, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         DmmaCfg<64, A_MN>::SMEM);
+  });
   switch (pick_rp(r)) {
-    case 16: dmma_gemm_kernel<16, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
-    case 32: dmma_gemm_kernel<32, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
-    case 64: dmma_gemm_kernel<64, A_MN><<<grid, 128, 0, st>>>(X, B, M, ldx, r, K, kps, out); return true;
+    case 16:
+      dmma_gemm_kernel<16, A_MN><<<grid, 128, DmmaCfg<16, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
+      return true;
+    case 32:
+      dmma_gemm_kernel<32, A_MN><<<grid, 128, DmmaCfg<32, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
+      return true;
+    case 64:
+      dmma_gemm_kernel<64, A_MN><<<grid, 128, DmmaCfg<64, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
+      return true;
     default: return false;
   }
 }
