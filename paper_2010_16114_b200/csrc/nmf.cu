@@ -584,27 +584,28 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
                         dim3 grid, double* out, cudaStream_t st) {
   static const bool disabled = getenv("BS_DISABLE_DMMA") != nullptr;  // A/B switch for benchmarks
   if (disabled) return false;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(dmma_gemm_kernel<16, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         DmmaCfg<16, A_MN>::SMEM);
-    cudaFuncSetAttribute(dmma_gemm_kernel<32, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         DmmaCfg<32, A_MN>::SMEM);
-    cudaFuncSetAttribute(dmma_gemm_kernel<64, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         DmmaCfg<64, A_MN>::SMEM);
-  });
-  switch (pick_rp(r)) {
-    case 16:
-      dmma_gemm_kernel<16, A_MN><<<grid, 128, DmmaCfg<16, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
-      return true;
-    case 32:
-      dmma_gemm_kernel<32, A_MN><<<grid, 128, DmmaCfg<32, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
-      return true;
-    case 64:
-      dmma_gemm_kernel<64, A_MN><<<grid, 128, DmmaCfg<64, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
-      return true;
+  // N padded to the next multiple of 8 the DMMA fragments need (r = 20 -> 24, not 32)
+  const int rp = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32 : r <= 48 ? 48 : r <= 64 ? 64 : 0;
+#define BS_DMMA(RPV)                                                                                         \
+  {                                                                                                          \
+    static std::once_flag once;                                                                              \
+    std::call_once(once, [] {                                                                                \
+      cudaFuncSetAttribute(dmma_gemm_kernel<RPV, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                           DmmaCfg<RPV, A_MN>::SMEM);                                                        \
+    });                                                                                                      \
+    dmma_gemm_kernel<RPV, A_MN><<<grid, 128, DmmaCfg<RPV, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out); \
+    return true;                                                                                             \
+  }
+  switch (rp) {
+    case 8: BS_DMMA(8)
+    case 16: BS_DMMA(16)
+    case 24: BS_DMMA(24)
+    case 32: BS_DMMA(32)
+    case 48: BS_DMMA(48)
+    case 64: BS_DMMA(64)
     default: return false;
   }
+#undef BS_DMMA
 }
 
 // scn b through the register-tiled kernel (RP <= 64) or the legacy one (RP = 128).
