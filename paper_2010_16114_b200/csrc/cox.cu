@@ -23,28 +23,36 @@ using namespace bs;
 
 template <typename TX, int VEC> struct VecLoad;
 template <> struct VecLoad<float, 4> {
+  static __device__ __forceinline__ void widen(uint4 v, double* o) {
+    o[0] = __uint_as_float(v.x); o[1] = __uint_as_float(v.y); o[2] = __uint_as_float(v.z); o[3] = __uint_as_float(v.w);
+  }
   static __device__ __forceinline__ void load(const float* p, double* o) {
-    const float4 v = ld_stream(reinterpret_cast<const float4*>(p));
-    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    widen(ld_stream(reinterpret_cast<const uint4*>(p)), o);
   }
 };
 template <> struct VecLoad<double, 2> {
+  static __device__ __forceinline__ void widen(uint4 v, double* o) {
+    o[0] = __hiloint2double(int(v.y), int(v.x));
+    o[1] = __hiloint2double(int(v.w), int(v.z));
+  }
   static __device__ __forceinline__ void load(const double* p, double* o) {
-    const double2 v = ld_stream(reinterpret_cast<const double2*>(p));
-    o[0] = v.x; o[1] = v.y;
+    widen(ld_stream(reinterpret_cast<const uint4*>(p)), o);
   }
 };
 template <> struct VecLoad<int8_t, 16> {
-  static __device__ __forceinline__ void load(const int8_t* p, double* o) {
-    const int4 v = ld_stream(reinterpret_cast<const int4*>(p));
-    const int w[4] = {v.x, v.y, v.z, v.w};
+  static __device__ __forceinline__ void widen(uint4 v, double* o) {
+    const unsigned int w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) o[4 * a + b] = double(int8_t((w[a] >> (8 * b)) & 0xff));
   }
+  static __device__ __forceinline__ void load(const int8_t* p, double* o) {
+    widen(ld_stream(reinterpret_cast<const uint4*>(p)), o);
+  }
 };
 template <typename TX> struct VecLoad<TX, 1> {
+  static __device__ __forceinline__ void widen(uint4, double*) {}
   static __device__ __forceinline__ void load(const TX* p, double* o) { o[0] = double(*p); }
 };
 
@@ -437,22 +445,22 @@ grad_kernel(const TX* __restrict__ X, const double* __restrict__ v, int64_t m, i
     const TX* col = X + j * m + r0;
     double acc0 = 0.0, acc1 = 0.0;
     int e = lane;
-    // four 16-byte loads in flight per lane (a warp streams one column)
-    for (; e + 96 < nvec; e += 128) {
-      double x0[VEC], x1[VEC], x2[VEC], x3[VEC];
-      VecLoad<TX, VEC>::load(col + e * VEC, x0);
-      VecLoad<TX, VEC>::load(col + (e + 32) * VEC, x1);
-      VecLoad<TX, VEC>::load(col + (e + 64) * VEC, x2);
-      VecLoad<TX, VEC>::load(col + (e + 96) * VEC, x3);
+    // eight 16-byte loads in flight per lane (a warp streams one column); raw words are
+    // held until all eight have been issued, then widened and accumulated in order
+    if constexpr (VEC > 1)
+    for (; e + 224 < nvec; e += 256) {
+      uint4 w[8];
 #pragma unroll
-      for (int u = 0; u < VEC; ++u) {
-        acc0 = fma(x0[u], vs[e * VEC + u], acc0);
-        acc1 = fma(x1[u], vs[(e + 32) * VEC + u], acc1);
-      }
+      for (int t = 0; t < 8; ++t) w[t] = ld_stream(reinterpret_cast<const uint4*>(col + (e + 32 * t) * VEC));
 #pragma unroll
-      for (int u = 0; u < VEC; ++u) {
-        acc0 = fma(x2[u], vs[(e + 64) * VEC + u], acc0);
-        acc1 = fma(x3[u], vs[(e + 96) * VEC + u], acc1);
+      for (int t = 0; t < 8; ++t) {
+        double xv[VEC];
+        VecLoad<TX, VEC>::widen(w[t], xv);
+#pragma unroll
+        for (int u = 0; u < VEC; ++u) {
+          if (t & 1) acc1 = fma(xv[u], vs[(e + 32 * t) * VEC + u], acc1);
+          else acc0 = fma(xv[u], vs[(e + 32 * t) * VEC + u], acc0);
+        }
       }
     }
     for (; e + 32 < nvec; e += 64) {
