@@ -43,6 +43,13 @@ inline int check_launch(const char* what, int n = 1) {
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Raises a kernel's dynamic shared-memory limit to `bytes` on the CURRENT device
+// (function attributes are per device: a process driving several GPUs -- the
+// in-process backend -- needs it once per device).  Cached per (kernel, device).
+void smem_attr(const void* kernel, int bytes);
+template <typename K>
+inline void smem_attr(K* kernel, int bytes) { smem_attr(reinterpret_cast<const void*>(kernel), bytes); }
+
 // Most split-K slabs the tcgen05 GEMMs write (nmf_tc.cu).
 constexpr int TC_MAX_SPLITS = 16;
 

@@ -4,6 +4,9 @@
 // (scn d local part).
 #include "bsb200.cuh"
 
+#include <map>
+#include <mutex>
+
 #include <cfloat>
 #include <cmath>
 #include <atomic>
@@ -37,6 +40,18 @@ int num_sms() {
     if (sms <= 0) sms = 148;
   });
   return sms;
+}
+
+void smem_attr(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  have = bytes;
 }
 
 }  // namespace bs
@@ -399,13 +414,8 @@ int launch_gram(const void* A, int dtype, int r, int64_t ncols, double* G, Works
   }
   const int64_t cpb = ceil_div(ncols, grid);
   const size_t smem = sizeof(double) * GRAM_COLS * r;
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(gram_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(double) * GRAM_COLS * GRAM_MAXR));
-    cudaFuncSetAttribute(gram_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(sizeof(double) * GRAM_COLS * GRAM_MAXR));
-  });
+  smem_attr(gram_kernel<double>, int(sizeof(double) * GRAM_COLS * GRAM_MAXR));
+  smem_attr(gram_kernel<float>, int(sizeof(double) * GRAM_COLS * GRAM_MAXR));
   if (dtype == BS_F64)
     gram_kernel<double><<<grid, 256, smem, st>>>(static_cast<const double*>(A), r, ncols, cpb, parts,
                                                   counter, G);

@@ -58,6 +58,13 @@ template <typename TX> struct VecLoad<TX, 1> {
 
 template <typename TX> constexpr int vec_of() { return 16 / int(sizeof(TX)); }
 
+// int8 byte k of w as an exact float: PRMT places (byte ^ 0x80) under the exponent of 2^23,
+// the subtraction removes 2^23 + 128 (two full-rate instructions; no conversion unit).
+__device__ __forceinline__ float i8_to_f32(unsigned int w_flipped, int k) {
+  const unsigned int bits = __byte_perm(w_flipped, 0x4B000000u, unsigned(k) | (4u << 4) | (4u << 8) | (7u << 12));
+  return __uint_as_float(bits) - 8388736.0f;
+}
+
 // ---------------------------------------------------------------------------
 // scn m: partial xb over a column chunk, VEC rows per thread.
 // grid = (row tiles, column splits); out slab s = parts + s*m.
@@ -152,11 +159,71 @@ extern "C" int64_t bs_cox_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) 
   return ws_bytes<double>(int64_t(std::max(g.splits, h.splits)) * m);
 }
 
+// scn m for int8 X with float32 arithmetic (the dtype of beta): 16 rows per thread (one
+// 16-byte word per column), float partial sums over 32-column blocks added into float64.
+__global__ void __launch_bounds__(XB_THREADS)
+xbeta_i8f_kernel(const int8_t* __restrict__ X, const float* __restrict__ beta, int64_t m, int64_t n_loc,
+                 int64_t cols_per_split, double* __restrict__ parts) {
+  const int64_t i0 = (int64_t(blockIdx.x) * XB_THREADS + threadIdx.x) * 16;
+  const int64_t j_begin = int64_t(blockIdx.y) * cols_per_split;
+  const int64_t j_end = min(n_loc, j_begin + cols_per_split);
+  if (i0 >= m) return;
+  double accd[16];
+#pragma unroll
+  for (int v = 0; v < 16; ++v) accd[v] = 0.0;
+  for (int64_t jb = j_begin; jb < j_end; jb += 32) {
+    const int64_t je = min(j_end, jb + 32);
+    float acc[16];
+#pragma unroll
+    for (int v = 0; v < 16; ++v) acc[v] = 0.f;
+    int64_t j = jb;
+    for (; j + 4 <= je; j += 4) {
+      uint4 w[4];
+      float b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w[u] = ld_stream(reinterpret_cast<const uint4*>(X + (j + u) * m + i0));
+        b[u] = __ldg(beta + j + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned int ww[4] = {w[u].x ^ 0x80808080u, w[u].y ^ 0x80808080u, w[u].z ^ 0x80808080u,
+                                    w[u].w ^ 0x80808080u};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[4 * a + k] = fmaf(i8_to_f32(ww[a], k), b[u], acc[4 * a + k]);
+      }
+    }
+    for (; j < je; ++j) {
+      const uint4 w = ld_stream(reinterpret_cast<const uint4*>(X + j * m + i0));
+      const float b = __ldg(beta + j);
+      const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[4 * a + k] = fmaf(i8_to_f32(ww[a], k), b, acc[4 * a + k]);
+    }
+#pragma unroll
+    for (int v = 0; v < 16; ++v) accd[v] += double(acc[v]);
+  }
+  double* out = parts + int64_t(blockIdx.y) * m;
+#pragma unroll
+  for (int v = 0; v < 16; ++v) out[i0 + v] = accd[v];
+}
+
 template <typename TX, typename TB>
 static void launch_xbeta(const TX* X, const TB* beta, int64_t m, int64_t n_loc, const XbGrid& g, double* out,
                          cudaStream_t st) {
   dim3 grid(unsigned(g.tiles), unsigned(g.splits));
   constexpr int V = vec_of<TX>();
+  if constexpr (sizeof(TX) == 1 && sizeof(TB) == 4) {
+    if (g.vec == V) {  // int8 genotypes, float32 arithmetic: no per-element conversion unit work
+      xbeta_i8f_kernel<<<grid, XB_THREADS, 0, st>>>(reinterpret_cast<const int8_t*>(X),
+                                                    reinterpret_cast<const float*>(beta), m, n_loc, g.cps, out);
+      return;
+    }
+  }
   if (g.vec == V)
     xbeta_kernel<TX, TB, V><<<grid, XB_THREADS, 0, st>>>(X, beta, m, n_loc, g.cps, out);
   else
@@ -545,17 +612,66 @@ extern "C" int64_t bs_cox_grad_workspace(int xdtype, int64_t m, int64_t n_loc) {
          ws_bytes<double>(prox_grid(n_loc));
 }
 
+// scn p for int8 X with float32 arithmetic: v staged as float, eight 16-byte words in flight
+// per lane, float partial sums per 16-element word added into float64 accumulators.
+__global__ void __launch_bounds__(GR_THREADS)
+grad_i8f_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, int64_t m, int64_t n_loc,
+                int64_t cols_per_group, double* __restrict__ parts, const int* flags) {
+  extern __shared__ __align__(16) double vsd[];
+  float* vs = reinterpret_cast<float*>(vsd);
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r0 = int64_t(blockIdx.y) * GR_SEG;
+  const int len = int(m - r0 < GR_SEG ? m - r0 : GR_SEG);
+  for (int e = threadIdx.x; e < len; e += blockDim.x) vs[e] = float(v[r0 + e]);
+  __syncthreads();
+  const int64_t c0 = int64_t(blockIdx.x) * cols_per_group;
+  const int64_t c1 = min(n_loc, c0 + cols_per_group);
+  const int nvec = len / 16;
+  for (int64_t j = c0 + wid; j < c1; j += GR_THREADS / 32) {
+    const int8_t* col = X + j * m + r0;
+    double acc0 = 0.0, acc1 = 0.0;
+    int e = lane;
+    auto word = [&](uint4 w, int ee) -> float {  // 16 rows of one word, float
+      const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+      const float4* vv = reinterpret_cast<const float4*>(vs + ee * 16);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const float4 q = vv[a];
+        s0 = fmaf(i8_to_f32(ww[a], 0), q.x, s0);
+        s1 = fmaf(i8_to_f32(ww[a], 1), q.y, s1);
+        s0 = fmaf(i8_to_f32(ww[a], 2), q.z, s0);
+        s1 = fmaf(i8_to_f32(ww[a], 3), q.w, s1);
+      }
+      return s0 + s1;
+    };
+    for (; e + 224 < nvec; e += 256) {
+      uint4 w[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) w[t] = ld_stream(reinterpret_cast<const uint4*>(col + (e + 32 * t) * 16));
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const float sv = word(w[t], e + 32 * t);
+        if (t & 1) acc1 += double(sv);
+        else acc0 += double(sv);
+      }
+    }
+    for (; e < nvec; e += 32) acc0 += double(word(ld_stream(reinterpret_cast<const uint4*>(col + e * 16)), e));
+    for (int t = nvec * 16 + lane; t < len; t += 32) acc1 = fma(double(col[t]), double(vs[t]), acc1);
+    const double sacc = warp_sum(acc0 + acc1);
+    if (lane == 0) parts[int64_t(blockIdx.y) * n_loc + j] = sacc;
+  }
+}
+
 template <typename TX>
 static void launch_grad(const TX* X, const double* v, int64_t m, int64_t n_loc, const GrGrid& g, bool vec_ok,
                         double* parts, const int* flags, cudaStream_t st) {
   dim3 grid(unsigned(g.groups), unsigned(g.segs));
   constexpr int V = vec_of<TX>();
   const int smem = int(sizeof(double) * GR_SEG);
-  static std::once_flag once;
-  std::call_once(once, [smem] {
-    cudaFuncSetAttribute(grad_kernel<TX, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(grad_kernel<TX, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
+  if (vec_ok) smem_attr(grad_kernel<TX, V>, smem);
+  else smem_attr(grad_kernel<TX, 1>, smem);
   if (vec_ok)
     grad_kernel<TX, V><<<grid, GR_THREADS, smem, st>>>(X, v, m, n_loc, g.cpg, parts, flags);
   else
@@ -581,7 +697,11 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
     const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
     if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
-    else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
+    else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic
+      dim3 grid(unsigned(g.groups), unsigned(g.segs));
+      grad_i8f_kernel<<<grid, GR_THREADS, int(sizeof(float) * GR_SEG), st>>>(static_cast<const int8_t*>(X), dmpd, m,
+                                                                             n_loc, g.cpg, parts, flags);
+    } else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else { set_error("bs_cox_grad_step: unsupported X dtype %d", xdtype); return BS_EINVAL; }
   }
   const int segs = m == 0 ? 1 : g.segs;
@@ -943,7 +1063,7 @@ static int launch_fused(const void* X, int64_t m, int64_t n_loc, const FuPlan& p
                         void* beta, double sigma, double lam, double* xb_out, double* partials, unsigned int* counters,
                         const int* flags, cudaStream_t st) {
   auto kern = cox_fused_kernel<TX, TB, W>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem));
+  smem_attr(kern, int(p.smem));
   const TX* Xp = static_cast<const TX*>(X);
   int64_t seg = p.seg;
   TB* g = static_cast<TB*>(grad);

@@ -567,18 +567,12 @@ static void launch_pass(const T* Y, const T* th, int64_t n, int64_t lo, int64_t 
   if constexpr (sizeof(T) == 4 && QM <= 32) {
     mds_norms_kernel<<<int(std::min<int64_t>(ceil_div(n, 256), 1184)), 256, 0, st>>>(
         reinterpret_cast<const float*>(th), n, q, norms);
-    static std::once_flag once2;
-    std::call_once(once2, [smem] {
-      cudaFuncSetAttribute(mds_pass_f32x2_kernel<QM, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
+    smem_attr(mds_pass_f32x2_kernel<QM, JB>, smem);
     mds_pass_f32x2_kernel<QM, JB><<<grid, MDS_THREADS, smem, st>>>(
         reinterpret_cast<const float*>(Y), reinterpret_cast<const float*>(th), n, lo, n_loc, q, perturb, mode,
         g.rows_per_seg, zp, tp, parts, ctr, red, norms);
   } else {
-    static std::once_flag once;
-    std::call_once(once, [smem] {
-      cudaFuncSetAttribute(mds_pass_kernel<T, QM, JB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    });
+    smem_attr(mds_pass_kernel<T, QM, JB>, smem);
     mds_pass_kernel<T, QM, JB><<<grid, MDS_THREADS, smem, st>>>(Y, th, n, lo, n_loc, q, perturb, mode,
                                                              g.rows_per_seg, zp, tp, parts, ctr, red);
   }

@@ -644,11 +644,11 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
     group = (e && atoi(e) > 0) ? atoi(e) : 2;
     const char* m = getenv("BS_MDS_TC_MODE");
     mode = m ? atoi(m) : 0;
-    cudaFuncSetAttribute(mds_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(mds_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(mds_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaFuncSetAttribute(mds_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
   });
+  smem_attr(mds_tc_kernel<1>, SMEM);
+  smem_attr(mds_tc_kernel<2>, SMEM);
+  smem_attr(mds_tc_kernel<3>, SMEM);
+  smem_attr(mds_tc_kernel<4>, SMEM);
   if (cudaMemsetAsync(nmax, 0, sizeof(float), st) != cudaSuccess) {
     set_error("bs_mds_pass: cudaMemsetAsync failed");
     return BS_ECUDA;

@@ -588,11 +588,7 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
   const int rp = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32 : r <= 48 ? 48 : r <= 64 ? 64 : 0;
 #define BS_DMMA(RPV)                                                                                         \
   {                                                                                                          \
-    static std::once_flag once;                                                                              \
-    std::call_once(once, [] {                                                                                \
-      cudaFuncSetAttribute(dmma_gemm_kernel<RPV, A_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                           DmmaCfg<RPV, A_MN>::SMEM);                                                        \
-    });                                                                                                      \
+    smem_attr(dmma_gemm_kernel<RPV, A_MN>, DmmaCfg<RPV, A_MN>::SMEM);                                      \
     dmma_gemm_kernel<RPV, A_MN><<<grid, 128, DmmaCfg<RPV, A_MN>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out); \
     return true;                                                                                             \
   }
@@ -924,14 +920,13 @@ static int launch_update(int algo, T* F, const TN* num, int S, int64_t slab, con
     return BS_EWORK;
   }
   const size_t smem = sizeof(double) * (r * r + UPD_COLS * r);
-  static std::once_flag once;
-  std::call_once(once, [] {
+  {
     const int big = int(sizeof(double) * (MAX_R * MAX_R + UPD_COLS * MAX_R));
-    cudaFuncSetAttribute(factor_update_kernel<T, TN, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(factor_update_kernel<T, TN, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(factor_update_kernel<T, TN, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(factor_update_kernel<T, TN, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-  });
+    smem_attr(factor_update_kernel<T, TN, 16>, big);
+    smem_attr(factor_update_kernel<T, TN, 32>, big);
+    smem_attr(factor_update_kernel<T, TN, 64>, big);
+    smem_attr(factor_update_kernel<T, TN, 128>, big);
+  }
   const int64_t cpb = ceil_div(ncols, grid);
 #define BS_UPD(RPV)                                                                              \
   factor_update_kernel<T, TN, RPV><<<grid, UPD_THREADS, smem, st>>>(algo, F, num, S, slab, gram, r, \

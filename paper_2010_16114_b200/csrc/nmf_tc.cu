@@ -412,10 +412,7 @@ template <bool A_MN, int NP>
 int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r, int splits, float* out, int64_t slab,
               cudaStream_t st, double* stats_part = nullptr, int* grid_out = nullptr) {
   using C = TcCfg<NP>;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaFuncSetAttribute(tc_gemm_kernel<A_MN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
+  smem_attr(tc_gemm_kernel<A_MN, NP>, C::SMEM);
   const int tiles = int(ceil_div(M, BM));
   const int kb_total = int(ceil_div(K, BK));
   const int kb_per = int(ceil_div(kb_total, splits));
