@@ -612,55 +612,93 @@ extern "C" int64_t bs_cox_grad_workspace(int xdtype, int64_t m, int64_t n_loc) {
          ws_bytes<double>(prox_grid(n_loc));
 }
 
-// scn p for int8 X with float32 arithmetic: v staged as float, eight 16-byte words in flight
-// per lane, float partial sums per 16-element word added into float64 accumulators.
+// scn p for int8 X with float32 arithmetic.  Warp w of a CTA owns rows
+// [w*1024, (w+1)*1024) of the CTA's 8192-row segment; lane l the 16-row words at
+// 16l and 512 + 16l, whose v values stay in registers (as float) for every column, so
+// the only memory traffic is the X stream: four columns at a time, eight 16-byte words
+// in flight per lane.  Per genotype: PRMT + packed FADD/FMA (f32x2).  Warp partials are
+// reduced across the eight warps in a fixed order per 32-column batch.
+typedef unsigned long long i8_f2;
+__device__ __forceinline__ i8_f2 i8_pack(float a, float b) {
+  i8_f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float i8_hsum(i8_f2 v) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+  return a + b;
+}
+__device__ __forceinline__ i8_f2 i8_fma2(i8_f2 a, i8_f2 b, i8_f2 c) {
+  i8_f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ i8_f2 i8_add2(i8_f2 a, i8_f2 b) {
+  i8_f2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// sum_k x_k v_k over the 16 int8 of word w (flipped by 0x80) against v[0..16)
+__device__ __forceinline__ float i8_word_dot(uint4 w, const float* v) {
+  const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+  const i8_f2 off = i8_pack(-8388736.0f, -8388736.0f);
+  i8_f2 s0 = i8_pack(0.f, 0.f), s1 = i8_pack(0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const unsigned int p0 = __byte_perm(ww[a], 0x4B000000u, 0x7440u), p1 = __byte_perm(ww[a], 0x4B000000u, 0x7441u);
+    const unsigned int p2 = __byte_perm(ww[a], 0x4B000000u, 0x7442u), p3 = __byte_perm(ww[a], 0x4B000000u, 0x7443u);
+    const i8_f2 x01 = i8_add2(i8_pack(__uint_as_float(p0), __uint_as_float(p1)), off);
+    const i8_f2 x23 = i8_add2(i8_pack(__uint_as_float(p2), __uint_as_float(p3)), off);
+    s0 = i8_fma2(x01, i8_pack(v[4 * a], v[4 * a + 1]), s0);
+    s1 = i8_fma2(x23, i8_pack(v[4 * a + 2], v[4 * a + 3]), s1);
+  }
+  return i8_hsum(s0) + i8_hsum(s1);
+}
+
 __global__ void __launch_bounds__(GR_THREADS)
 grad_i8f_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, int64_t m, int64_t n_loc,
                 int64_t cols_per_group, double* __restrict__ parts, const int* flags) {
-  extern __shared__ __align__(16) double vsd[];
-  float* vs = reinterpret_cast<float*>(vsd);
+  __shared__ double red[GR_THREADS / 32][32];
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t r0 = int64_t(blockIdx.y) * GR_SEG;
-  const int len = int(m - r0 < GR_SEG ? m - r0 : GR_SEG);
-  for (int e = threadIdx.x; e < len; e += blockDim.x) vs[e] = float(v[r0 + e]);
-  __syncthreads();
+  const int64_t ra = r0 + int64_t(wid) * 1024 + 16 * lane, rb = ra + 512;  // this lane's two words
+  const bool ha = ra < m, hb = rb < m;  // m % 16 == 0: a word is either whole or absent
+  float va[16], vb[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    va[k] = ha ? float(v[ra + k]) : 0.f;
+    vb[k] = hb ? float(v[rb + k]) : 0.f;
+  }
   const int64_t c0 = int64_t(blockIdx.x) * cols_per_group;
   const int64_t c1 = min(n_loc, c0 + cols_per_group);
-  const int nvec = len / 16;
-  for (int64_t j = c0 + wid; j < c1; j += GR_THREADS / 32) {
-    const int8_t* col = X + j * m + r0;
-    double acc0 = 0.0, acc1 = 0.0;
-    int e = lane;
-    auto word = [&](uint4 w, int ee) -> float {  // 16 rows of one word, float
-      const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
-      const float4* vv = reinterpret_cast<const float4*>(vs + ee * 16);
-      float s0 = 0.f, s1 = 0.f;
+  const uint4 zero = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // int8 zeros once flipped back
+  for (int64_t cb = c0; cb < c1; cb += 32) {
+    const int nb = int(c1 - cb < 32 ? c1 - cb : 32);
+    for (int jj = 0; jj < nb; jj += 4) {
+      uint4 wa[4], wb[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const float4 q = vv[a];
-        s0 = fmaf(i8_to_f32(ww[a], 0), q.x, s0);
-        s1 = fmaf(i8_to_f32(ww[a], 1), q.y, s1);
-        s0 = fmaf(i8_to_f32(ww[a], 2), q.z, s0);
-        s1 = fmaf(i8_to_f32(ww[a], 3), q.w, s1);
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j = cb + jj + u;
+        const bool live = jj + u < nb;
+        const int8_t* col = X + j * m;
+        wa[u] = (live && ha) ? ld_stream(reinterpret_cast<const uint4*>(col + ra)) : zero;
+        wb[u] = (live && hb) ? ld_stream(reinterpret_cast<const uint4*>(col + rb)) : zero;
       }
-      return s0 + s1;
-    };
-    for (; e + 224 < nvec; e += 256) {
-      uint4 w[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) w[t] = ld_stream(reinterpret_cast<const uint4*>(col + (e + 32 * t) * 16));
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        const float sv = word(w[t], e + 32 * t);
-        if (t & 1) acc1 += double(sv);
-        else acc0 += double(sv);
+      for (int u = 0; u < 4; ++u) {
+        const double s = warp_sum(double(i8_word_dot(wa[u], va)) + double(i8_word_dot(wb[u], vb)));
+        if (lane == 0 && jj + u < nb) red[wid][jj + u] = s;
       }
     }
-    for (; e < nvec; e += 32) acc0 += double(word(ld_stream(reinterpret_cast<const uint4*>(col + e * 16)), e));
-    for (int t = nvec * 16 + lane; t < len; t += 32) acc1 = fma(double(col[t]), double(vs[t]), acc1);
-    const double sacc = warp_sum(acc0 + acc1);
-    if (lane == 0) parts[int64_t(blockIdx.y) * n_loc + j] = sacc;
+    __syncthreads();
+    if (threadIdx.x < nb) {
+      double t = 0.0;
+      for (int w = 0; w < GR_THREADS / 32; ++w) t += red[w][threadIdx.x];
+      parts[int64_t(blockIdx.y) * n_loc + cb + threadIdx.x] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -699,8 +737,7 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
     else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic
       dim3 grid(unsigned(g.groups), unsigned(g.segs));
-      grad_i8f_kernel<<<grid, GR_THREADS, int(sizeof(float) * GR_SEG), st>>>(static_cast<const int8_t*>(X), dmpd, m,
-                                                                             n_loc, g.cpg, parts, flags);
+      grad_i8f_kernel<<<grid, GR_THREADS, 0, st>>>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g.cpg, parts, flags);
     } else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else { set_error("bs_cox_grad_step: unsupported X dtype %d", xdtype); return BS_EINVAL; }
   }
