@@ -160,22 +160,51 @@ extern "C" int64_t bs_cox_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) 
 }
 
 // scn m for int8 X with float32 arithmetic (the dtype of beta): 16 rows per thread (one
-// 16-byte word per column), float partial sums over 32-column blocks added into float64.
+// 16-byte word per column), PRMT widening and packed f32x2 FMAs, float partial sums over
+// 32-column blocks added into float64.
 __global__ void __launch_bounds__(XB_THREADS)
 xbeta_i8f_kernel(const int8_t* __restrict__ X, const float* __restrict__ beta, int64_t m, int64_t n_loc,
                  int64_t cols_per_split, double* __restrict__ parts) {
+  typedef unsigned long long f2x;
+  auto pack = [](float a, float b) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+  };
+  auto fma2 = [](f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+  };
+  auto add2 = [](f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  };
   const int64_t i0 = (int64_t(blockIdx.x) * XB_THREADS + threadIdx.x) * 16;
   const int64_t j_begin = int64_t(blockIdx.y) * cols_per_split;
   const int64_t j_end = min(n_loc, j_begin + cols_per_split);
   if (i0 >= m) return;
+  const f2x off = pack(-8388736.0f, -8388736.0f);
   double accd[16];
 #pragma unroll
   for (int v = 0; v < 16; ++v) accd[v] = 0.0;
+  auto word = [&](uint4 w, float b, f2x* acc) {  // acc[8] pairs += x(16 rows) * b
+    const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+    const f2x bb = pack(b, b);
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const unsigned int p0 = __byte_perm(ww[a], 0x4B000000u, 0x7440u), p1 = __byte_perm(ww[a], 0x4B000000u, 0x7441u);
+      const unsigned int p2 = __byte_perm(ww[a], 0x4B000000u, 0x7442u), p3 = __byte_perm(ww[a], 0x4B000000u, 0x7443u);
+      acc[2 * a] = fma2(add2(pack(__uint_as_float(p0), __uint_as_float(p1)), off), bb, acc[2 * a]);
+      acc[2 * a + 1] = fma2(add2(pack(__uint_as_float(p2), __uint_as_float(p3)), off), bb, acc[2 * a + 1]);
+    }
+  };
   for (int64_t jb = j_begin; jb < j_end; jb += 32) {
     const int64_t je = min(j_end, jb + 32);
-    float acc[16];
+    f2x acc[8];
 #pragma unroll
-    for (int v = 0; v < 16; ++v) acc[v] = 0.f;
+    for (int v = 0; v < 8; ++v) acc[v] = pack(0.f, 0.f);
     int64_t j = jb;
     for (; j + 4 <= je; j += 4) {
       uint4 w[4];
@@ -186,26 +215,16 @@ xbeta_i8f_kernel(const int8_t* __restrict__ X, const float* __restrict__ beta, i
         b[u] = __ldg(beta + j + u);
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const unsigned int ww[4] = {w[u].x ^ 0x80808080u, w[u].y ^ 0x80808080u, w[u].z ^ 0x80808080u,
-                                    w[u].w ^ 0x80808080u};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[4 * a + k] = fmaf(i8_to_f32(ww[a], k), b[u], acc[4 * a + k]);
-      }
+      for (int u = 0; u < 4; ++u) word(w[u], b[u], acc);
     }
-    for (; j < je; ++j) {
-      const uint4 w = ld_stream(reinterpret_cast<const uint4*>(X + j * m + i0));
-      const float b = __ldg(beta + j);
-      const unsigned int ww[4] = {w.x ^ 0x80808080u, w.y ^ 0x80808080u, w.z ^ 0x80808080u, w.w ^ 0x80808080u};
+    for (; j < je; ++j) word(ld_stream(reinterpret_cast<const uint4*>(X + j * m + i0)), __ldg(beta + j), acc);
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) acc[4 * a + k] = fmaf(i8_to_f32(ww[a], k), b, acc[4 * a + k]);
+    for (int v = 0; v < 8; ++v) {
+      float lo, hi;
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc[v]));
+      accd[2 * v] += double(lo);
+      accd[2 * v + 1] += double(hi);
     }
-#pragma unroll
-    for (int v = 0; v < 16; ++v) accd[v] += double(acc[v]);
   }
   double* out = parts + int64_t(blockIdx.y) * m;
 #pragma unroll
