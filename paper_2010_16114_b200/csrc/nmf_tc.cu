@@ -325,12 +325,16 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
           }
           if (stats_part) {  // _nmf_check + ||X||^2 ride on this pass (solvers.py:139-141)
+            // squares summed in fp32 over the row's 32 values (two chains), then into float64
+            float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const float x = __uint_as_float(hi[k]);
-              xmin = fminf(xmin, x);
-              xsq = fma(double(x), double(x), xsq);
+            for (int k = 0; k < 32; k += 2) {
+              const float x0 = __uint_as_float(hi[k]), x1 = __uint_as_float(hi[k + 1]);
+              xmin = fminf(xmin, fminf(x0, x1));
+              s0 = fmaf(x0, x0, s0);
+              s1 = fmaf(x1, x1, s1);
             }
+            xsq += double(s0) + double(s1);
           }
 #pragma unroll
           for (int k = 0; k < 32; ++k) {
