@@ -18,8 +18,8 @@ Usage:
 
 Other workloads (--workload): nmf_mu_c1 (10k x 10k, r=20, float64), mds_c3
 (n=100,000 from 1000-dim points, q=20, float32), cox_c4 (100,000 x 200,000,
-float32, lambda=1e-8), cox_c5 (int8 genotypes 400,000 x 500,000; needs >= 2
-GPUs).  Only the default is the driver's headline line.
+float32, lambda=1e-8), cox_c5 (counter-based int8 genotypes 400,000 x 500,000,
+Breslow ties, 4.5% events; needs >= 2 GPUs).  Only the default is the driver's headline line.
 """
 
 from __future__ import annotations
@@ -183,17 +183,9 @@ def _setup(comm, wl):
     if kind == "cox":
         m, n = wl["m"], wl["n"]
         if wl["dtype"] == "int8":
+            # X_ij ~ Bin(2, MAF_j), MAF_j ~ U(0.05, 0.5), counter-based
             x = bs.empty((m, n), comm, np.int8)
-            gen = torch.Generator(device=comm.device)
-            gen.manual_seed(5 + comm.rank)
-            maf = torch.rand(x.local.shape[1], generator=gen, device=comm.device) * 0.45 + 0.05
-            for c0 in range(0, x.local.shape[1], 4096):
-                c1 = min(c0 + 4096, x.local.shape[1])
-                p = maf[c0:c1]
-                u1 = torch.rand((c1 - c0, m), generator=gen, device=comm.device)
-                u2 = torch.rand((c1 - c0, m), generator=gen, device=comm.device)
-                g = (u1 < p[:, None]).to(torch.int8) + (u2 < p[:, None]).to(torch.int8)
-                x.local[:, c0:c1].copy_(g.t())
+            bs.genotype_fill(x, seed=2016, maf_range=(0.05, 0.5))
             sdt = np.float32
         else:
             x = bs.empty((m, n), comm, np.dtype(wl["dtype"]))
@@ -201,9 +193,16 @@ def _setup(comm, wl):
             gen.manual_seed(2012 + comm.rank)
             x.local.normal_(generator=gen)
             sdt = None
-        y = np.arange(m, 0, -1, dtype=np.float64)          # cli.py:194
-        delta = (np.random.Generator(np.random.Philox(2013)).random(m) > 0.3).astype(np.float64)  # cli.py:195
-        st = bs.cox_init(x, y, delta, lam=wl["lam"], sigma=1e-7, dtype=sdt)
+        if wl["dtype"] == "int8":
+            # C5: tied survival times handled by Breslow,
+            # events ~ Bernoulli(0.045)
+            y = np.floor(np.arange(m, 0, -1, dtype=np.float64) / 4.0)
+            delta = (np.random.Generator(np.random.Philox(2013)).random(m) < 0.045).astype(np.float64)
+            st = bs.cox_init(x, y, delta, lam=wl["lam"], sigma=1e-7, ties="breslow", dtype=sdt)
+        else:
+            y = np.arange(m, 0, -1, dtype=np.float64)          # cli.py:194
+            delta = (np.random.Generator(np.random.Philox(2013)).random(m) > 0.3).astype(np.float64)  # cli.py:195
+            st = bs.cox_init(x, y, delta, lam=wl["lam"], sigma=1e-7, dtype=sdt)
         return st, (lambda k: bs.cox_fit(st, k, trace_every=1)), ["bs_cox_xbeta", "bs_cox_grad_step"], x
     if kind == "mds":
         dt = np.dtype(wl["dtype"])
@@ -369,12 +368,18 @@ def _cpu_baseline(wl, samples=1):
     elif wl["kind"] == "cox":
         m, n = s["m"], s["n"]
         gen = np.random.Generator(np.random.Philox(2012))
-        x = gen.standard_normal((m, n), dtype=np.float32) if wl["dtype"] != "int8" else \
-            gen.binomial(2, 0.2, size=(m, n)).astype(np.float32)
-        delta = (gen.random(m) > 0.3).astype(np.float32)
-        orc.cox_fit(x, delta, np.arange(m), wl["lam"], 1e-7, 1)
+        if wl["dtype"] != "int8":
+            x = gen.standard_normal((m, n), dtype=np.float32)
+            delta = (gen.random(m) > 0.3).astype(np.float32)
+            cuts = np.arange(m)
+        else:  # genotypes, tied times (Breslow cuts, solvers.py:332-334), 4.5% events
+            x = orc.genotype_fill(m, n, 2016).astype(np.float32)
+            delta = (gen.random(m) < 0.045).astype(np.float32)
+            y = np.floor(np.arange(m, 0, -1, dtype=np.float64) / 4.0)
+            cuts = np.searchsorted(-y, -y, side="right") - 1
+        orc.cox_fit(x, delta, cuts, wl["lam"], 1e-7, 1)
         t0 = time.perf_counter()
-        orc.cox_fit(x, delta, np.arange(m), wl["lam"], 1e-7, samples)
+        orc.cox_fit(x, delta, cuts, wl["lam"], 1e-7, samples)
         dt_s = (time.perf_counter() - t0) / samples
         scale = (m * n) / (wl["m"] * wl["n"])
         desc = f"oracle cox_fit on a {m}x{n} float32 sample; it/s scaled by elements ({scale:.3g})"

@@ -81,6 +81,14 @@ int64_t bs_launch_count(void);
 int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t first,
                       uint64_t key0, uint64_t key1, void* stream);
 
+/* Counter-based genotype matrix (the C5 input; no reference
+ * equivalent -- the reference's rand_fill is float-only, distarray.py:176-177):
+ * X[i, j] = [u1 < maf[j - lo]] + [u2 < maf[j - lo]] for the local columns j in
+ * [lo, lo + n_loc), with u1, u2 elements 2e and 2e+1 (e = j*m + i) of
+ * Generator(Philox(key)).random(., float64).  Rank-count independent. */
+int bs_genotype_fill(int8_t* X, const double* maf, int64_t m, int64_t lo, int64_t n_loc,
+                     uint64_t key0, uint64_t key1, void* stream);
+
 /* reduce_all local fold (distarray.py:335-348): out_dev[0] = op over
  * transform(x[0..count)) in float64.  Empty input gives the neutral element. */
 int64_t bs_reduce_workspace(int64_t count);

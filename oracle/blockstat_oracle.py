@@ -331,3 +331,16 @@ def survival_data(seed, m, n, beta_true=None):
     delta = (gen.random(m) > 0.3).astype(np.float64)
     order = np.argsort(-times)
     return x[order], times[order], delta[order]
+
+
+def genotype_fill(m, n, seed, maf_range=(0.05, 0.5)):
+    """Counter-based genotypes (this build's C5 input; the reference has no int8 fill):
+    p_j = lo + (hi - lo) * Generator(Philox(seed + 1)).random(n)[j];
+    X[i, j] = [u[2e] < p_j] + [u[2e + 1] < p_j], e = j*m + i, u = Generator(Philox(seed)).random(2mn).
+    Small sizes only (test infrastructure)."""
+    lo, hi = maf_range
+    p = lo + (hi - lo) * np.random.Generator(np.random.Philox(seed + 1)).random(n)
+    u = np.random.Generator(np.random.Philox(seed)).random(2 * m * n).reshape(m * n, 2)
+    pe = np.repeat(p, m)
+    x = (u[:, 0] < pe).astype(np.int8) + (u[:, 1] < pe).astype(np.int8)
+    return x.reshape((m, n), order="F")

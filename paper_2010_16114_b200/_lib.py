@@ -41,6 +41,7 @@ SIGNATURES = {
     "bs_num_sms": (_i, []),
     "bs_launch_count": (_i64, []),
     "bs_philox_uniform": (_i, [_p, _i, _i64, _i64, _u64, _u64, _p]),
+    "bs_genotype_fill": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),
     "bs_reduce_workspace": (_i64, [_i64]),
     "bs_reduce": (_i, [_p, _i, _i64, _i, _i, _p, _p, _i64, _p]),
     "bs_fold": (_i, [_p, _p, _i, _i64, _i, _i, _p]),

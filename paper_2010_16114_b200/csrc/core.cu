@@ -143,6 +143,46 @@ extern "C" int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t fi
   return check_launch("bs_philox_uniform");
 }
 
+// Counter-based genotypes: X[i, j] = [u1 < p_j] + [u2 < p_j] with u1, u2
+// elements 2e, 2e+1 (e = j*m + i, j global) of Generator(Philox(key)).random(., float64) and
+// p_j = maf[j_local].  Each element depends only on (key, i, j): any rank count / partition
+// produces the same global matrix without a scatter.  One thread per Philox block = 2 elements.
+__global__ void genotype_kernel(int8_t* __restrict__ X, const double* __restrict__ maf, int64_t m, int64_t lo,
+                                int64_t n_loc, uint64_t k0, uint64_t k1) {
+  const int64_t total = m * n_loc;  // local elements, column-major
+  const int64_t e_first = lo * m;   // global index of local element 0
+  const int64_t b_first = e_first / 2, b_last = (e_first + total - 1) / 2;
+  for (int64_t b = b_first + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b <= b_last;
+       b += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t c[4] = {uint64_t(b) + 1ULL, 0ULL, 0ULL, 0ULL};
+    philox4x64_10(c, k0, k1);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t e = 2 * b + h;  // global element; words 2e, 2e+1 = c[2h], c[2h+1]
+      const int64_t el = e - e_first;
+      if (el < 0 || el >= total) continue;
+      const double p = maf[el / m];
+      const double u1 = double(c[2 * h] >> 11) * (1.0 / 9007199254740992.0);
+      const double u2 = double(c[2 * h + 1] >> 11) * (1.0 / 9007199254740992.0);
+      X[el] = int8_t((u1 < p ? 1 : 0) + (u2 < p ? 1 : 0));
+    }
+  }
+}
+
+extern "C" int bs_genotype_fill(int8_t* X, const double* maf, int64_t m, int64_t lo, int64_t n_loc, uint64_t key0,
+                                uint64_t key1, void* stream) {
+  clear_error();
+  if (m < 0 || lo < 0 || n_loc < 0) {
+    set_error("bs_genotype_fill: negative shape");
+    return BS_EINVAL;
+  }
+  if (m == 0 || n_loc == 0) return BS_OK;
+  const int64_t blocks = (m * n_loc + 2) / 2 + 1;
+  const int grid = int(std::min<int64_t>(ceil_div(blocks, 256), int64_t(num_sms()) * 16));
+  genotype_kernel<<<grid, 256, 0, as_stream(stream)>>>(X, maf, m, lo, n_loc, key0, key1);
+  return check_launch("bs_genotype_fill");
+}
+
 // ---------------------------------------------------------------------------
 // reduce_all (distarray.py:335-348) — deterministic two-level fold in float64.
 // ---------------------------------------------------------------------------

@@ -152,3 +152,32 @@ def test_opnorm_power_matches_reference(golden, p):
     assert abs(got - golden["opnorm_l2"][0]) <= 1e-12 * got
     sv = np.linalg.svd(a, compute_uv=False)[0]
     assert abs(got - sv) <= 1e-5 * sv
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_genotype_fill_matches_oracle_and_is_rank_independent(p):
+    """Counter-based genotypes (the C5 input): every element depends only on (seed, i, j)."""
+    m, n, seed = 37, 23, 77
+
+    def fn(comm):
+        x = bs.empty((m, n), comm, np.int8)
+        bs.genotype_fill(x, seed)
+        return bs.gather_full(x)
+
+    want = orc.genotype_fill(m, n, seed)
+    for got in bs.run_inproc(p, fn):
+        np.testing.assert_array_equal(got, want)
+    assert set(np.unique(want)) <= {0, 1, 2}
+
+
+def test_genotype_fill_frequencies():
+    m, n = 20000, 40
+
+    def fn(comm):
+        x = bs.empty((m, n), comm, np.int8)
+        bs.genotype_fill(x, 5, maf_range=(0.1, 0.4))
+        return bs.gather_full(x)
+
+    x = bs.run_inproc(1, fn)[0].astype(np.float64)
+    p = 0.1 + 0.3 * np.random.Generator(np.random.Philox(6)).random(n)
+    np.testing.assert_allclose(x.mean(axis=0), 2 * p, atol=0.03)   # Bin(2, p) means
