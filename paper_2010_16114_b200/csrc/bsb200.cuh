@@ -164,7 +164,7 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
 }
 
 // Grid-stride walk over x[0..count) calling f(double) per element: 16-byte
-// streaming loads, four in flight per thread, scalar head/tail.  Every element is
+// streaming loads, eight in flight per thread, scalar head/tail.  Every element is
 // visited exactly once by exactly one thread; the per-thread order is fixed for
 // a fixed grid, so folds built on it are deterministic.
 template <typename T, typename F>
@@ -180,12 +180,12 @@ __device__ __forceinline__ void stream_elems(const T* __restrict__ x, int64_t co
   const int64_t nvec = (count - head) / V;
   const uint4* xv = reinterpret_cast<const uint4*>(xa);
   int64_t v = tid;
-  for (; v + 3 * nth < nvec; v += 4 * nth) {
-    uint4 w[4];
+  for (; v + 7 * nth < nvec; v += 8 * nth) {
+    uint4 w[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) w[u] = ld_stream(xv + v + u * nth);
+    for (int u = 0; u < 8; ++u) w[u] = ld_stream(xv + v + u * nth);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const T* e = reinterpret_cast<const T*>(&w[u]);
 #pragma unroll
       for (int k = 0; k < V; ++k) f(double(e[k]));

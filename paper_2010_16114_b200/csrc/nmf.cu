@@ -39,16 +39,62 @@ constexpr int MAX_R = 128;
 // _nmf_check + ||X||^2: min and sum of squares in one pass.
 // ---------------------------------------------------------------------------
 
+// float32 data: min and squares in fp32 over each 16-byte word (full-rate FMNMX / FFMA),
+// then into float64; eight words in flight per thread.  NaN propagates like np.min.
+__device__ __forceinline__ void scan_words_f32(const float* __restrict__ x, int64_t count, double& mn, double& sq) {
+  const int64_t tid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t nth = int64_t(gridDim.x) * blockDim.x;
+  const int64_t mis = (reinterpret_cast<uintptr_t>(x) & 15) / 4;
+  const int64_t head = mis ? (count < 4 - mis ? count : 4 - mis) : 0;
+  bool nan = false;
+  float fmn = CUDART_INF_F;
+  auto one = [&](float v) {
+    nan |= (v != v);
+    fmn = fminf(fmn, v);
+    sq = fma(double(v), double(v), sq);
+  };
+  for (int64_t i = tid; i < head; i += nth) one(x[i]);
+  const float4* xv = reinterpret_cast<const float4*>(x + head);
+  const int64_t nvec = (count - head) / 4;
+  int64_t v = tid;
+  for (; v + 7 * nth < nvec; v += 8 * nth) {
+    float4 w[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) w[u] = ld_stream(xv + v + u * nth);
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      nan |= (w[u].x != w[u].x) | (w[u].y != w[u].y) | (w[u].z != w[u].z) | (w[u].w != w[u].w);
+      fmn = fminf(fmn, fminf(fminf(w[u].x, w[u].y), fminf(w[u].z, w[u].w)));
+      s0 = fmaf(w[u].x, w[u].x, s0);
+      s1 = fmaf(w[u].y, w[u].y, s1);
+      s0 = fmaf(w[u].z, w[u].z, s0);
+      s1 = fmaf(w[u].w, w[u].w, s1);
+    }
+    sq += double(s0) + double(s1);
+  }
+  for (; v < nvec; v += nth) {
+    const float4 w = ld_stream(xv + v);
+    one(w.x); one(w.y); one(w.z); one(w.w);
+  }
+  for (int64_t i = head + nvec * 4 + tid; i < count; i += nth) one(x[i]);
+  mn = nan ? CUDART_NAN : rop_apply(BS_MIN, mn, double(fmn));
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 scan_kernel(const T* __restrict__ x, int64_t count, double* __restrict__ parts,
             unsigned int* counter, double* out) {
   __shared__ double shm[32], shs[32];
   double mn = CUDART_INF, sq = 0.0;
-  stream_elems(x, count, [&](double v) {
-    mn = rop_apply(BS_MIN, mn, v);
-    sq = fma(v, v, sq);
-  });
+  if constexpr (sizeof(T) == 4) {
+    scan_words_f32(reinterpret_cast<const float*>(x), count, mn, sq);
+  } else {
+    stream_elems(x, count, [&](double v) {
+      mn = rop_apply(BS_MIN, mn, v);
+      sq = fma(v, v, sq);
+    });
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
