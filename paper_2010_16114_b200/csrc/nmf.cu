@@ -944,6 +944,141 @@ __global__ void __launch_bounds__(128) fold_rows_kernel(const double* __restrict
   out[e] = s;
 }
 
+// Register-blocked variant (RP <= 64): per stage of UPD_COLS columns the old factor
+// columns and NUM (slabs summed, rounded to T) are staged in shared memory; each thread
+// computes den = GRAM f for KB = RP/16 rows x 2 columns (l ascending: the same order as
+// the shuffle kernel, so den is bitwise identical), applies the update, and later
+// accumulates a GB x GB block (GB = RP/16) of the new factor's Gram over the stage.
+// Writes of F (and the copy) go back coalesced from the staged tile.
+template <typename T, typename TN, int RP>
+__global__ void __launch_bounds__(UPD_THREADS)
+factor_update_rb_kernel(int algo, T* __restrict__ F, const TN* __restrict__ num, int S,
+                        int64_t num_slab, const double* __restrict__ gram, int r, int64_t ncols,
+                        double eps, int64_t cols_per_block, T* __restrict__ Fcopy,
+                        double* __restrict__ parts) {
+  static_assert(RP % 16 == 0 && RP <= 64, "register-blocked update needs RP in {16, 32, 64}");
+  constexpr int KB = RP / 16;   // den rows per thread (16 row groups x 16 column pairs)
+  constexpr int GB = RP / 16;   // Gram block edge per thread (16 x 16 thread grid)
+  constexpr int C = UPD_COLS;   // 32 columns per stage
+  extern __shared__ double upd_smem[];
+  auto gT = reinterpret_cast<double (*)[RP]>(upd_smem);                             // [RP][RP]: gram[k][l] at [l][k]
+  auto fs = reinterpret_cast<double (*)[RP + 1]>(upd_smem + RP * RP);               // [C] old columns
+  auto ns = reinterpret_cast<double (*)[RP + 1]>(upd_smem + RP * RP + C * (RP + 1));  // [C] NUM (rounded to T)
+  auto tile = reinterpret_cast<double (*)[RP + 1]>(upd_smem + RP * RP + 2 * C * (RP + 1));  // [C] new columns
+  __shared__ double sh_red[32];
+  __shared__ double sh_step;
+  const int tid = threadIdx.x;
+  const int rr = r * r;
+  for (int e = tid; e < RP * RP; e += UPD_THREADS) {
+    const int l = e / RP, k = e % RP;
+    gT[l][k] = (l < r && k < r) ? gram[k * r + l] : 0.0;
+  }
+  if (tid == 0) {
+    double s = 0.0;
+    for (int e = 0; e < rr; ++e) s = fma(gram[e], gram[e], s);
+    sh_step = 1.0 / (2.0 * s + eps);  // solvers.py:174 / 180
+  }
+  __syncthreads();
+  const double step = sh_step;
+  const int cp = tid & 15, kg = tid >> 4;  // den: columns 2cp, 2cp+1; rows KB*kg ..
+  const int gi = tid & 15, gj = tid >> 4;  // Gram block rows GB*gi.., columns GB*gj..
+  double gacc[GB][GB];
+#pragma unroll
+  for (int a = 0; a < GB; ++a)
+#pragma unroll
+    for (int b = 0; b < GB; ++b) gacc[a][b] = 0.0;
+  double cross = 0.0;
+  const int64_t c_begin = int64_t(blockIdx.x) * cols_per_block;
+  const int64_t c_end = min(ncols, c_begin + cols_per_block);
+  for (int64_t cb = c_begin; cb < c_end; cb += C) {
+    const int nc = int(c_end - cb < C ? c_end - cb : C);
+    __syncthreads();  // stage buffers free
+    // stage old F and NUM (columns contiguous: nc * r elements each, coalesced)
+    for (int e = tid; e < C * RP; e += UPD_THREADS) {
+      const int cc = e / RP, k = e % RP;
+      double f = 0.0, nm = 0.0;
+      if (cc < nc && k < r) {
+        const int64_t o = (cb + cc) * r + k;
+        f = double(F[o]);
+        double sn = double(num[o]);
+        for (int p = 1; p < S; ++p) sn += double(num[int64_t(p) * num_slab + o]);
+        nm = double(T(sn));  // NUM is rounded to the storage type like the reference's WXt / VtX
+      }
+      fs[cc][k] = f;
+      ns[cc][k] = nm;
+    }
+    __syncthreads();
+    // den = GRAM f, update, new column values into the tile
+    {
+      double den[KB][2];
+#pragma unroll
+      for (int a = 0; a < KB; ++a) den[a][0] = den[a][1] = 0.0;
+      for (int l = 0; l < r; ++l) {
+        const double f0 = fs[2 * cp][l], f1 = fs[2 * cp + 1][l];
+#pragma unroll
+        for (int a = 0; a < KB; ++a) {
+          const double g = gT[l][KB * kg + a];
+          den[a][0] = fma(g, f0, den[a][0]);
+          den[a][1] = fma(g, f1, den[a][1]);
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < KB; ++a)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = KB * kg + a, cc = 2 * cp + h;
+          double out = 0.0;
+          if (k < r && cc < nc) {
+            const T dd = T(den[a][h]);  // WWtVt / VtVW in the storage type
+            const T fo = T(fs[cc][k]), nmT = T(ns[cc][k]);
+            T fn;
+            if (algo == BS_NMF_MU) {
+              fn = fo * nmT / (dd + T(eps));
+            } else {
+              const T vv = fo - T(step) * (dd - nmT);
+              fn = vv > T(0) ? vv : T(0);
+            }
+            out = double(fn);
+            cross = fma(ns[cc][k], out, cross);
+          }
+          tile[cc][k] = out;
+        }
+    }
+    __syncthreads();
+    // coalesced write-back of the new columns
+    for (int e = tid; e < nc * r; e += UPD_THREADS) {
+      const int cc = e / r, k = e - cc * r;
+      const T v = T(tile[cc][k]);
+      F[cb * r + e] = v;
+      if (Fcopy) Fcopy[cb * r + e] = v;
+    }
+    // Gram of the new columns: GB x GB block per thread, columns in order
+    for (int cc = 0; cc < nc; ++cc) {
+      double av[GB], bv[GB];
+#pragma unroll
+      for (int a = 0; a < GB; ++a) {
+        av[a] = tile[cc][GB * gi + a];
+        bv[a] = tile[cc][GB * gj + a];
+      }
+#pragma unroll
+      for (int a = 0; a < GB; ++a)
+#pragma unroll
+        for (int b = 0; b < GB; ++b) gacc[a][b] = fma(av[a], bv[b], gacc[a][b]);
+    }
+  }
+  // per-block partial: [r*r gram][cross]
+  double* mine = parts + int64_t(blockIdx.x) * (rr + 1);
+#pragma unroll
+  for (int a = 0; a < GB; ++a)
+#pragma unroll
+    for (int b = 0; b < GB; ++b) {
+      const int k = GB * gi + a, l = GB * gj + b;
+      if (k < r && l < r) mine[k * r + l] = gacc[a][b];
+    }
+  const double csum = block_sum(cross, sh_red);
+  if (tid == 0) mine[rr] = csum;
+}
+
 // >= 64 columns per block, at most 2 blocks per SM (the last block folds grid x (r^2 + 1) partials)
 static int upd_grid(int64_t ncols) {
   return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 64), int64_t(num_sms()) * 2)));
@@ -978,12 +1113,29 @@ static int launch_update(int algo, T* F, const TN* num, int S, int64_t slab, con
   factor_update_kernel<T, TN, RPV><<<grid, UPD_THREADS, smem, st>>>(algo, F, num, S, slab, gram, r, \
                                                                      ncols, eps, cpb, Fcopy, parts,  \
                                                                      counter, red)
-  switch (pick_rp(r)) {
-    case 16: BS_UPD(16); break;
-    case 32: BS_UPD(32); break;
-    case 64: BS_UPD(64); break;
-    default: BS_UPD(128); break;
+  static const bool legacy = getenv("BS_UPD_LEGACY") != nullptr;  // A/B switch
+#define BS_UPD_RB(RPV)                                                                                      \
+  {                                                                                                          \
+    const int sm_rb = int(sizeof(double) * (RPV * RPV + 3 * UPD_COLS * (RPV + 1)));                          \
+    smem_attr(factor_update_rb_kernel<T, TN, RPV>, sm_rb);                                                   \
+    factor_update_rb_kernel<T, TN, RPV><<<grid, UPD_THREADS, sm_rb, st>>>(algo, F, num, S, slab, gram, r, ncols, \
+                                                                          eps, cpb, Fcopy, parts);           \
   }
+  if (!legacy && r <= 64) {
+    switch (pick_rp(r)) {
+      case 16: BS_UPD_RB(16); break;
+      case 32: BS_UPD_RB(32); break;
+      default: BS_UPD_RB(64); break;
+    }
+  } else {
+    switch (pick_rp(r)) {
+      case 16: BS_UPD(16); break;
+      case 32: BS_UPD(32); break;
+      case 64: BS_UPD(64); break;
+      default: BS_UPD(128); break;
+    }
+  }
+#undef BS_UPD_RB
 #undef BS_UPD
   fold_rows_kernel<<<(r * r + 1 + 127) / 128, 128, 0, st>>>(parts, grid, r * r + 1, red);
   return check_launch("factor update", 2);
