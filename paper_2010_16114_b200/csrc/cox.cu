@@ -695,7 +695,7 @@ grad_i8f_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, int6
   const uint4 zero = make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);  // int8 zeros once flipped back
   for (int64_t cb = c0; cb < c1; cb += 32) {
     const int nb = int(c1 - cb < 32 ? c1 - cb : 32);
-    for (int jj = 0; jj < nb; jj += 4) {
+    for (int jj = 0; jj < nb; jj += 4) {  // four columns: eight 16-byte words in flight per lane
       uint4 wa[4], wb[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -707,8 +707,9 @@ grad_i8f_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, int6
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const double s = warp_sum(double(i8_word_dot(wa[u], va)) + double(i8_word_dot(wb[u], vb)));
-        if (lane == 0 && jj + u < nb) red[wid][jj + u] = s;
+        // 32 rows per lane, then the warp's 1024 rows, in float; float64 across warps / segments
+        const float sf = warp_sum(i8_word_dot(wa[u], va) + i8_word_dot(wb[u], vb));
+        if (lane == 0 && jj + u < nb) red[wid][jj + u] = double(sf);
       }
     }
     __syncthreads();
