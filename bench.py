@@ -18,8 +18,9 @@ Usage:
 
 Other workloads (--workload): nmf_mu_c1 (10k x 10k, r=20, float64), mds_c3
 (n=100,000 from 1000-dim points, q=20, float32), cox_c4 (100,000 x 200,000,
-float32, lambda=1e-8), cox_c5 (counter-based int8 genotypes 400,000 x 500,000,
-Breslow ties, 4.5% events; needs >= 2 GPUs).  Only the default is the driver's headline line.
+float32, lambda=1e-8), cox_c5 (counter-based genotypes 400,000 x 500,000 packed
+2 bits per entry, Breslow ties, 4.5% events; fits one GPU), cox_c5_int8 (the same
+matrix stored int8; needs >= 2 GPUs).  Only the default is the driver's headline line.
 """
 
 from __future__ import annotations
@@ -46,8 +47,12 @@ WORKLOADS = {
                    desc="MDS n=100000 points from 1000-dim data, q=20 (BASELINE configs[2])"),
     "cox_c4": dict(kind="cox", m=100_000, n=200_000, dtype="float32", lam=1e-8,
                    desc="l1-Cox 100000x200000, lambda=1e-8 (BASELINE configs[3])"),
-    "cox_c5": dict(kind="cox", m=400_000, n=500_000, dtype="int8", lam=1e-8,
-                   desc="l1-Cox int8 genotypes 400000x500000 (BASELINE configs[4])"),
+    "cox_c5": dict(kind="cox", m=400_000, n=500_000, dtype="int8", storage="u2", lam=1e-8,
+                   desc="l1-Cox genotypes 400000x500000, 2-bit packed (50 GB), float32 arithmetic "
+                        "(BASELINE configs[4])"),
+    "cox_c5_int8": dict(kind="cox", m=400_000, n=500_000, dtype="int8", storage="int8", lam=1e-8,
+                        desc="l1-Cox genotypes 400000x500000 stored int8 (200 GB: >= 2 GPUs), float32 "
+                             "arithmetic (BASELINE configs[4])"),
 }
 
 
@@ -229,7 +234,7 @@ def _setup(comm, wl):
         m, n = wl["m"], wl["n"]
         if wl["dtype"] == "int8":
             # X_ij ~ Bin(2, MAF_j), MAF_j ~ U(0.05, 0.5), counter-based
-            x = bs.empty((m, n), comm, np.int8)
+            x = bs.PackedGenotypes(comm, (m, n)) if wl.get("storage") == "u2" else bs.empty((m, n), comm, np.int8)
             bs.genotype_fill(x, seed=2016, maf_range=(0.05, 0.5))
             sdt = np.float32
         else:
@@ -333,6 +338,8 @@ def _run_b200(args, wl):
 
 
 def _arith_dtype(wl):
+    if wl.get("storage") == "u2":
+        return "u2->f32"
     return {"float32": "f32", "float64": "f64", "int8": "int8->f32"}[wl["dtype"]]
 
 

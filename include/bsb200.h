@@ -44,6 +44,7 @@ extern "C" {
 #define BS_F64 1
 #define BS_I64 2
 #define BS_I8 3
+#define BS_U2 4  /* 2-bit packed genotypes (X only; see bs_genotype_pack) */
 
 /* ReduceOp codes (comm.py:54-58) */
 #define BS_SUM 0
@@ -88,6 +89,17 @@ int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t first,
  * Generator(Philox(key)).random(., float64).  Rank-count independent. */
 int bs_genotype_fill(int8_t* X, const double* maf, int64_t m, int64_t lo, int64_t n_loc,
                      uint64_t key0, uint64_t key1, void* stream);
+
+/* 2-bit packed genotypes (BS_U2): column j of the local block takes
+ * bs_genotype_packed_bytes(m) = ceil(m/64)*16 bytes at offset j * that; genotype i is
+ * bits 2(i%4)..+1 of byte i/4.  Accepted as X by bs_cox_xbeta / bs_cox_grad_step with
+ * float32 arithmetic (dtype BS_F32).  pack / unpack convert from / to int8 blocks;
+ * fill_packed writes the bs_genotype_fill matrix directly packed. */
+int64_t bs_genotype_packed_bytes(int64_t m);
+int bs_genotype_pack(const int8_t* X, int64_t m, int64_t n_loc, void* P, void* stream);
+int bs_genotype_unpack(const void* P, int64_t m, int64_t n_loc, int8_t* X, void* stream);
+int bs_genotype_fill_packed(void* P, const double* maf, int64_t m, int64_t lo, int64_t n_loc,
+                            uint64_t key0, uint64_t key1, void* stream);
 
 /* reduce_all local fold (distarray.py:335-348): out_dev[0] = op over
  * transform(x[0..count)) in float64.  Empty input gives the neutral element. */

@@ -344,3 +344,16 @@ def genotype_fill(m, n, seed, maf_range=(0.05, 0.5)):
     pe = np.repeat(p, m)
     x = (u[:, 0] < pe).astype(np.int8) + (u[:, 1] < pe).astype(np.int8)
     return x.reshape((m, n), order="F")
+
+
+def pack_genotypes_u2(x):
+    """2-bit packing of an (m, n) genotype matrix (this build's BS_U2 layout, include/bsb200.h):
+    column j is ceil(m/64)*16 bytes, genotype i in bits 2(i%4)..+1 of byte i//4, zero pad.
+    Returns the (ld, n) uint8 block, column-major like the device block."""
+    x = np.asarray(x)
+    m, n = x.shape
+    ld = ((m + 63) // 64) * 16
+    g = np.zeros((ld * 4, n), dtype=np.uint8)
+    g[:m] = x.astype(np.uint8) & 3
+    q = g.reshape(ld, 4, n)
+    return (q[:, 0] | (q[:, 1] << 2) | (q[:, 2] << 4) | (q[:, 3] << 6)).astype(np.uint8)

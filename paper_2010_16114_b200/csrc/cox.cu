@@ -131,7 +131,14 @@ __global__ void sum_slabs_f64(const double* __restrict__ parts, int S, int64_t l
   }
 }
 
-static int xsize(int xdtype) { return xdtype == BS_F64 ? 8 : xdtype == BS_F32 ? 4 : 1; }
+static int xsize(int xdtype) { return xdtype == BS_F64 ? 8 : xdtype == BS_F32 ? 4 : 1; }  // BS_U2: 16 rows / word
+
+namespace bs {
+int launch_xbeta_u2(const void* P, const void* beta, bool f64, int64_t m, int64_t n_loc, int64_t splits,
+                    int64_t cps, double* parts, int* splits_used, cudaStream_t st);
+int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t n_loc, int groups, int segs,
+                   int64_t cpg, double* parts, const int* flags, cudaStream_t st);
+}  // namespace bs
 
 struct XbGrid {
   int64_t tiles;
@@ -256,11 +263,22 @@ extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dty
   if (m < 0 || n_loc < 0) { set_error("bs_cox_xbeta: negative shape"); return BS_EINVAL; }
   if (m == 0) return BS_OK;
   if (n_loc == 0) return cudaMemsetAsync(out, 0, sizeof(double) * m, st) == cudaSuccess ? BS_OK : BS_ECUDA;
-  const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  const bool vec_ok = xdtype == BS_U2 ||
+                      ((m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0));
   XbGrid g = xb_grid(xdtype, m, n_loc, vec_ok);
   Workspace ws(work, work_bytes);
   double* parts = g.splits > 1 ? ws.take<double>(int64_t(g.splits) * m) : out;
   if (!parts) { set_error("bs_cox_xbeta: workspace too small"); return BS_EWORK; }
+  if (xdtype == BS_U2) {  // 2-bit packed genotypes (genotype_u2.cu)
+    if (dtype != BS_F32 && dtype != BS_F64) { set_error("bs_cox_xbeta: unsupported dtype %d", dtype); return BS_EINVAL; }
+    int used = 1;
+    launch_xbeta_u2(X, beta, dtype == BS_F64, m, n_loc, g.splits, g.cps, parts, &used, st);
+    if (used > 1)
+      sum_slabs_f64<<<int(std::min<int64_t>(ceil_div(m, 256), 2048)), 256, 0, st>>>(parts, used, m, out);
+    else if (parts != out)
+      cudaMemcpyAsync(out, parts, sizeof(double) * m, cudaMemcpyDeviceToDevice, st);
+    return check_launch("bs_cox_xbeta", used > 1 ? 2 : 1);
+  }
 #define BS_XB(TXT, TBT) launch_xbeta<TXT, TBT>(static_cast<const TXT*>(X), static_cast<const TBT*>(beta), m, n_loc, g, parts, st)
   if (dtype == BS_F64) {
     if (xdtype == BS_F64) BS_XB(double, double);
@@ -741,6 +759,7 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
                                 const int* flags, void* work, int64_t work_bytes, void* stream) {
   clear_error();
   cudaStream_t st = as_stream(stream);
+  if (dtype != BS_F32 && dtype != BS_F64) { set_error("bs_cox_grad_step: unsupported dtype %d", dtype); return BS_EINVAL; }
   if (n_loc == 0) return cudaMemsetAsync(l1_dev, 0, sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
   Workspace ws(work, work_bytes);
   GrGrid g = gr_grid(m, n_loc);
@@ -753,7 +772,9 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
     if (cudaMemsetAsync(parts, 0, sizeof(double) * n_loc, st) != cudaSuccess) return BS_ECUDA;
   } else {
     const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-    if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
+    if (xdtype == BS_U2) {
+      launch_grad_u2(X, dtype == BS_F64, dmpd, m, n_loc, g.groups, g.segs, g.cpg, parts, flags, st);
+    } else if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic
       dim3 grid(unsigned(g.groups), unsigned(g.segs));

@@ -126,11 +126,14 @@ def opnorm(a, which="l2_power", tol=1e-6, maxiter=1000, seed=95376):
     are exact reductions (not on the hot path).
     """
     torch = _torch()
-    if not isinstance(a, DistArray) or a.ndim != 2:
+    packed = getattr(a, "packed", False)
+    if not (isinstance(a, DistArray) or packed) or a.ndim != 2:
         raise TypeError("opnorm expects a 2-D DistArray")
     m, n = a.shape
     if m == 0 or n == 0:
         raise ShapeError("opnorm of an empty matrix")
+    if packed and which != "l2_power":
+        raise TypeError("packed genotypes support opnorm(..., 'l2_power') only; unpack_genotypes first")
     comm = a.comm
     if which == "l1":
         local = a.local.double().abs().sum(dim=0).max().reshape(1) if a.local.numel() else \
@@ -154,7 +157,7 @@ def opnorm(a, which="l2_power", tol=1e-6, maxiter=1000, seed=95376):
     v /= np.linalg.norm(v)
     v_loc = torch.from_numpy(np.ascontiguousarray(v[a.lo:a.hi])).to(dev)
     n_loc = a.hi - a.lo
-    xcode = _lib.dtype_code(a.dtype)
+    xcode = _lib.xcode(a)
     single = a.dtype == np.dtype(np.float32)
     u = torch.zeros(m + 1, dtype=torch.float64, device=dev)
     w_loc = torch.zeros(max(n_loc, 1), dtype=torch.float64, device=dev)

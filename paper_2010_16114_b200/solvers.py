@@ -605,8 +605,8 @@ def _xbeta(s, beta_local):
     xb = s._dev["xb"]
     st = _lib.stream_ptr()
     local_reduce(beta_local, ReduceOp.SUM, _lib.BS_T_ABS, out=xb[m:m + 1])
-    wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", _lib.dtype_code(x.dtype), m, n_loc))
-    _lib.call("bs_cox_xbeta", _lib.ptr(_flat_local(x)), _lib.dtype_code(x.dtype), _lib.ptr(beta_local),
+    wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", _lib.xcode(x), m, n_loc))
+    _lib.call("bs_cox_xbeta", _lib.ptr(_flat_local(x)), _lib.xcode(x), _lib.ptr(beta_local),
               _lib.dtype_code(beta_local.dtype), m, n_loc, _lib.ptr(xb), wp, wn, st)
     if comm.size > 1:
         comm.allreduce(xb, ReduceOp.SUM)
@@ -687,7 +687,7 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
     dev = x.comm.device
     st = _lib.stream_ptr()
     code = _lib.dtype_code(s.beta.dtype)
-    xcode = _lib.dtype_code(x.dtype)
+    xcode = _lib.xcode(x)
     sigma, lam = float(s.sigma), float(s.lam)
     xb = s._dev["xb"]
     dmpd = s._dev["dmpd"]

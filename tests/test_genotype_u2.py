@@ -1,0 +1,189 @@
+"""2-bit packed genotypes: the packed block feeds the same Cox / opnorm
+kernels as int8 X and must give the int8 results.
+
+CPU tests pin the oracle's packing against a per-element loop; the gpu tests check the
+device pack / unpack / fill against it, and the packed scn-m / scn-p kernels and full
+cox_fit traces against the int8 path and the oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2010_16114_b200 as bs
+from paper_2010_16114_b200 import _lib
+from oracle import blockstat_oracle as orc
+
+
+def _loop_pack(x):
+    m, n = x.shape
+    ld = ((m + 63) // 64) * 16
+    out = np.zeros((ld, n), dtype=np.uint8)
+    for j in range(n):
+        for i in range(m):
+            out[i // 4, j] |= (int(x[i, j]) & 3) << (2 * (i % 4))
+    return out
+
+
+@pytest.mark.parametrize("m", [1, 3, 64, 65, 130])
+def test_oracle_packing_matches_loop(m):
+    x = np.random.Generator(np.random.Philox(m)).integers(0, 3, size=(m, 5)).astype(np.int8)
+    np.testing.assert_array_equal(orc.pack_genotypes_u2(x), _loop_pack(x))
+    assert bs.packed_bytes_per_column(m) == orc.pack_genotypes_u2(x).shape[0]
+
+
+def _device_block(p):
+    return p.local.cpu().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(1, 3), (15, 4), (64, 7), (65, 9), (1000, 33), (8193, 5)])
+def test_pack_unpack_match_oracle(m, n):
+    x = np.random.Generator(np.random.Philox(m + n)).integers(0, 3, size=(m, n)).astype(np.int8)
+    want = orc.pack_genotypes_u2(x)
+
+    def fn(comm):
+        a = bs.distribute(x if comm.rank == 0 else None, comm)
+        p = bs.pack_genotypes(a)
+        assert p.local.shape == (want.shape[0], p.hi - p.lo)
+        np.testing.assert_array_equal(_device_block(p), want[:, p.lo:p.hi])
+        return bs.gather_full(bs.unpack_genotypes(p))
+
+    for p in (1, 3):
+        for got in bs.run_inproc(p, fn):
+            np.testing.assert_array_equal(got, x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [37, 64, 131])
+def test_fill_packed_matches_int8_fill(m):
+    """Packed fill = pack(int8 fill) for odd m (Philox blocks straddling columns) and p ranks."""
+    n, seed = 23, 77
+    want = orc.pack_genotypes_u2(orc.genotype_fill(m, n, seed))
+
+    def fn(comm):
+        p = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        return p.lo, _device_block(p)
+
+    for ranks in (1, 3):
+        for lo, blk in bs.run_inproc(ranks, fn):
+            np.testing.assert_array_equal(blk, want[:, lo:lo + blk.shape[1]])
+
+
+def _xbeta_grad(X, code, beta, v, dtype):
+    """Raw C-ABI calls: xb = X beta and g = X^T v for one local block."""
+    m, n_loc = v.numel(), beta.numel()
+    dev = beta.device
+    tcode = _lib.dtype_code(dtype)
+    xb = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+    ws = torch.zeros(max(_lib.query("bs_cox_xbeta_workspace", code, m, n_loc), 256), dtype=torch.uint8, device=dev)
+    _lib.call("bs_cox_xbeta", _lib.ptr(X), code, _lib.ptr(beta), tcode, m, n_loc, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    grad = torch.zeros(n_loc, dtype=dtype, device=dev)
+    dummy = torch.zeros(n_loc, dtype=dtype, device=dev)
+    l1 = torch.zeros(1, dtype=torch.float64, device=dev)
+    wg = torch.zeros(max(_lib.query("bs_cox_grad_workspace", code, m, n_loc), 256), dtype=torch.uint8, device=dev)
+    _lib.call("bs_cox_grad_step", _lib.ptr(X), code, _lib.ptr(v), tcode, m, n_loc, _lib.ptr(grad), _lib.ptr(dummy),
+              0.0, 0.0, 0, _lib.ptr(l1), None, _lib.ptr(wg), wg.numel(), _lib.stream_ptr())
+    return xb[:m].cpu().numpy(), grad.cpu().numpy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("m,n", [(100, 7), (4096, 65), (20000, 300), (9000, 1)])
+def test_packed_scans_match_int8(dtype, m, n):
+    gen = np.random.Generator(np.random.Philox(3 * m + n))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    beta = gen.standard_normal(n)
+    v = gen.standard_normal(m)
+    dev = torch.device("cuda:0")
+    X8 = torch.from_numpy(np.asfortranarray(x).ravel(order="F")).to(dev)
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    b = torch.from_numpy(beta).to(dev, dtype)
+    vd = torch.from_numpy(v).to(dev)
+    xb8, g8 = _xbeta_grad(X8, _lib.BS_I8, b, vd, dtype)
+    xbp, gp = _xbeta_grad(XP, _lib.BS_U2, b, vd, dtype)
+    bh = b.double().cpu().numpy()
+    want_xb = x.astype(np.float64) @ bh
+    want_g = x.astype(np.float64).T @ v
+    rtol = 1e-12 if dtype == torch.float64 else 2e-5
+    scale_xb = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
+    scale_g = np.abs(x).astype(np.float64).T @ np.abs(v) + 1e-300
+    for got, ref, sc in ((xbp, want_xb, scale_xb), (xb8, want_xb, scale_xb), (gp, want_g, scale_g),
+                         (g8, want_g, scale_g)):
+        assert np.max(np.abs(got - ref) / sc) < rtol
+    np.testing.assert_allclose(xbp, xb8, rtol=0, atol=rtol * scale_xb.max())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [1, 2])
+def test_cox_fit_packed_matches_int8_and_oracle(p):
+    m, n, seed, iters = 3000, 257, 11, 12
+    x = orc.genotype_fill(m, n, seed)
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(2)).random(m) < 0.6).astype(np.float64)
+    lam = 0.05
+
+    def fn(comm, packed):
+        if packed:
+            a = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        else:
+            a = bs.genotype_fill(bs.empty((m, n), comm, np.int8), seed)
+        st = bs.cox_init(a, y, delta, lam, ties="breslow", dtype=np.float32)
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace, dtype=np.float64), bs.gather_full(st.beta), st.sigma
+
+    int8_runs = bs.run_inproc(p, lambda c: fn(c, False))
+    packed_runs = bs.run_inproc(p, lambda c: fn(c, True))
+    (t8, b8, s8), (tp, bp, sp) = int8_runs[0], packed_runs[0]
+    np.testing.assert_allclose(sp, s8, rtol=1e-10)  # opnorm through the packed kernels
+    np.testing.assert_allclose(tp, t8, rtol=2e-5)
+    np.testing.assert_allclose(bp, b8, rtol=2e-3, atol=2e-5 * np.abs(b8).max())
+    _, _, otr = orc.cox_fit(x.astype(np.float64), delta, orc.tie_cuts(y), lam, sp, iters)
+    np.testing.assert_allclose(tp, otr, rtol=5e-5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [1e-35, 1e-12, 1.0, 1e20])
+def test_packed_grad_any_v_scale(scale):
+    """The packed scn-p kernel rescales each lane's v by a power of two (subnormal widening);
+    results must keep float32 accuracy for tiny and huge v, and with mixed magnitudes."""
+    m, n = 20000, 70
+    gen = np.random.Generator(np.random.Philox(17))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    v = gen.standard_normal(m) * scale
+    v[::7] *= 1e-6  # mixed magnitudes inside one lane's rows
+    v[5::97] = 0.0
+    dev = torch.device("cuda:0")
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    vd = torch.from_numpy(v).to(dev)
+    b = torch.zeros(n, dtype=torch.float32, device=dev)
+    _, gp = _xbeta_grad(XP, _lib.BS_U2, b, vd, torch.float32)
+    want = x.astype(np.float64).T @ v.astype(np.float32).astype(np.float64)
+    sc = np.abs(x).astype(np.float64).T @ np.abs(v)
+    assert np.all(np.isfinite(gp))
+    assert np.max(np.abs(gp - want) / sc) < 2e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e25])
+def test_packed_xbeta_any_beta_scale(scale):
+    """The packed scn-m kernel scales beta by a power of two per CTA (subnormal widening)."""
+    m, n = 9000, 300
+    gen = np.random.Generator(np.random.Philox(19))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    beta = (gen.standard_normal(n) * scale).astype(np.float32)
+    beta[::5] *= np.float32(1e-5)
+    beta[3::11] = 0.0
+    dev = torch.device("cuda:0")
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    b = torch.from_numpy(beta).to(dev)
+    xbp, _ = _xbeta_grad(XP, _lib.BS_U2, b, torch.zeros(m, dtype=torch.float64, device=dev), torch.float32)
+    bh = beta.astype(np.float64)
+    want = x.astype(np.float64) @ bh
+    sc = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
+    assert np.all(np.isfinite(xbp))
+    if scale > 1e-30:
+        assert np.max(np.abs(xbp - want) / sc) < 2e-5
+    else:  # |beta| below 2^-104: subnormal products, absolute error <= 2^-127 per product
+        assert np.max(np.abs(xbp - want)) < n * 2.0 ** -127
