@@ -173,3 +173,28 @@ def test_tcp_descriptor_validation():
     for bad in ("tcp:", "tcp:127.0.0.1:1", "tcp:127.0.0.1:x,rank=0", "tcp:127.0.0.1:1,rank=3", "bogus"):
         with pytest.raises(bs.CommInitError):
             bs.init(bad)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_standard_normal_chunked_stream_cpu(monkeypatch, dtype):
+    """standard_normal is drawn on the host in bounded chunks and scattered chunk by chunk;
+    the content equals one numpy call (chunk-invariant stream), for any rank count."""
+    from oracle import blockstat_oracle as orc
+    from paper_2010_16114_b200 import distarray as bda
+
+    monkeypatch.setattr(bda, "_NORMAL_CHUNK", 7)
+    shape = (5, 11)
+    want = orc.rand_fill_common(shape, 21, dtype, "standard_normal")
+
+    def fn(comm):
+        a = bs.empty(shape, comm, dtype)
+        bs.rand_fill(a, seed=21, common_init=True, dist="standard_normal")
+        b = bs.empty(shape, comm, dtype)
+        bs.rand_fill(b, seed=30, dist="standard_normal")  # per-rank stream seed + rank
+        return bs.gather_full(a), b.lo, fortran_flat(b.local)[0].cpu().numpy()
+
+    for p in (1, 3, 4):
+        for rank, (full, lo, blk) in enumerate(bs.run_inproc(p, fn)):
+            np.testing.assert_array_equal(full, want)
+            own = np.random.Generator(np.random.Philox(30 + rank)).standard_normal(blk.size, dtype=dtype)
+            np.testing.assert_array_equal(blk, own)
