@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 using namespace bs;
 
@@ -869,6 +870,32 @@ __device__ __forceinline__ void fu_wait(uint32_t bar, uint32_t parity) {  // tra
     }
   }
 }
+constexpr int FU_F32_KB = 4;                     // float4 row groups per consumer thread
+constexpr int64_t FU_F32_SEGMAX = 1024 * FU_F32_KB;  // largest segment of the float32 fast path
+typedef unsigned long long u2f;
+__device__ __forceinline__ u2f f2_pack(float a, float b) {
+  u2f r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(u2f v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ u2f f2_fma(u2f a, u2f b, u2f c) {
+  u2f d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u2f f2_add(u2f a, u2f b) {
+  u2f d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float f2_hsum(u2f v) {
+  float a, b;
+  f2_unpack(v, a, b);
+  return a + b;
+}
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -897,6 +924,10 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
   double* gsum = bnew + W;                                                                  // [FU_CONS]
   uint64_t* bars = reinterpret_cast<uint64_t*>(gsum + FU_CONS);  // full[S], empty[S], bfull[BS], bempty[BS], pfull[2], pempty[2]
   constexpr int PB0 = 2 * FU_STAGES + 2 * FU_BSTAGES;
+  // float32 X with float32 arithmetic (the C4 setting) runs float fast paths: v as float in
+  // smem next to the barriers, xb for the CTA's rows in registers (seg <= FU_F32_SEGMAX)
+  constexpr bool F32 = std::is_same<TX, float>::value && std::is_same<TB, float>::value;
+  float* vsegf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(bars + PB0 + 4) + 15) & ~uintptr_t(15));  // [seg]
   __shared__ double l1_sh[FU_CONS / 32];
   auto bar_u32 = [&](int i) { return static_cast<uint32_t>(__cvta_generic_to_shared(bars + i)); };
   const int64_t nwaves = (n_loc + W - 1) / W;
@@ -919,6 +950,7 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
   for (int i = tid; i < rows; i += FU_THREADS) {
     vseg[i] = v[r0 + i];
     xbseg[i] = 0.0;
+    if constexpr (F32) vsegf[i] = float(v[r0 + i]);
   }
   __syncthreads();
 
@@ -985,6 +1017,9 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
   // ---------------- consumers (warps 1..8) ----------------
   const int ct = tid - 32, cw = warp - 1;  // consumer thread / warp index
   double l1 = 0.0;
+  double xbr[F32 ? 4 * FU_F32_KB : 1];  // F32: rows 4ct + 1024k + e of the CTA's segment
+#pragma unroll
+  for (int e = 0; e < (F32 ? 4 * FU_F32_KB : 1); ++e) xbr[e] = 0.0;
   int64_t k = 0, kb = 0;
   auto cons_sync = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
   for (int64_t w = 0; w < nwaves + FU_LAG; ++w) {
@@ -998,7 +1033,19 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
         fu_wait(bar_u32(s), uint32_t((k / FU_STAGES) & 1));
         const int64_t j = w * W + q * FU_CW + cw;
         double acc = 0.0;
-        if (j < n_loc) {
+        if constexpr (F32) {
+          if (j < n_loc) {
+            const float* col = reinterpret_cast<const float*>(ring + s * stage_elems + int64_t(cw) * seg);
+            u2f a0 = f2_pack(0.f, 0.f), a1 = f2_pack(0.f, 0.f);
+            for (int i = 4 * lane; i < rows; i += 128) {
+              const float4 x = *reinterpret_cast<const float4*>(col + i);
+              const float4 vv = *reinterpret_cast<const float4*>(vsegf + i);
+              a0 = f2_fma(f2_pack(x.x, x.y), f2_pack(vv.x, vv.y), a0);
+              a1 = f2_fma(f2_pack(x.z, x.w), f2_pack(vv.z, vv.w), a1);
+            }
+            acc = double(warp_sum(f2_hsum(f2_add(a0, a1))));
+          }
+        } else if (j < n_loc) {
           const TX* col = ring + s * stage_elems + int64_t(cw) * seg;
           double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
           int i = lane;
@@ -1013,7 +1060,7 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
           for (; i < rows; i += 32) a0 = fma(double(col[i]), vseg[i], a0);
           acc = (a0 + a1) + (a2 + a3);
         }
-        acc = warp_sum(acc);
+        if constexpr (!F32) acc = warp_sum(acc);
         if (lane == 0) {
           part[q * FU_CW + cw] = acc;
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_u32(FU_STAGES + s)) : "memory");
@@ -1066,7 +1113,33 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
         fu_wait(bar_u32(2 * FU_STAGES + s), uint32_t((kb / FU_BSTAGES) & 1));
         const TX* tile = bring + s * stage_elems;
         const int ncq = min(FU_CW, nc - q * FU_CW);
-        if (ncq == FU_CW) {  // full stage: the 8 coefficients in registers, compile-time column loop
+        if constexpr (F32) {
+          float bq[FU_CW];
+#pragma unroll
+          for (int jj = 0; jj < FU_CW; ++jj) bq[jj] = jj < ncq ? float(bnew[q * FU_CW + jj]) : 0.f;
+          const float* tf = reinterpret_cast<const float*>(tile);
+#pragma unroll
+          for (int kq = 0; kq < FU_F32_KB; ++kq) {
+            const int i = 4 * ct + 1024 * kq;
+            if (i < rows) {
+              u2f lo = f2_pack(0.f, 0.f), hi = f2_pack(0.f, 0.f);
+#pragma unroll
+              for (int jj = 0; jj < FU_CW; ++jj) {  // absent columns: stale smem times 0
+                const float4 x = *reinterpret_cast<const float4*>(tf + int64_t(jj) * seg + i);
+                const u2f bb = f2_pack(bq[jj], bq[jj]);
+                lo = f2_fma(f2_pack(x.x, x.y), bb, lo);
+                hi = f2_fma(f2_pack(x.z, x.w), bb, hi);
+              }
+              float l0, l1_, h0, h1;
+              f2_unpack(lo, l0, l1_);
+              f2_unpack(hi, h0, h1);
+              xbr[4 * kq] += double(l0);
+              xbr[4 * kq + 1] += double(l1_);
+              xbr[4 * kq + 2] += double(h0);
+              xbr[4 * kq + 3] += double(h1);
+            }
+          }
+        } else if (ncq == FU_CW) {  // full stage: the 8 coefficients in registers, compile-time column loop
           double bq[FU_CW];
 #pragma unroll
           for (int jj = 0; jj < FU_CW; ++jj) bq[jj] = bnew[q * FU_CW + jj];
@@ -1091,7 +1164,17 @@ cox_fused_kernel(const TX* __restrict__ X, int64_t m, int64_t n_loc, int64_t seg
       cons_sync();  // bnew / gsum / pbuf reusable
     }
   }
-  for (int i = ct; i < rows; i += FU_CONS) xb_out[r0 + i] = xbseg[i];
+  if constexpr (F32) {
+#pragma unroll
+    for (int kq = 0; kq < FU_F32_KB; ++kq)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = 4 * ct + 1024 * kq + e;
+        if (i < rows) xb_out[r0 + i] = xbr[4 * kq + e];
+      }
+  } else {
+    for (int i = ct; i < rows; i += FU_CONS) xb_out[r0 + i] = xbseg[i];
+  }
   if (c == 0) {  // ||beta_new||_1 in a fixed order: consumer threads by column residue, warps in order
     const double sm = warp_sum(l1);
     if (lane == 0) l1_sh[cw] = sm;
@@ -1126,7 +1209,7 @@ static FuPlan fu_plan(int xdtype, int64_t m, int64_t n_loc) {
   const int64_t budget = int64_t(maxsm) - 2048;
   const int W = 32;
   const int64_t need = int64_t(FU_STAGES + FU_BSTAGES) * FU_CW * seg * es + 2 * int64_t(G) * W * 8 + 2 * seg * 8 +
-                       (FU_LAG + 2) * W * 8 + FU_CONS * 8 + (2 * (FU_STAGES + FU_BSTAGES) + 4) * 8 + 64;
+                       (FU_LAG + 2) * W * 8 + FU_CONS * 8 + (2 * (FU_STAGES + FU_BSTAGES) + 4) * 8 + seg * 4 + 80;
   if (need > budget) return p;
   p.ok = true;
   p.grid = int(std::min<int64_t>(G, ceil_div(m, seg)));
@@ -1168,10 +1251,28 @@ static int64_t fused_ws(const FuPlan& p) {
   return ws_bytes<unsigned int>(FU_RING) + ws_bytes<double>(int64_t(FU_RING) * p.grid * p.W);
 }
 
+namespace bs {  // cox_fused2.cu: 2-D grid one-stream pass, float32 X and arithmetic
+struct F2Plan {
+  bool ok;
+  int S, Gc;
+  int64_t R, cpg;
+  size_t smem;
+};
+F2Plan f2_plan(int64_t m, int64_t n_loc);
+int64_t f2_workspace(const F2Plan& p, int64_t m);
+int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const double* v, float* grad, float* beta,
+              double sigma, double lam, double* xb_out, const int* flags, Workspace& ws, cudaStream_t st);
+}  // namespace bs
+
 extern "C" int64_t bs_cox_grad_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) {
   const FuPlan p = fu_plan(xdtype, m, n_loc);
   const int64_t two = bs_cox_grad_workspace(xdtype, m, n_loc) + bs_cox_xbeta_workspace(xdtype, m, n_loc) + 512;
-  return std::max<int64_t>(p.ok ? fused_ws(p) : 0, two);
+  int64_t need = std::max<int64_t>(p.ok ? fused_ws(p) : 0, two);
+  if (xdtype == BS_F32) {
+    const F2Plan q = f2_plan(m, n_loc);
+    if (q.ok) need = std::max<int64_t>(need, f2_workspace(q, m) + 512);
+  }
+  return need;
 }
 
 extern "C" int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, int dtype, int64_t m, int64_t n_loc,
@@ -1180,10 +1281,19 @@ extern "C" int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, 
   clear_error();
   cudaStream_t st = as_stream(stream);
   if (m < 0 || n_loc < 0) { set_error("bs_cox_grad_xbeta: negative shape"); return BS_EINVAL; }
+  if (allow_fused && xdtype == BS_F32 && dtype == BS_F32 && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    const F2Plan q = f2_plan(m, n_loc);
+    if (q.ok) {
+      Workspace ws(work, work_bytes);
+      return f2_launch(q, static_cast<const float*>(X), m, n_loc, dmpd, static_cast<float*>(grad),
+                       static_cast<float*>(beta), sigma, lam, xb_out, flags, ws, st);
+    }
+  }
   const FuPlan p = fu_plan(xdtype, m, n_loc);
   const bool fuse = allow_fused && p.ok && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
                     (dtype == BS_F32 || dtype == BS_F64) &&
-                    (xdtype == BS_F32 || xdtype == BS_F64 || xdtype == BS_I8);
+                    (xdtype == BS_F32 || xdtype == BS_F64 || xdtype == BS_I8) &&
+                    !(xdtype == BS_F32 && dtype == BS_F32 && p.seg > FU_F32_SEGMAX);
   if (!fuse) {
     // two passes: scn p + prox (l1 -> xb_out[m]), then scn m with the new beta
     Workspace ws(work, work_bytes);

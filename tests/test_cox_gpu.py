@@ -258,7 +258,9 @@ def test_cox_unpenalized_gradient_vanishes_at_optimum():
 
 
 @pytest.mark.parametrize("xdt,bdt,m,n", [(torch.float32, torch.float32, 4004, 777), (torch.float64, torch.float64, 3002, 301),
-                                         (torch.int8, torch.float32, 8000, 250), (torch.float32, torch.float64, 5000, 33)])
+                                         (torch.int8, torch.float32, 8000, 250), (torch.float32, torch.float64, 5000, 33),
+                                         (torch.float32, torch.float32, 20004, 3001),
+                                         (torch.float32, torch.float32, 100000, 1999)])
 def test_fused_grad_xbeta_pass_matches_two_pass(xdt, bdt, m, n):
     """bs_cox_grad_xbeta: the cooperative one-stream pass (allow_fused=1) gives the same
     grad, prox step, ||beta||_1 and X beta_new as bs_cox_grad_step + bs_cox_xbeta."""
