@@ -1254,7 +1254,7 @@ static int64_t fused_ws(const FuPlan& p) {
 namespace bs {  // cox_fused2.cu: 2-D grid one-stream pass, float32 X and arithmetic
 struct F2Plan {
   bool ok;
-  int S, Gc;
+  int S, Gc, cfg;
   int64_t R, cpg;
   size_t smem;
 };

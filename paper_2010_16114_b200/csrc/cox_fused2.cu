@@ -32,10 +32,7 @@ constexpr int F2_THREADS = 320;  // warp 0: A producer, warp 1: B producer, warp
 constexpr int F2_CW = 4;         // columns per ring stage
 constexpr int F2_W = 16;         // columns per wave
 constexpr int F2_QPW = F2_W / F2_CW;
-constexpr int F2_LAG = 2;        // waves between A(w) and B(w)
-constexpr int F2_RING = 8;       // partial slots / counters per group (> 2 LAG)
-constexpr int F2_AS = 2;         // A stages (HBM)
-constexpr int F2_BS = 2;         // B stages (L2)
+constexpr int F2_RING = 12;      // partial slots / counters per group (> 2 LAG)
 constexpr int F2_KB = 3;         // float4 row groups per consumer thread: R <= 3072
 constexpr int64_t F2_RMAX = 1024 * F2_KB;
 constexpr int64_t F2_STAGE_MAX = 48 * 1024;  // bytes of one stage (F2_CW columns x R rows)
@@ -68,7 +65,7 @@ __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, 256;" ::
 struct F2Args {
   const float* X;
   int64_t m, n_loc, R, cpg;
-  int S, Gc;
+  int S, Gc, pf;  // pf: stages of X prefetched into L2 ahead of the A ring (0 = off)
   const double* v;
   float* grad;
   float* beta;
@@ -80,7 +77,10 @@ struct F2Args {
   const int* flags;
 };
 
+// F2_AS A stages (HBM), F2_BS B stages (L2), F2_LAG waves between A(w) and B(w)
+template <int F2_AS, int F2_BS, int F2_LAG>
 __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args a) {
+  static_assert(F2_RING > 2 * F2_LAG, "partial slots must outlive the lag");
   extern __shared__ __align__(1024) uint8_t smem[];
   if (a.flags && (*a.flags & BS_FLAG_NONFINITE)) return;  // every CTA sees the same flag
   const int S = a.S, g = int(blockIdx.x) / S, sg = int(blockIdx.x) % S;
@@ -128,9 +128,24 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
     if (lane == 0 && rows > 0) {
       uint64_t keep;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
+      const int nst = nw * F2_QPW;
+      for (int k = 0; k < min(a.pf, nst); ++k)  // L2 prefetch of the first pf stages
+        for (int jj = 0; jj < F2_CW; ++jj) {
+          const int64_t j = c0 + int64_t(k) * F2_CW + jj;
+          if (j < c1)
+            asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a.X + j * m + r0),
+                         "r"(bytes_col), "l"(keep) : "memory");
+        }
       for (int w = 0; w < nw; ++w)
         for (int q = 0; q < F2_QPW; ++q) {
           const int k = w * F2_QPW + q, s = k % F2_AS;
+          if (a.pf > 0 && k + a.pf < nst)
+            for (int jj = 0; jj < F2_CW; ++jj) {
+              const int64_t j = c0 + int64_t(k + a.pf) * F2_CW + jj;
+              if (j < c1)
+                asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(a.X + j * m + r0),
+                             "r"(bytes_col), "l"(keep) : "memory");
+            }
           mbar_wait_sleep(bar(AE + s), uint32_t((k / F2_AS) & 1) ^ 1u);
           const int64_t j0 = c0 + int64_t(w) * F2_W + q * F2_CW;
           const int nc = int(c1 - j0 <= 0 ? 0 : (c1 - j0 < F2_CW ? c1 - j0 : F2_CW));
@@ -194,11 +209,15 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
       xbr[4 * k + e] = 0.0;
     }
   double l1 = 0.0;
+  float bpre = (ct < F2_W && c0 + ct < c1) ? a.beta[c0 + ct] : 0.f;  // beta of the next wave, loaded a wave early
   for (int w = 0; w < nw + F2_LAG; ++w) {
     if (w < nw) {
       // ---- A(w): per-thread partial of each of the wave's 16 columns ----
-      const int64_t jw = c0 + int64_t(w) * F2_W;
-      if (ct < F2_W) bold[(w % (F2_LAG + 1)) * F2_W + ct] = jw + ct < c1 ? double(a.beta[jw + ct]) : 0.0;
+      if (ct < F2_W) {
+        bold[(w % (F2_LAG + 1)) * F2_W + ct] = double(bpre);
+        const int64_t jn = c0 + int64_t(w + 1) * F2_W + ct;
+        bpre = jn < c1 ? a.beta[jn] : 0.f;
+      }
       float cs[F2_W];
 #pragma unroll
       for (int q = 0; q < F2_QPW; ++q) {
@@ -346,7 +365,7 @@ namespace bs {
 
 struct F2Plan {
   bool ok;
-  int S, Gc;
+  int S, Gc, cfg;
   int64_t R, cpg;
   size_t smem;
 };
@@ -363,7 +382,16 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (!coop) return p;
   const int G = num_sms();
-  const int64_t rmax = std::min<int64_t>(F2_RMAX, F2_STAGE_MAX / (4 * F2_CW));
+  static const int cfg = [] {
+    const char* c = getenv("BS_F2_CFG");
+    return c ? atoi(c) : 0;
+  }();
+  static const int as_[9] = {2, 3, 2, 3, 2, 3, 3, 2, 4}, bs_[9] = {2, 1, 2, 1, 2, 2, 2, 3, 2},
+                   lag_[9] = {2, 2, 3, 3, 4, 3, 2, 2, 2};
+  const int ci = cfg >= 0 && cfg < 9 ? cfg : 0;
+  p.cfg = ci;
+  const int nst = as_[ci] + bs_[ci];
+  const int64_t rmax = std::min<int64_t>(F2_RMAX, (4 * F2_STAGE_MAX / nst) / (4 * F2_CW));
   int best_s = 0, best_u = 0;
   for (int S = int(ceil_div(m, rmax)); S <= G; ++S) {
     const int u = S * (G / S);
@@ -376,8 +404,8 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
   p.R = ceil_div(ceil_div(m, p.S), int64_t(4)) * 4;
   if (p.R > rmax) return p;
   p.cpg = ceil_div(n_loc, int64_t(p.Gc));
-  p.smem = size_t((F2_AS + F2_BS) * F2_CW * p.R * 4 + 2 * int64_t(p.S) * F2_W * 8 + (F2_LAG + 1) * F2_W * 8 +
-                  2 * F2_W * 4 + 2 * 8 * F2_W * 4 + (2 * F2_AS + 2 * F2_BS + 4) * 8 + 64);
+  p.smem = size_t(nst * F2_CW * p.R * 4 + 2 * int64_t(p.S) * F2_W * 8 + (lag_[ci] + 1) * F2_W * 8 +
+                  2 * F2_W * 4 + 2 * 8 * F2_W * 4 + (2 * nst + 4) * 8 + 64);
   if (int64_t(p.smem) > int64_t(maxsm) - 1024) return p;
   p.ok = true;
   return p;
@@ -402,11 +430,25 @@ int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const d
     set_error("bs_cox_grad_xbeta: cudaMemsetAsync failed");
     return BS_ECUDA;
   }
-  F2Args a{X, m, n_loc, p.R, p.cpg, p.S, p.Gc, v, grad, beta, sigma, lam, xb_parts, l1_parts, partials, counters, flags};
-  smem_attr(cox_fused2_kernel, int(p.smem));
+  static const int pf = [] {
+    const char* c = getenv("BS_F2_PF");
+    return c ? atoi(c) : 0;
+  }();
+  F2Args a{X, m, n_loc, p.R, p.cpg, p.S, p.Gc, pf, v, grad, beta, sigma, lam, xb_parts, l1_parts, partials, counters, flags};
+  const void* k = nullptr;
+  switch (p.cfg) {
+    case 1: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 1, 2>); smem_attr(cox_fused2_kernel<3, 1, 2>, int(p.smem)); break;
+    case 2: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 3>); smem_attr(cox_fused2_kernel<2, 2, 3>, int(p.smem)); break;
+    case 3: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 1, 3>); smem_attr(cox_fused2_kernel<3, 1, 3>, int(p.smem)); break;
+    case 4: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 4>); smem_attr(cox_fused2_kernel<2, 2, 4>, int(p.smem)); break;
+    case 5: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 2, 3>); smem_attr(cox_fused2_kernel<3, 2, 3>, int(p.smem)); break;
+    case 6: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 2, 2>); smem_attr(cox_fused2_kernel<3, 2, 2>, int(p.smem)); break;
+    case 7: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 3, 2>); smem_attr(cox_fused2_kernel<2, 3, 2>, int(p.smem)); break;
+    case 8: k = reinterpret_cast<const void*>(cox_fused2_kernel<4, 2, 2>); smem_attr(cox_fused2_kernel<4, 2, 2>, int(p.smem)); break;
+    default: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 2>); smem_attr(cox_fused2_kernel<2, 2, 2>, int(p.smem)); break;
+  }
   void* args[] = {&a};
-  cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(cox_fused2_kernel), dim3(p.S * p.Gc),
-                                              dim3(F2_THREADS), args, p.smem, st);
+  cudaError_t e = cudaLaunchCooperativeKernel(k, dim3(p.S * p.Gc), dim3(F2_THREADS), args, p.smem, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("bs_cox_grad_xbeta: cooperative launch failed: %s", cudaGetErrorString(e));

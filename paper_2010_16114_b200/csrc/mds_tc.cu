@@ -295,7 +295,12 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const uint32_t c = cbase + uint32_t(t1);
           const int s = int(c % NB1);
           const uint32_t b = c & 1;
-          if (mbar_test(b1_full(s), (c / NB1) & 1) && mbar_test(d1_empty(b), ((c >> 1) & 1) ^ 1)) {
+          // lanes could see a phase complete at different instants: decide on lane 0 only,
+          // or part of the warp would issue the MMA now and the rest again later
+          const bool go = __shfl_sync(0xffffffffu,
+                                      int(mbar_test(b1_full(s), (c / NB1) & 1) && mbar_test(d1_empty(b), ((c >> 1) & 1) ^ 1)),
+                                      0) != 0;
+          if (go) {
             tc_fence_after();
             const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D1 + b * CHI, 0);
             const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A1, 0);
@@ -319,8 +324,12 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const int s = int(c % NB2);
           const bool first = (t2 % a.G) == 0;
           const bool last = ((t2 % a.G) == a.G - 1) || (t2 == nch - 1);
-          if (mbar_test(a2_full(b), (c >> 1) & 1) && (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
-              mbar_test(b2_full(s), (c / NB2) & 1)) {
+          const bool go = __shfl_sync(0xffffffffu,
+                                      int(mbar_test(a2_full(b), (c >> 1) & 1) &&
+                                          (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
+                                          mbar_test(b2_full(s), (c / NB2) & 1)),
+                                      0) != 0;
+          if (go) {
             tc_fence_after();
             const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D2, 0);
             const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A2 + b * 128, 0);

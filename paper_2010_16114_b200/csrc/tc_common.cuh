@@ -54,7 +54,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 
-// Non-blocking probe of phase `parity` (warp-uniform when every lane tests the same barrier).
+// Non-blocking probe of phase `parity`.  NOT warp-uniform: lanes may observe the phase
+// flip at different instants, so a warp that branches on it must broadcast one lane's result.
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   uint32_t done;
   asm volatile(

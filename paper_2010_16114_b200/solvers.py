@@ -701,10 +701,13 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
     pp, pn = s._work.args("pd", _lib.query("bs_cox_pi_delta_workspace", m))
     gp, gn = s._work.args("grad", _lib.query("bs_cox_grad_workspace", xcode, m, n_loc))
     comm = x.comm
-    # The fused pass (one X stream per iteration) is opt-in until it beats the two-pass
-    # path (see cox.cu); it spins on grid-wide counters, so never with other ranks'
-    # kernels sharing this GPU.
-    fuse = int(os.environ.get("BS_COX_FUSION") == "1" and dev.type == "cuda"
+    # The fused pass (one X stream per iteration, bs_cox_grad_xbeta) is the default for
+    # float32 X with float32 arithmetic, where its 2-D grid kernel (cox_fused2.cu) beats
+    # the two passes; BS_COX_FUSION=1 forces it for every dtype, =0 disables it.  It spins
+    # on per-group counters, so never with other ranks' kernels sharing this GPU.
+    mode = os.environ.get("BS_COX_FUSION", "auto")
+    want = mode == "1" or (mode == "auto" and xcode == _lib.BS_F32 and code == _lib.BS_F32)
+    fuse = int(want and dev.type == "cuda"
                and (comm.backend != "inproc" or comm.size <= torch.cuda.device_count()))
     if fuse:
         fp, fn_ = s._work.args("grad_xbeta", _lib.query("bs_cox_grad_xbeta_workspace", xcode, m, n_loc))
