@@ -253,7 +253,8 @@ def _setup(comm, wl):
             y = np.arange(m, 0, -1, dtype=np.float64)          # cli.py:194
             delta = (np.random.Generator(np.random.Philox(2013)).random(m) > 0.3).astype(np.float64)  # cli.py:195
             st = bs.cox_init(x, y, delta, lam=wl["lam"], sigma=1e-7, dtype=sdt)
-        return st, (lambda k: bs.cox_fit(st, k, trace_every=1)), ["bs_cox_xbeta", "bs_cox_grad_step"], x
+        return st, (lambda k: bs.cox_fit(st, k, trace_every=1)), ["bs_cox_grad_xbeta", "bs_cox_xbeta",
+                                                                  "bs_cox_grad_step"], x
     if kind == "mds":
         dt = np.dtype(wl["dtype"])
         pts = bs.empty((wl["d"], wl["n"]), comm, dt)

@@ -604,6 +604,7 @@ def _xbeta(s, beta_local):
     n_loc = x.local.shape[1]
     xb = s._dev["xb"]
     st = _lib.stream_ptr()
+    s._dev.pop("xb_beta", None)  # xb no longer holds a fused pass's partial
     local_reduce(beta_local, ReduceOp.SUM, _lib.BS_T_ABS, out=xb[m:m + 1])
     wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", _lib.xcode(x), m, n_loc))
     _lib.call("bs_cox_xbeta", _lib.ptr(_flat_local(x)), _lib.xcode(x), _lib.ptr(beta_local),
@@ -713,12 +714,19 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
         fp, fn_ = s._work.args("grad_xbeta", _lib.query("bs_cox_grad_xbeta_workspace", xcode, m, n_loc))
     host_trace = []
     ran = iters
-    if fuse:
+    # A previous call's last fused pass left xb = (local X beta, ||beta||_1) for the beta it
+    # produced; reuse it when beta is untouched since (same storage, and torch's in-place
+    # version counter unchanged: any torch write to st.beta.local bumps it).  Saves a pass
+    # over X per call.
+    snap = s._dev.pop("xb_beta", None)
+    reuse = bool(fuse and snap is not None and os.environ.get("BS_COX_REUSE", "1") != "0"
+                 and snap == (s.beta.local.data_ptr(), s.beta.local._version))
+    if fuse and not reuse:
         _xbeta(s, beta)                                         # the fused pass supplies the later ones
     for it in range(iters):
         if not fuse:
             _xbeta(s, beta)                                     # scn m + ||beta||_1 (solvers.py:436)
-        elif it > 0 and comm.size > 1:
+        elif (it > 0 or reuse) and comm.size > 1:
             comm.allreduce(xb, ReduceOp.SUM)                    # X beta partials of the fused pass
         _risk(s)                                                # solvers.py:437
         fhist[it:it + 1].copy_(flags)
@@ -744,6 +752,8 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
                       _lib.ptr(beta), sigma, lam, 1, _at(xb, m), _lib.ptr(flags), gp, gn, st)
     fl_all = fhist[:max(ran, 1)].cpu().numpy() if ran else np.zeros(0, dtype=np.int32)
     bad = np.nonzero(fl_all & _lib.BS_FLAG_NONFINITE)[0] if fl_all.size else []
+    if fuse and ran == iters and not len(bad) and not (int(flags.item()) & _lib.BS_FLAG_NONFINITE):
+        s._dev["xb_beta"] = (s.beta.local.data_ptr(), s.beta.local._version)  # xb: last fused pass's partial
     stop = int(bad[0]) if len(bad) else ran
     if monitor is not None:
         s.trace.extend(host_trace[:len([it for it in range(stop) if trace_every and it % trace_every == 0])])

@@ -316,3 +316,41 @@ def test_cox_int8_genotypes_float32_arithmetic():
         tr32, b32 = bs.run_inproc(p, fn, g.astype(np.float32))[0]
         np.testing.assert_allclose(tr8, tr32, rtol=2e-5)
         assert np.abs(b8 - b32).max() <= 1e-4 * max(np.abs(b32).max(), 1e-30)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cox_fit_split_calls_match_one_call(p):
+    """float32 fits run the fused one-stream pass; a fit split over several calls reuses the
+    last pass's X beta (no extra pass) and must equal one long call, including after beta is
+    changed between calls (the reuse is then skipped)."""
+    gen = np.random.Generator(np.random.Philox(41))
+    m, n = 8000, 900
+    x = gen.standard_normal((m, n)).astype(np.float32)
+    delta = (gen.random(m) < 0.5).astype(np.float64)
+    y = np.arange(m, 0, -1, dtype=np.float64)
+
+    def fn(comm, splits, poke):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.02, sigma=2e-5)
+        for k in splits:
+            bs.cox_fit(st, k)
+            if poke:
+                st.beta.local.mul_(1.0)  # same values: reuse stays valid
+        return np.asarray(st.trace), bs.gather_full(st.beta)
+
+    one = bs.run_inproc(p, fn, [12], False)[0]
+    split = bs.run_inproc(p, fn, [5, 4, 3], False)[0]
+    poked = bs.run_inproc(p, fn, [5, 7], True)[0]
+    for got in (split, poked):
+        np.testing.assert_allclose(got[0], one[0], rtol=1e-6)
+        np.testing.assert_allclose(got[1], one[1], rtol=1e-5, atol=1e-7)
+
+    def changed(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.02, sigma=2e-5)
+        bs.cox_fit(st, 3)
+        st.beta.local.zero_()  # restart from zero: the cached X beta must not be used
+        bs.cox_fit(st, 4)
+        return np.asarray(st.trace)
+
+    tr = bs.run_inproc(p, changed)[0]
+    fresh = bs.run_inproc(p, fn, [4], False)[0][0]
+    np.testing.assert_allclose(tr[3:], fresh, rtol=1e-6)
