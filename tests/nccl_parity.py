@@ -65,6 +65,33 @@ def main():
     ok &= check("cox trace", st.trace, otr, 1e-10)
     ok &= check("cox beta", bs.gather_full(st.beta), ob, 1e-8)
     ok &= check("cox sigma (power iteration)", bs.opnorm(xd), orc.opnorm_l2_power(xs), 1e-12)
+    # Cox float32 (the fused one-stream pass, cox_fused2.cu), split over two calls so the
+    # second reuses the last pass's X beta partial (allreduced at the start of the call)
+    gen = np.random.Generator(np.random.Philox(12))
+    xf = gen.standard_normal((8000, 1203)).astype(np.float32)
+    df = (gen.random(8000) < 0.5).astype(np.float64)
+    yf = np.arange(8000, 0, -1, dtype=np.float64)
+    sgf = 2e-5
+    xfd = bs.distribute(xf if comm.rank == 0 else None, comm)
+    st = bs.cox_init(xfd, yf, df, lam=1e-4, sigma=sgf)
+    bs.cox_fit(st, 6)
+    bs.cox_fit(st, 6)
+    ob, og, otr = orc.cox_fit(xf.astype(np.float64), df, np.arange(8000), 1e-4, sgf, 12)
+    ok &= check("cox float32 fused: nonzero coefficients", [min(np.count_nonzero(ob), 1)], [1], 0)
+    ok &= check("cox float32 fused trace", st.trace, otr, 2e-5)
+    ok &= check("cox float32 fused beta", bs.gather_full(st.beta), ob, 2e-4)
+    # packed genotypes (2-bit) against int8 storage of the same matrix
+    gp = bs.genotype_fill(bs.PackedGenotypes(comm, (6000, 777)), 31)
+    g8 = bs.genotype_fill(bs.empty((6000, 777), comm, np.int8), 31)
+    yg = np.floor(np.arange(6000, 0, -1) / 4.0)
+    dg = (np.random.Generator(np.random.Philox(3)).random(6000) < 0.3).astype(np.float64)
+    tr = []
+    for a in (gp, g8):
+        st = bs.cox_init(a, yg, dg, lam=1e-6, sigma=2e-7, ties="breslow", dtype=np.float32)
+        bs.cox_fit(st, 8)
+        tr.append(np.asarray(st.trace))
+        ok &= check("cox packed/int8: nonzero coefficients", [min(np.count_nonzero(bs.gather_full(st.beta)), 1)], [1], 0)
+    ok &= check("cox packed genotypes vs int8 trace", tr[0], tr[1], 2e-5)
     comm.barrier()
     import torch.distributed as dist
 

@@ -330,7 +330,7 @@ def test_cox_fit_split_calls_match_one_call(p):
     y = np.arange(m, 0, -1, dtype=np.float64)
 
     def fn(comm, splits, poke):
-        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.02, sigma=2e-5)
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=2e-5)
         for k in splits:
             bs.cox_fit(st, k)
             if poke:
@@ -340,12 +340,13 @@ def test_cox_fit_split_calls_match_one_call(p):
     one = bs.run_inproc(p, fn, [12], False)[0]
     split = bs.run_inproc(p, fn, [5, 4, 3], False)[0]
     poked = bs.run_inproc(p, fn, [5, 7], True)[0]
+    assert 0 < np.count_nonzero(one[1]) < n
     for got in (split, poked):
         np.testing.assert_allclose(got[0], one[0], rtol=1e-6)
         np.testing.assert_allclose(got[1], one[1], rtol=1e-5, atol=1e-7)
 
     def changed(comm):
-        st = bs.cox_init(_dist(comm, x), y, delta, lam=0.02, sigma=2e-5)
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=2e-5)
         bs.cox_fit(st, 3)
         st.beta.local.zero_()  # restart from zero: the cached X beta must not be used
         bs.cox_fit(st, 4)

@@ -122,7 +122,7 @@ def test_cox_fit_packed_matches_int8_and_oracle(p):
     x = orc.genotype_fill(m, n, seed)
     y = np.floor(np.arange(m, 0, -1) / 4.0)
     delta = (np.random.Generator(np.random.Philox(2)).random(m) < 0.6).astype(np.float64)
-    lam = 0.05
+    lam = 1e-6
 
     def fn(comm, packed):
         if packed:
@@ -137,6 +137,7 @@ def test_cox_fit_packed_matches_int8_and_oracle(p):
     packed_runs = bs.run_inproc(p, lambda c: fn(c, True))
     (t8, b8, s8), (tp, bp, sp) = int8_runs[0], packed_runs[0]
     np.testing.assert_allclose(sp, s8, rtol=1e-10)  # opnorm through the packed kernels
+    assert 0 < np.count_nonzero(b8) < n  # the step moved and the threshold zeroed some
     np.testing.assert_allclose(tp, t8, rtol=2e-5)
     np.testing.assert_allclose(bp, b8, rtol=2e-3, atol=2e-5 * np.abs(b8).max())
     _, _, otr = orc.cox_fit(x.astype(np.float64), delta, orc.tie_cuts(y), lam, sp, iters)
