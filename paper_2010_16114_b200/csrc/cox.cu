@@ -1285,8 +1285,12 @@ extern "C" int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, 
     const F2Plan q = f2_plan(m, n_loc);
     if (q.ok) {
       Workspace ws(work, work_bytes);
-      return f2_launch(q, static_cast<const float*>(X), m, n_loc, dmpd, static_cast<float*>(grad),
-                       static_cast<float*>(beta), sigma, lam, xb_out, flags, ws, st);
+      const int rc = f2_launch(q, static_cast<const float*>(X), m, n_loc, dmpd, static_cast<float*>(grad),
+                               static_cast<float*>(beta), sigma, lam, xb_out, flags, ws, st);
+      if (rc != -1000) return rc;  // F2_REFUSED
+      // the cooperative launch was refused (e.g. SMs taken by another context): two passes
+      return bs_cox_grad_xbeta(X, xdtype, dmpd, dtype, m, n_loc, grad, beta, sigma, lam, xb_out, flags, 0, work,
+                               work_bytes, stream);
     }
   }
   const FuPlan p = fu_plan(xdtype, m, n_loc);

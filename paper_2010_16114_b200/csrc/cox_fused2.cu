@@ -363,6 +363,8 @@ __global__ void cox_fused2_finish(const double* __restrict__ xb_parts, const dou
 
 namespace bs {
 
+constexpr int F2_REFUSED = -1000;  // internal: cooperative launch refused
+
 struct F2Plan {
   bool ok;
   int S, Gc, cfg;
@@ -452,7 +454,7 @@ int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const d
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("bs_cox_grad_xbeta: cooperative launch failed: %s", cudaGetErrorString(e));
-    return BS_ECUDA;
+    return F2_REFUSED;  // the caller falls back to two passes
   }
   cox_fused2_finish<<<int(std::min<int64_t>(ceil_div(m + 1, 256), 1024)), 256, 0, st>>>(xb_parts, l1_parts, p.Gc, m,
                                                                                          xb_out);
