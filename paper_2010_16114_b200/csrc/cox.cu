@@ -139,6 +139,10 @@ int launch_xbeta_u2(const void* P, const void* beta, bool f64, int64_t m, int64_
                     int64_t cps, double* parts, int* splits_used, cudaStream_t st);
 int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t n_loc, int groups, int segs,
                    int64_t cpg, double* parts, const int* flags, cudaStream_t st);
+bool launch_xbeta_i8_ring(const int8_t* X, const float* beta, int64_t m, int64_t n_loc, int64_t splits,
+                          double* parts, int* splits_used, cudaStream_t st);
+bool launch_grad_i8_ring(const int8_t* X, const double* v, int64_t m, int64_t n_loc, int segs, double* parts,
+                         const int* flags, cudaStream_t st);
 }  // namespace bs
 
 struct XbGrid {
@@ -279,6 +283,17 @@ extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dty
     else if (parts != out)
       cudaMemcpyAsync(out, parts, sizeof(double) * m, cudaMemcpyDeviceToDevice, st);
     return check_launch("bs_cox_xbeta", used > 1 ? 2 : 1);
+  }
+  if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic: TMA ring
+    int used = 1;
+    if (launch_xbeta_i8_ring(static_cast<const int8_t*>(X), static_cast<const float*>(beta), m, n_loc, g.splits, parts,
+                             &used, st)) {
+      if (used > 1)
+        sum_slabs_f64<<<int(std::min<int64_t>(ceil_div(m, 256), 2048)), 256, 0, st>>>(parts, used, m, out);
+      else if (parts != out)
+        cudaMemcpyAsync(out, parts, sizeof(double) * m, cudaMemcpyDeviceToDevice, st);
+      return check_launch("bs_cox_xbeta", used > 1 ? 2 : 1);
+    }
   }
 #define BS_XB(TXT, TBT) launch_xbeta<TXT, TBT>(static_cast<const TXT*>(X), static_cast<const TBT*>(beta), m, n_loc, g, parts, st)
   if (dtype == BS_F64) {
@@ -777,7 +792,9 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
       launch_grad_u2(X, dtype == BS_F64, dmpd, m, n_loc, g.groups, g.segs, g.cpg, parts, flags, st);
     } else if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
-    else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic
+    else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok &&
+             launch_grad_i8_ring(static_cast<const int8_t*>(X), dmpd, m, n_loc, g.segs, parts, flags, st)) {
+    } else if (xdtype == BS_I8 && dtype == BS_F32 && vec_ok) {  // genotypes, float32 arithmetic
       dim3 grid(unsigned(g.groups), unsigned(g.segs));
       grad_i8f_kernel<<<grid, GR_THREADS, 0, st>>>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g.cpg, parts, flags);
     } else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);

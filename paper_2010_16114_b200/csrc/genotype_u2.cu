@@ -562,6 +562,194 @@ xbeta_u2_ring_kernel(const uint32_t* __restrict__ P, const float* __restrict__ b
     if (wi * 16 + q < m) out[wi * 16 + q] = accd[q];
 }
 
+// ---------------------------------------------------------------------------
+// int8 X with float32 arithmetic through the same TMA ring (cox.cu's register kernels
+// xbeta_i8f / grad_i8f keep too little in flight: 4.0 / 5.4 TB/s).  Widening as there:
+// one PRMT puts byte ^ 0x80 under the exponent of 2^23, a packed FADD removes 2^23 + 128
+// (exact for every int8), a packed FMA accumulates.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ u2_f2 i8r_pair(uint32_t ww, int k) {  // bytes k, k+1 of ww (already ^ 0x80808080)
+  const float a = __uint_as_float(__byte_perm(ww, 0x4B000000u, 0x7440u + k));
+  const float b = __uint_as_float(__byte_perm(ww, 0x4B000000u, 0x7440u + k + 1));
+  return u2_add2(u2_pack(a, b), u2_pack(-8388736.0f, -8388736.0f));
+}
+
+// scn p: as grad_u2_ring_kernel; lane owns 32 consecutive rows (two 16-byte words per column)
+__global__ void __launch_bounds__(UR_THREADS, 2)
+grad_i8_ring_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, int64_t m, int64_t n_loc,
+                    int64_t cols_per_group, double* __restrict__ parts, const int* flags) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int CF = 2;  // columns per stage, 8 KB each
+  const uint32_t ring = smem_u32(smem);
+  const uint32_t full = ring + UR_STAGES * UR_STAGE_BYTES, empty = full + 8 * UR_STAGES;
+  float(*red)[32] = reinterpret_cast<float(*)[32]>(smem + UR_STAGES * UR_STAGE_BYTES + 16 * UR_STAGES);
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = int64_t(blockIdx.y) * U2_SEG;
+  const int64_t c0 = int64_t(blockIdx.x) * cols_per_group;
+  const int64_t c1 = min(n_loc, c0 + cols_per_group);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < UR_STAGES; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0)
+      ur_produce<CF>(reinterpret_cast<const uint8_t*>(X), m, r0, uint32_t(m - r0 < U2_SEG ? m - r0 : U2_SEG), c0, c1,
+                     ring, full, empty);
+    return;
+  }
+  const int wid = warp - 1;
+  // lane owns the 16-row words at 16 lane and 512 + 16 lane of the warp's 1024 rows
+  // (consecutive lanes, consecutive 16-byte words: conflict-free LDS.128)
+  float vs[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const int64_t r = r0 + int64_t(wid) * 1024 + 512 * (k >> 4) + 16 * lane + (k & 15);
+    vs[k] = r < m ? float(v[r]) : 0.f;
+  }
+  const uint32_t my = ring + uint32_t(wid * 1024 + lane * 16);
+  int k = 0;
+  for (int64_t cb = c0; cb < c1; cb += 32) {
+    float cs[32];
+#pragma unroll
+    for (int b = 0; b < 32 / CF; ++b) {
+      if (cb + CF * b < c1) {
+        const int s = k % UR_STAGES;
+        mbar_wait(full + 8 * s, uint32_t((k / UR_STAGES) & 1));
+        uint4 w[CF][2];
+#pragma unroll
+        for (int u = 0; u < CF; ++u)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) w[u][h] = ld_shared_v4(my + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF) + 512 * h);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
+        ++k;
+#pragma unroll
+        for (int u = 0; u < CF; ++u) {
+          u2_f2 acc = u2_pack(0.f, 0.f);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t q4[4] = {w[u][h].x ^ 0x80808080u, w[u][h].y ^ 0x80808080u, w[u][h].z ^ 0x80808080u,
+                                    w[u][h].w ^ 0x80808080u};
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+              acc = u2_fma2(i8r_pair(q4[a], 0), u2_pack(vs[16 * h + 4 * a], vs[16 * h + 4 * a + 1]), acc);
+              acc = u2_fma2(i8r_pair(q4[a], 2), u2_pack(vs[16 * h + 4 * a + 2], vs[16 * h + 4 * a + 3]), acc);
+            }
+          }
+          float s0, s1;
+          u2_unpack(acc, s0, s1);
+          cs[CF * b + u] = s0 + s1;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < CF; ++u) cs[CF * b + u] = 0.f;
+      }
+    }
+    red[wid][lane] = transpose_reduce32(cs, lane);
+    ur_consumer_sync();
+    const int nb = int(c1 - cb < 32 ? c1 - cb : 32);
+    const int t = threadIdx.x - 32;
+    if (t < nb) {
+      double acc = 0.0;
+      for (int w2 = 0; w2 < 8; ++w2) acc += double(red[w2][t]);
+      parts[int64_t(blockIdx.y) * n_loc + cb + t] = acc;
+    }
+    ur_consumer_sync();
+  }
+}
+
+// scn m: the CTA owns 4096 rows (one 16-byte word of 16 rows per consumer thread), stages of
+// 4 columns x 4 KB
+__global__ void __launch_bounds__(UR_THREADS, 2)
+xbeta_i8_ring_kernel(const int8_t* __restrict__ X, const float* __restrict__ beta, int64_t m, int64_t n_loc,
+                     int64_t cols_per_split, double* __restrict__ parts) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int CF = 4;
+  const uint32_t ring = smem_u32(smem);
+  const uint32_t full = ring + UR_STAGES * UR_STAGE_BYTES, empty = full + 8 * UR_STAGES;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t j_begin = int64_t(blockIdx.y) * cols_per_split;
+  const int64_t j_end = min(n_loc, j_begin + cols_per_split);
+  const int64_t off = int64_t(blockIdx.x) * 4096;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < UR_STAGES; ++s) {
+      mbar_init(full + 8 * s, 1);
+      mbar_init(empty + 8 * s, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0)
+      ur_produce<CF>(reinterpret_cast<const uint8_t*>(X), m, off, uint32_t(m - off < 4096 ? m - off : 4096), j_begin,
+                     j_end, ring, full, empty);
+    return;
+  }
+  const int t = threadIdx.x - 32;
+  const int64_t i0 = off + 16 * int64_t(t);
+  double accd[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) accd[q] = 0.0;
+  int k = 0;
+  for (int64_t jb = j_begin; jb < j_end; jb += 32) {
+    u2_f2 acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = u2_pack(0.f, 0.f);
+#pragma unroll
+    for (int b = 0; b < 32 / CF; ++b) {
+      const int64_t j = jb + CF * b;
+      if (j < j_end) {
+        const int s = k % UR_STAGES;
+        mbar_wait(full + 8 * s, uint32_t((k / UR_STAGES) & 1));
+        uint4 w[CF];
+#pragma unroll
+        for (int u = 0; u < CF; ++u) w[u] = ld_shared_v4(ring + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF) + 16 * t);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
+        ++k;
+        const int nc = int(j_end - j < CF ? j_end - j : CF);
+#pragma unroll
+        for (int u = 0; u < CF; ++u) {
+          const float bj = u < nc ? __ldg(beta + j + u) : 0.f;
+          const u2_f2 bb = u2_pack(bj, bj);
+          const uint32_t q4[4] = {w[u].x ^ 0x80808080u, w[u].y ^ 0x80808080u, w[u].z ^ 0x80808080u,
+                                  w[u].w ^ 0x80808080u};
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            acc[2 * a] = u2_fma2(i8r_pair(q4[a], 0), bb, acc[2 * a]);
+            acc[2 * a + 1] = u2_fma2(i8r_pair(q4[a], 2), bb, acc[2 * a + 1]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q2 = 0; q2 < 8; ++q2) {
+      float lo, hi;
+      u2_unpack(acc[q2], lo, hi);
+      accd[2 * q2] += double(lo);
+      accd[2 * q2 + 1] += double(hi);
+    }
+  }
+  if (i0 >= m) return;
+  double* out = parts + int64_t(blockIdx.y) * m;
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    if (i0 + q < m) out[i0 + q] = accd[q];
+}
+
+static bool i8_ring() {
+  static const bool on = [] {
+    const char* e = getenv("BS_I8_RING");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static bool u2_den() {
   static const bool on = [] {
     const char* e = getenv("BS_U2_SUBNORMAL");
@@ -705,6 +893,36 @@ int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t 
   else
     grad_u2_kernel<<<grid, U2_THREADS, 0, st>>>(static_cast<const uint32_t*>(P), v, m, n_loc, cpg, parts, flags);
   return BS_OK;
+}
+
+// int8 X, float32 arithmetic, m % 16 == 0 and X 16-byte aligned: ring kernels; returns
+// false (nothing launched) when disabled (BS_I8_RING=0) so the caller uses cox.cu's kernels.
+bool launch_xbeta_i8_ring(const int8_t* X, const float* beta, int64_t m, int64_t n_loc, int64_t splits,
+                          double* parts, int* splits_used, cudaStream_t st) {
+  if (!i8_ring()) return false;
+  const int64_t tiles = ceil_div(m, int64_t(4096));
+  int64_t sp = std::max<int64_t>(1, (2 * int64_t(num_sms())) / tiles);
+  sp = std::min<int64_t>({sp, splits, std::max<int64_t>(1, n_loc / 64)});
+  const int64_t c = ceil_div(std::max<int64_t>(n_loc, 1), sp);
+  sp = ceil_div(std::max<int64_t>(n_loc, 1), c);
+  *splits_used = int(sp);
+  smem_attr(xbeta_i8_ring_kernel, UR_SMEM);
+  const dim3 grid{unsigned(tiles), unsigned(sp)};
+  xbeta_i8_ring_kernel<<<grid, UR_THREADS, UR_SMEM, st>>>(X, beta, m, n_loc, c, parts);
+  return true;
+}
+
+bool launch_grad_i8_ring(const int8_t* X, const double* v, int64_t m, int64_t n_loc, int segs, double* parts,
+                         const int* flags, cudaStream_t st) {
+  if (!i8_ring()) return false;
+  int64_t gr = std::max<int64_t>(1, (2 * int64_t(num_sms())) / segs);
+  gr = std::min<int64_t>(gr, std::max<int64_t>(1, ceil_div(n_loc, 8)));
+  const int64_t c = ceil_div(std::max<int64_t>(n_loc, 1), gr);
+  gr = ceil_div(std::max<int64_t>(n_loc, 1), c);
+  smem_attr(grad_i8_ring_kernel, UR_SMEM);
+  const dim3 grid{unsigned(gr), unsigned(segs)};
+  grad_i8_ring_kernel<<<grid, UR_THREADS, UR_SMEM, st>>>(X, v, m, n_loc, c, parts, flags);
+  return true;
 }
 
 }  // namespace bs
