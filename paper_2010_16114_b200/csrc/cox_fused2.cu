@@ -160,7 +160,21 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
     if (lane == 0) {
       uint64_t drop;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
+      // B stages do not depend on the partials: the first F2_BS stages of wave u are issued
+      // before waiting for the group's counter, so they land while the fold is pending
+      auto bstage = [&](int u, int q) {
+        const int k = u * F2_QPW + q, s = k % F2_BS;
+        mbar_wait_sleep(bar(BE + s), uint32_t((k / F2_BS) & 1) ^ 1u);
+        const int64_t j0 = c0 + int64_t(u) * F2_W + q * F2_CW;
+        const int nc = int(c1 - j0 <= 0 ? 0 : (c1 - j0 < F2_CW ? c1 - j0 : F2_CW));
+        mbar_expect_tx(bar(BF + s), bytes_col * uint32_t(nc));
+        for (int jj = 0; jj < nc; ++jj)
+          bulk(smem_u32(bring + s * stage_f + jj * R), a.X + (j0 + jj) * m + r0, bytes_col, bar(BF + s), drop);
+      };
+      constexpr int EARLY = F2_BS < F2_QPW ? F2_BS : F2_QPW;
       for (int u = 0; u < nw; ++u) {
+        if (rows > 0)
+          for (int q = 0; q < EARLY; ++q) bstage(u, q);
         const int slot = u % F2_RING;
         const unsigned int* ctr = a.counters + g * F2_RING + slot;
         const unsigned int target = unsigned(S) * unsigned(u / F2_RING + 1);
@@ -182,15 +196,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
         bulk(smem_u32(pbuf + pb * S * F2_W), a.partials + (int64_t(g) * F2_RING + slot) * S * F2_W, pbytes, bar(PF + pb),
              drop);
         if (rows > 0)
-          for (int q = 0; q < F2_QPW; ++q) {
-            const int k = u * F2_QPW + q, s = k % F2_BS;
-            mbar_wait_sleep(bar(BE + s), uint32_t((k / F2_BS) & 1) ^ 1u);
-            const int64_t j0 = c0 + int64_t(u) * F2_W + q * F2_CW;
-            const int nc = int(c1 - j0 <= 0 ? 0 : (c1 - j0 < F2_CW ? c1 - j0 : F2_CW));
-            mbar_expect_tx(bar(BF + s), bytes_col * uint32_t(nc));
-            for (int jj = 0; jj < nc; ++jj)
-              bulk(smem_u32(bring + s * stage_f + jj * R), a.X + (j0 + jj) * m + r0, bytes_col, bar(BF + s), drop);
-          }
+          for (int q = EARLY; q < F2_QPW; ++q) bstage(u, q);
       }
     }
     return;
