@@ -47,6 +47,7 @@ def test_pack_unpack_match_oracle(m, n):
         p = bs.pack_genotypes(a)
         assert p.local.shape == (want.shape[0], p.hi - p.lo)
         np.testing.assert_array_equal(_device_block(p), want[:, p.lo:p.hi])
+        assert np.array_equal(bs.gather_full(p), bs.gather_full(bs.unpack_genotypes(p)))
         return bs.gather_full(bs.unpack_genotypes(p))
 
     for p in (1, 3):
