@@ -355,3 +355,22 @@ def test_cox_fit_split_calls_match_one_call(p):
     tr = bs.run_inproc(p, changed)[0]
     fresh = bs.run_inproc(p, fn, [4], False)[0][0]
     np.testing.assert_allclose(tr[3:], fresh, rtol=1e-6)
+
+
+@pytest.mark.parametrize("m,n", [(8002, 300), (8000, 40)])
+def test_cox_float32_shapes_outside_the_fused_plan(m, n):
+    """m % 4 != 0 or fewer than 64 local columns: bs_cox_grad_xbeta takes the two-pass path;
+    cox_fit results are unchanged against the oracle."""
+    gen = np.random.Generator(np.random.Philox(m + n))
+    x = gen.standard_normal((m, n)).astype(np.float32)
+    delta = (gen.random(m) < 0.5).astype(np.float64)
+    y = np.arange(m, 0, -1, dtype=np.float64)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=2e-5)
+        bs.cox_fit(st, 6)
+        return np.asarray(st.trace)
+
+    tr = bs.run_inproc(1, fn)[0]
+    _, _, otr = orc.cox_fit(x.astype(np.float64), delta, np.arange(m), 1e-4, 2e-5, 6)
+    np.testing.assert_allclose(tr, otr, rtol=2e-5)

@@ -189,3 +189,24 @@ def test_packed_xbeta_any_beta_scale(scale):
         assert np.max(np.abs(xbp - want) / sc) < 2e-5
     else:  # |beta| below 2^-104: subnormal products, absolute error <= 2^-127 per product
         assert np.max(np.abs(xbp - want)) < n * 2.0 ** -127
+
+
+@pytest.mark.gpu
+def test_packed_more_ranks_than_columns():
+    """Ranks that own no columns (partition_of gives them empty blocks) still join every
+    collective; the fit equals the one-rank fit."""
+    m, n, seed = 2000, 3, 5
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(8)).random(m) < 0.5).astype(np.float64)
+
+    def fn(comm):
+        a = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        st = bs.cox_init(a, y, delta, lam=1e-6, sigma=1e-5, ties="breslow", dtype=np.float32)
+        bs.cox_fit(st, 5)
+        return np.asarray(st.trace), bs.gather_full(st.beta), bs.gather_full(a)
+
+    one = bs.run_inproc(1, fn)[0]
+    for got in bs.run_inproc(5, fn):
+        np.testing.assert_allclose(got[0], one[0], rtol=1e-6)
+        np.testing.assert_allclose(got[1], one[1], rtol=1e-5, atol=1e-9)
+        np.testing.assert_array_equal(got[2], orc.genotype_fill(m, n, seed))
