@@ -314,7 +314,7 @@ grad_u2_kernel(const uint32_t* __restrict__ P, const double* __restrict__ v, int
 constexpr int UR_THREADS = 288;  // warp 0 producer, warps 1..8 consumers
 constexpr int UR_STAGES = 4;
 constexpr int UR_STAGE_BYTES = 16384;
-constexpr int UR_SMEM = UR_STAGES * UR_STAGE_BYTES + 2 * UR_STAGES * 8 + 8 * 32 * 4 + 64;
+constexpr int UR_SMEM = UR_STAGES * UR_STAGE_BYTES + 2 * UR_STAGES * 8 + 2 * 8 * 32 * 4 + 64;
 
 __device__ __forceinline__ void ur_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar, uint64_t pol) {
   asm volatile(
@@ -431,16 +431,18 @@ grad_u2_ring_kernel(const uint32_t* __restrict__ P, const double* __restrict__ v
         for (int u = 0; u < CF; ++u) cs[CF * b + u] = 0.f;
       }
     }
-    red[wid][lane] = transpose_reduce32(cs, lane);
+    // red is double-buffered by 32-column block: the next block's writes go to the other
+    // half, and the one after that follows this block's barrier, so one barrier suffices
+    float(*rb)[32] = red + ((cb - c0) / 32 & 1) * 8;
+    rb[wid][lane] = transpose_reduce32(cs, lane);
     ur_consumer_sync();
     const int nb = int(c1 - cb < 32 ? c1 - cb : 32);
     const int t = threadIdx.x - 32;
     if (t < nb) {
       double acc = 0.0;
-      for (int w2 = 0; w2 < 8; ++w2) acc += double(red[w2][t]);
+      for (int w2 = 0; w2 < 8; ++w2) acc += double(rb[w2][t]);
       parts[int64_t(blockIdx.y) * n_loc + cb + t] = acc;
     }
-    ur_consumer_sync();
   }
 }
 
