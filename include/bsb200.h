@@ -226,7 +226,10 @@ int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dtype,
  *   Xbeta = xb, w = exp(min(xb, clamp)), W = cumsum(w) (forward),
  *   loglik_dev[0] = sum delta (xb - log W[cuts]).
  * Sets BS_FLAG_CLAMPED / BS_FLAG_NONFINITE in *flags.  Outputs in `dtype`.
- * A set BS_FLAG_NONFINITE on entry makes the call a no-op. */
+ * A set BS_FLAG_NONFINITE on entry makes the call a no-op.  With a zeroed
+ * workspace of bs_cox_risk_workspace(m) bytes (nonzero for long m) the scans run
+ * on many CTAs with results bitwise equal to the single-CTA scan; without one
+ * (NULL, 0) the single-CTA kernel runs. */
 int64_t bs_cox_risk_workspace(int64_t m);
 int bs_cox_risk(const double* xb, const void* delta, const int64_t* cuts,
                 int dtype, int64_t m, double clamp, void* Xbeta, void* w,

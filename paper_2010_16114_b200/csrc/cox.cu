@@ -415,15 +415,155 @@ risk_kernel(const double* __restrict__ xb, const T* __restrict__ delta, const in
   }
 }
 
-extern "C" int64_t bs_cox_risk_workspace(int64_t m) { (void)m; return 0; }
+// ---------------------------------------------------------------------------
+// Multi-CTA versions of the scans for long m (C5: m = 400,000 took ~1.2 ms per
+// iteration in the single-CTA kernels, paid on every GPU).  Tile t of SCAN_TILE
+// elements is scanned by CTA t with the same block_exscan tree as the single-CTA
+// kernels, and the carries are the same sequential sums of tile totals, so W and S
+// are bitwise identical to the single-CTA results.  Phase 1: per-tile totals (and
+// Xbeta, w); phase 2: one thread sums the totals in tile order; phase 3: the tiles'
+// scans in parallel.  loglik is a fixed-grid reduction folded in CTA order.
+// ---------------------------------------------------------------------------
+constexpr int64_t SCAN_MULTI_MIN = 8 * SCAN_TILE;  // shorter vectors keep the single-CTA kernels
+constexpr int LL_GRID = 128;
+
+__global__ void scan_carry_kernel(const double* __restrict__ totals, int64_t tiles, double* __restrict__ carries) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double c = 0.0;
+    for (int64_t t = 0; t < tiles; ++t) {
+      carries[t] = c;
+      c += totals[t];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+risk_tile_kernel(const double* __restrict__ xb, int64_t m, double clamp, T* __restrict__ Xbeta, T* __restrict__ w,
+                 double* __restrict__ totals, int* __restrict__ newflags, const int* flags) {
+  __shared__ double sh[32];
+  if (*flags & BS_FLAG_NONFINITE) return;
+  const int64_t base = int64_t(blockIdx.x) * SCAN_TILE + int64_t(threadIdx.x) * SCAN_PER;
+  int myflag = 0;
+  double loc = 0.0;
+#pragma unroll
+  for (int u = 0; u < SCAN_PER; ++u) {
+    const int64_t i = base + u;
+    if (i < m) {
+      const T xt = T(xb[i]);
+      Xbeta[i] = xt;
+      T arg = xt;
+      if (xt > T(clamp)) {  // solvers.py:383-385
+        myflag |= BS_FLAG_CLAMPED;
+        arg = T(clamp);
+      }
+      const T e = exp(arg);
+      if (!isfinite(double(e))) myflag |= BS_FLAG_NONFINITE;
+      w[i] = e;
+      loc += double(e);
+    }
+  }
+  double total;
+  block_exscan(loc, sh, &total);
+  if (threadIdx.x == 0) totals[blockIdx.x] = total;
+  if (myflag) atomicOr(newflags, myflag);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+risk_scan_kernel(const T* __restrict__ w, int64_t m, const double* __restrict__ carries, T* __restrict__ W,
+                 const int* flags) {
+  __shared__ double sh[32];
+  if (*flags & BS_FLAG_NONFINITE) return;
+  const int64_t base = int64_t(blockIdx.x) * SCAN_TILE + int64_t(threadIdx.x) * SCAN_PER;
+  double wv[SCAN_PER];
+  double loc = 0.0;
+#pragma unroll
+  for (int u = 0; u < SCAN_PER; ++u) {
+    const int64_t i = base + u;
+    wv[u] = i < m ? double(w[i]) : 0.0;
+    loc += wv[u];
+  }
+  double total;
+  double run = carries[blockIdx.x] + block_exscan(loc, sh, &total);
+#pragma unroll
+  for (int u = 0; u < SCAN_PER; ++u) {
+    const int64_t i = base + u;
+    run += wv[u];
+    if (i < m) W[i] = T(run);
+  }
+}
+
+// loglik = sum delta (Xbeta - log W[cuts]) (solvers.py:398); the last CTA folds the
+// partials in CTA order and publishes the flags the tile pass raised.
+template <typename T>
+__global__ void __launch_bounds__(256)
+loglik_kernel(const T* __restrict__ Xbeta, const T* __restrict__ W, const T* __restrict__ delta,
+              const int64_t* __restrict__ cuts, int64_t m, double* __restrict__ parts, unsigned int* counter,
+              int* newflags, double* loglik, int* flags) {
+  __shared__ double sh[32];
+  if (*flags & BS_FLAG_NONFINITE) return;
+  double ll = 0.0;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+    const double dl = double(delta[i]);
+    if (dl != 0.0) {
+      const int64_t c = cuts ? cuts[i] : i;
+      ll += dl * (double(Xbeta[i]) - log(double(W[c])));
+    }
+  }
+  ll = block_sum(ll, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = ll;
+  if (last_block_done(counter) && threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned int k = 0; k < gridDim.x; ++k) t += parts[k];
+    loglik[0] = t;
+    const int nf = *newflags;
+    if (nf) atomicOr(flags, nf);
+    *newflags = 0;
+  }
+}
+
+static int64_t risk_multi_ws(int64_t m) {
+  const int64_t tiles = ceil_div(m, int64_t(SCAN_TILE));
+  return 2 * ws_bytes<double>(tiles) + ws_bytes<double>(LL_GRID) + ws_bytes<unsigned int>(1) + ws_bytes<int>(1);
+}
+
+extern "C" int64_t bs_cox_risk_workspace(int64_t m) { return m >= SCAN_MULTI_MIN ? risk_multi_ws(m) : 0; }
+
+template <typename T>
+static void launch_risk_multi(const double* xb, const T* delta, const int64_t* cuts, int64_t m, double clamp,
+                              T* Xbeta, T* w, T* W, double* loglik, int* flags, double* totals, double* carries,
+                              double* llp, unsigned int* counter, int* newflags, cudaStream_t st) {
+  const int64_t tiles = ceil_div(m, int64_t(SCAN_TILE));
+  risk_tile_kernel<T><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(xb, m, clamp, Xbeta, w, totals, newflags, flags);
+  scan_carry_kernel<<<1, 32, 0, st>>>(totals, tiles, carries);
+  risk_scan_kernel<T><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(w, m, carries, W, flags);
+  loglik_kernel<T><<<LL_GRID, 256, 0, st>>>(Xbeta, W, delta, cuts, m, llp, counter, newflags, loglik, flags);
+}
 
 extern "C" int bs_cox_risk(const double* xb, const void* delta, const int64_t* cuts, int dtype, int64_t m,
                            double clamp, void* Xbeta, void* w, void* W, double* loglik_dev, int* flags, void* work,
                            int64_t work_bytes, void* stream) {
   clear_error();
-  (void)work;
-  (void)work_bytes;
   cudaStream_t st = as_stream(stream);
+  if (m >= SCAN_MULTI_MIN && work && work_bytes >= risk_multi_ws(m) && (dtype == BS_F64 || dtype == BS_F32)) {
+    Workspace ws(work, work_bytes);
+    const int64_t tiles = ceil_div(m, int64_t(SCAN_TILE));
+    unsigned int* counter = ws.take<unsigned int>(1);  // zeroed by the caller once, re-armed by the last CTA
+    int* newflags = ws.take<int>(1);                    // idem
+    double* totals = ws.take<double>(tiles);
+    double* carries = ws.take<double>(tiles);
+    double* llp = ws.take<double>(LL_GRID);
+    if (dtype == BS_F64)
+      launch_risk_multi<double>(xb, static_cast<const double*>(delta), cuts, m, clamp, static_cast<double*>(Xbeta),
+                                static_cast<double*>(w), static_cast<double*>(W), loglik_dev, flags, totals, carries,
+                                llp, counter, newflags, st);
+    else
+      launch_risk_multi<float>(xb, static_cast<const float*>(delta), cuts, m, clamp, static_cast<float*>(Xbeta),
+                               static_cast<float*>(w), static_cast<float*>(W), loglik_dev, flags, totals, carries, llp,
+                               counter, newflags, st);
+    return check_launch("bs_cox_risk", 4);
+  }
   if (dtype == BS_F64)
     risk_kernel<double><<<1, SCAN_THREADS, 0, st>>>(xb, static_cast<const double*>(delta), cuts, m, clamp,
                                                     static_cast<double*>(Xbeta), static_cast<double*>(w),
@@ -504,7 +644,49 @@ __global__ void pd_kernel(const T* __restrict__ w, const T* __restrict__ delta, 
   }
 }
 
-extern "C" int64_t bs_cox_pi_delta_workspace(int64_t m) { return ws_bytes<double>(m); }
+// suffix sums, multi-CTA (see the risk scans above): tile t covers reversed positions
+// [t SCAN_TILE, (t+1) SCAN_TILE); phase 1 totals, phase 2 carries, phase 3 scans.
+template <typename T>
+__global__ void __launch_bounds__(SCAN_THREADS)
+suffix_tile_kernel(const T* __restrict__ W, const T* __restrict__ delta, const int64_t* __restrict__ cuts,
+                   int64_t lo, int64_t hi, const double* __restrict__ carries, double* __restrict__ totals,
+                   double* __restrict__ S, const int* flags) {
+  __shared__ double sh[32];
+  if (flags && (*flags & BS_FLAG_NONFINITE)) return;
+  const int64_t len = hi - lo;
+  const int64_t base = int64_t(blockIdx.x) * SCAN_TILE + int64_t(threadIdx.x) * SCAN_PER;
+  double cv[SCAN_PER];
+  double loc = 0.0;
+#pragma unroll
+  for (int u = 0; u < SCAN_PER; ++u) {
+    const int64_t rk = base + u;
+    cv[u] = 0.0;
+    if (rk < len) {
+      const int64_t j = hi - 1 - rk;
+      const int64_t c = cuts ? cuts[j] : j;
+      cv[u] = double(T(delta[j]) / W[c]);  // solvers.py:412
+      loc += cv[u];
+    }
+  }
+  double total;
+  const double ex = block_exscan(loc, sh, &total);
+  if (carries == nullptr) {  // phase 1
+    if (threadIdx.x == 0) totals[blockIdx.x] = total;
+    return;
+  }
+  double run = carries[blockIdx.x] + ex;
+#pragma unroll
+  for (int u = 0; u < SCAN_PER; ++u) {
+    const int64_t rk = base + u;
+    run += cv[u];
+    if (rk < len) S[hi - 1 - rk - lo] = run;
+  }
+}
+
+extern "C" int64_t bs_cox_pi_delta_workspace(int64_t m) {
+  const int64_t tiles = ceil_div(std::max<int64_t>(m, 1), int64_t(SCAN_TILE));
+  return ws_bytes<double>(m) + 2 * ws_bytes<double>(tiles);
+}
 
 extern "C" int bs_cox_pi_delta(const void* w, const void* W, const void* delta, const int64_t* cuts, int dtype,
                                int64_t m, int64_t lo, int64_t hi, void* pd, double* dmpd, const int* flags,
@@ -520,6 +702,30 @@ extern "C" int bs_cox_pi_delta(const void* w, const void* W, const void* delta, 
   double* S = ws.take<double>(std::max<int64_t>(hi - lo, 1));
   if (!S) { set_error("bs_cox_pi_delta: workspace too small"); return BS_EWORK; }
   const int grid = int(std::min<int64_t>(ceil_div(m, 256), int64_t(num_sms()) * 4));
+  const int64_t tiles = ceil_div(std::max<int64_t>(hi - lo, 1), int64_t(SCAN_TILE));
+  double* totals = ws.take<double>(tiles);
+  double* carries = ws.take<double>(tiles);
+  const bool multi = hi - lo >= SCAN_MULTI_MIN && totals && carries;
+  if (multi && (dtype == BS_F64 || dtype == BS_F32)) {
+    if (dtype == BS_F64) {
+      suffix_tile_kernel<double><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(
+          static_cast<const double*>(W), static_cast<const double*>(delta), cuts, lo, hi, nullptr, totals, S, flags);
+      scan_carry_kernel<<<1, 32, 0, st>>>(totals, tiles, carries);
+      suffix_tile_kernel<double><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(
+          static_cast<const double*>(W), static_cast<const double*>(delta), cuts, lo, hi, carries, totals, S, flags);
+      pd_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(w), static_cast<const double*>(delta), cuts,
+                                              S, m, lo, hi, static_cast<double*>(pd), dmpd, flags);
+    } else {
+      suffix_tile_kernel<float><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(
+          static_cast<const float*>(W), static_cast<const float*>(delta), cuts, lo, hi, nullptr, totals, S, flags);
+      scan_carry_kernel<<<1, 32, 0, st>>>(totals, tiles, carries);
+      suffix_tile_kernel<float><<<unsigned(tiles), SCAN_THREADS, 0, st>>>(
+          static_cast<const float*>(W), static_cast<const float*>(delta), cuts, lo, hi, carries, totals, S, flags);
+      pd_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w), static_cast<const float*>(delta), cuts, S,
+                                             m, lo, hi, static_cast<float*>(pd), dmpd, flags);
+    }
+    return check_launch("bs_cox_pi_delta", 4);
+  }
   if (dtype == BS_F64) {
     if (hi > lo)
       suffix_kernel<double><<<1, SCAN_THREADS, 0, st>>>(static_cast<const double*>(W),

@@ -616,9 +616,10 @@ def _xbeta(s, beta_local):
 def _risk(s):
     m = s.X.shape[0]
     clamp = _EXP_CLAMP[np.dtype(s.beta.dtype)]
+    rp, rn = s._work.args("risk", _lib.query("bs_cox_risk_workspace", m))
     _lib.call("bs_cox_risk", _lib.ptr(s._dev["xb"]), _lib.ptr(s.delta), _cuts_ptr(s), _lib.dtype_code(s.beta.dtype),
               m, clamp, _lib.ptr(s.Xbeta), _lib.ptr(s.w), _lib.ptr(s.W), _lib.ptr(s._dev["loglik"]),
-              _lib.ptr(s._dev["flags"]), None, 0, _lib.stream_ptr())
+              _lib.ptr(s._dev["flags"]), rp, rn, _lib.stream_ptr())
 
 
 def _raise_flags(flags_value):

@@ -374,3 +374,47 @@ def test_cox_float32_shapes_outside_the_fused_plan(m, n):
     tr = bs.run_inproc(1, fn)[0]
     _, _, otr = orc.cox_fit(x.astype(np.float64), delta, np.arange(m), 1e-4, 2e-5, 6)
     np.testing.assert_allclose(tr, otr, rtol=2e-5)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("ties", ["none", "breslow"])
+def test_long_risk_and_suffix_scans_match_single_cta(dtype, ties):
+    """m >= 8 scan tiles: bs_cox_risk / bs_cox_pi_delta run the multi-CTA scans; W, pd and
+    loglik equal the single-CTA kernels' (workspace-less call) bit for bit / to rounding."""
+    from paper_2010_16114_b200 import _lib
+
+    m = 70_001
+    dev = torch.device("cuda:0")
+    gen = np.random.Generator(np.random.Philox(91))
+    xb = torch.from_numpy(np.r_[gen.standard_normal(m) * 0.5, 0.0]).to(dev)
+    delta_h = (gen.random(m) < 0.3).astype(dtype)
+    delta = torch.from_numpy(delta_h).to(dev)
+    y = np.floor(np.arange(m, 0, -1) / 3.0)
+    cuts = None
+    if ties == "breslow":
+        cuts = torch.from_numpy(np.searchsorted(-y, -y, side="right").astype(np.int64) - 1).to(dev)
+    code = _lib.dtype_code(dtype)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    out = {}
+    for multi in (0, 1):
+        Xb, w, W, pd = (torch.empty(m, dtype=tdt, device=dev) for _ in range(4))
+        dmpd = torch.empty(m, dtype=torch.float64, device=dev)
+        ll = torch.zeros(1, dtype=torch.float64, device=dev)
+        flags = torch.zeros(1, dtype=torch.int32, device=dev)
+        nb = _lib.query("bs_cox_risk_workspace", m)
+        assert nb > 0
+        ws = torch.zeros(nb, dtype=torch.uint8, device=dev)
+        cp = _lib.ptr(cuts) if cuts is not None else None
+        _lib.call("bs_cox_risk", _lib.ptr(xb), _lib.ptr(delta), cp, code, m, 700.0, _lib.ptr(Xb), _lib.ptr(w),
+                  _lib.ptr(W), _lib.ptr(ll), _lib.ptr(flags), _lib.ptr(ws) if multi else None, nb if multi else 0,
+                  _lib.stream_ptr())
+        pw = torch.zeros(_lib.query("bs_cox_pi_delta_workspace", m), dtype=torch.uint8, device=dev)
+        pw_n = pw.numel() if multi else 8 * m  # single-CTA: S only, no room for the tile totals
+        _lib.call("bs_cox_pi_delta", _lib.ptr(w), _lib.ptr(W), _lib.ptr(delta), cp, code, m, 0, m, _lib.ptr(pd),
+                  _lib.ptr(dmpd), _lib.ptr(flags), _lib.ptr(pw), pw_n, _lib.stream_ptr())
+        torch.cuda.synchronize()
+        out[multi] = (W.cpu().numpy(), pd.cpu().numpy(), float(ll.item()), int(flags.item()))
+    np.testing.assert_array_equal(out[1][0], out[0][0])
+    np.testing.assert_array_equal(out[1][1], out[0][1])
+    np.testing.assert_allclose(out[1][2], out[0][2], rtol=1e-12)
+    assert out[1][3] == out[0][3] == 0
