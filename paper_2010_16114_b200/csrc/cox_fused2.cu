@@ -30,8 +30,7 @@ namespace {
 
 constexpr int F2_THREADS = 320;  // warp 0: A producer, warp 1: B producer, warps 2..9 consumers
 constexpr int F2_CW = 4;         // columns per ring stage
-constexpr int F2_W = 16;         // columns per wave
-constexpr int F2_QPW = F2_W / F2_CW;
+constexpr int F2_WMAX = 32;      // largest wave (columns); the wave is a template parameter
 constexpr int F2_RING = 12;      // partial slots / counters per group (> 2 LAG)
 constexpr int F2_KB = 3;         // float4 row groups per consumer thread: R <= 3072
 constexpr int64_t F2_RMAX = 1024 * F2_KB;
@@ -78,9 +77,11 @@ struct F2Args {
 };
 
 // F2_AS A stages (HBM), F2_BS B stages (L2), F2_LAG waves between A(w) and B(w)
-template <int F2_AS, int F2_BS, int F2_LAG>
+template <int F2_AS, int F2_BS, int F2_LAG, int F2_W>
 __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args a) {
   static_assert(F2_RING > 2 * F2_LAG, "partial slots must outlive the lag");
+  static_assert(F2_W == 16 || F2_W == 32, "waves of 16 or 32 columns");
+  constexpr int F2_QPW = F2_W / F2_CW;
   extern __shared__ __align__(1024) uint8_t smem[];
   if (a.flags && (*a.flags & BS_FLAG_NONFINITE)) return;  // every CTA sees the same flag
   const int S = a.S, g = int(blockIdx.x) / S, sg = int(blockIdx.x) % S;
@@ -249,11 +250,13 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
         __syncwarp();
         if (lane == 0 && rows > 0) mbar_arrive(bar(AE + s));
       }
-      // fold the 16 columns over the warp: lane l ends with column l & 15
+      // fold the wave's columns over the warp: lane l ends with column l % W
+      if constexpr (F2_W == 16) {
 #pragma unroll
-      for (int j = 0; j < F2_W; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+        for (int j = 0; j < F2_W; ++j) cs[j] += __shfl_xor_sync(0xffffffffu, cs[j], 16);
+      }
 #pragma unroll
-      for (int o = 8; o >= 1; o >>= 1) {
+      for (int o = F2_W / 2; o >= 1; o >>= 1) {
         const bool up = lane & o;
 #pragma unroll
         for (int k = 0; k < o; ++k) {
@@ -381,7 +384,7 @@ struct F2Plan {
 F2Plan f2_plan(int64_t m, int64_t n_loc) {
   F2Plan p{};
   p.ok = false;
-  if (m < 4096 || n_loc < 4 * F2_W || m % 4) return p;
+  if (m < 4096 || n_loc < 4 * F2_WMAX || m % 4) return p;
   const char* e = getenv("BS_COX_FUSED2");
   if (e && e[0] == '0') return p;
   int dev = 0, coop = 0, maxsm = 0;
@@ -394,9 +397,11 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
     const char* c = getenv("BS_F2_CFG");
     return c ? atoi(c) : 0;
   }();
-  static const int as_[9] = {2, 3, 2, 3, 2, 3, 3, 2, 4}, bs_[9] = {2, 1, 2, 1, 2, 2, 2, 3, 2},
-                   lag_[9] = {2, 2, 3, 3, 4, 3, 2, 2, 2};
-  const int ci = cfg >= 0 && cfg < 9 ? cfg : 0;
+  static const int as_[12] = {2, 3, 2, 3, 2, 3, 3, 2, 4, 2, 2, 2}, bs_[12] = {2, 1, 2, 1, 2, 2, 2, 3, 2, 2, 2, 3},
+                   lag_[12] = {2, 2, 3, 3, 4, 3, 2, 2, 2, 1, 2, 1},
+                   w_[12] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 32};
+  const int ci = cfg >= 0 && cfg < 12 ? cfg : 0;
+  const int W = w_[ci];
   p.cfg = ci;
   const int nst = as_[ci] + bs_[ci];
   const int64_t rmax = std::min<int64_t>(F2_RMAX, (4 * F2_STAGE_MAX / nst) / (4 * F2_CW));
@@ -406,28 +411,33 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
     if (u > best_u) { best_u = u; best_s = S; }
     if (u * 100 >= G * 96) { best_s = S; best_u = u; break; }
   }
+  static const int force_s = [] {
+    const char* c = getenv("BS_F2_S");  // experiments: fixed segment count
+    return c ? atoi(c) : 0;
+  }();
+  if (force_s >= int(ceil_div(m, rmax)) && force_s <= G) best_s = force_s;
   if (best_s == 0) return p;
   p.S = best_s;
   p.Gc = G / best_s;
   p.R = ceil_div(ceil_div(m, p.S), int64_t(4)) * 4;
   if (p.R > rmax) return p;
   p.cpg = ceil_div(n_loc, int64_t(p.Gc));
-  p.smem = size_t(nst * F2_CW * p.R * 4 + 2 * int64_t(p.S) * F2_W * 8 + (lag_[ci] + 1) * F2_W * 8 +
-                  2 * F2_W * 4 + 2 * 8 * F2_W * 4 + (2 * nst + 4) * 8 + 64);
+  p.smem = size_t(nst * F2_CW * p.R * 4 + 2 * int64_t(p.S) * W * 8 + (lag_[ci] + 1) * W * 8 + 2 * W * 4 +
+                  2 * 8 * W * 4 + (2 * nst + 4) * 8 + 64);
   if (int64_t(p.smem) > int64_t(maxsm) - 1024) return p;
   p.ok = true;
   return p;
 }
 
 int64_t f2_workspace(const F2Plan& p, int64_t m) {
-  return ws_bytes<unsigned int>(int64_t(p.Gc) * F2_RING) + ws_bytes<double>(int64_t(p.Gc) * F2_RING * p.S * F2_W) +
+  return ws_bytes<unsigned int>(int64_t(p.Gc) * F2_RING) + ws_bytes<double>(int64_t(p.Gc) * F2_RING * p.S * F2_WMAX) +
          ws_bytes<double>(int64_t(p.Gc) * m) + ws_bytes<double>(p.Gc);
 }
 
 int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const double* v, float* grad, float* beta,
               double sigma, double lam, double* xb_out, const int* flags, Workspace& ws, cudaStream_t st) {
   unsigned int* counters = ws.take<unsigned int>(int64_t(p.Gc) * F2_RING);
-  double* partials = ws.take<double>(int64_t(p.Gc) * F2_RING * p.S * F2_W);
+  double* partials = ws.take<double>(int64_t(p.Gc) * F2_RING * p.S * F2_WMAX);
   double* xb_parts = ws.take<double>(int64_t(p.Gc) * m);
   double* l1_parts = ws.take<double>(p.Gc);
   if (!counters || !partials || !xb_parts || !l1_parts) {
@@ -444,17 +454,24 @@ int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const d
   }();
   F2Args a{X, m, n_loc, p.R, p.cpg, p.S, p.Gc, pf, v, grad, beta, sigma, lam, xb_parts, l1_parts, partials, counters, flags};
   const void* k = nullptr;
+#define F2K(A, B, L, W)                                                       \
+  k = reinterpret_cast<const void*>(cox_fused2_kernel<A, B, L, W>);         \
+  smem_attr(cox_fused2_kernel<A, B, L, W>, int(p.smem));
   switch (p.cfg) {
-    case 1: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 1, 2>); smem_attr(cox_fused2_kernel<3, 1, 2>, int(p.smem)); break;
-    case 2: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 3>); smem_attr(cox_fused2_kernel<2, 2, 3>, int(p.smem)); break;
-    case 3: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 1, 3>); smem_attr(cox_fused2_kernel<3, 1, 3>, int(p.smem)); break;
-    case 4: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 4>); smem_attr(cox_fused2_kernel<2, 2, 4>, int(p.smem)); break;
-    case 5: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 2, 3>); smem_attr(cox_fused2_kernel<3, 2, 3>, int(p.smem)); break;
-    case 6: k = reinterpret_cast<const void*>(cox_fused2_kernel<3, 2, 2>); smem_attr(cox_fused2_kernel<3, 2, 2>, int(p.smem)); break;
-    case 7: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 3, 2>); smem_attr(cox_fused2_kernel<2, 3, 2>, int(p.smem)); break;
-    case 8: k = reinterpret_cast<const void*>(cox_fused2_kernel<4, 2, 2>); smem_attr(cox_fused2_kernel<4, 2, 2>, int(p.smem)); break;
-    default: k = reinterpret_cast<const void*>(cox_fused2_kernel<2, 2, 2>); smem_attr(cox_fused2_kernel<2, 2, 2>, int(p.smem)); break;
+    case 1: F2K(3, 1, 2, 16) break;
+    case 2: F2K(2, 2, 3, 16) break;
+    case 3: F2K(3, 1, 3, 16) break;
+    case 4: F2K(2, 2, 4, 16) break;
+    case 5: F2K(3, 2, 3, 16) break;
+    case 6: F2K(3, 2, 2, 16) break;
+    case 7: F2K(2, 3, 2, 16) break;
+    case 8: F2K(4, 2, 2, 16) break;
+    case 9: F2K(2, 2, 1, 32) break;
+    case 10: F2K(2, 2, 2, 32) break;
+    case 11: F2K(2, 3, 1, 32) break;
+    default: F2K(2, 2, 2, 16) break;
   }
+#undef F2K
   void* args[] = {&a};
   cudaError_t e = cudaLaunchCooperativeKernel(k, dim3(p.S * p.Gc), dim3(F2_THREADS), args, p.smem, st);
   if (e != cudaSuccess) {
