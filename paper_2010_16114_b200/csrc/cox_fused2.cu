@@ -29,11 +29,8 @@ using namespace tc;
 namespace {
 
 constexpr int F2_THREADS = 320;  // warp 0: A producer, warp 1: B producer, warps 2..9 consumers
-constexpr int F2_CW = 4;         // columns per ring stage
 constexpr int F2_WMAX = 32;      // largest wave (columns); the wave is a template parameter
 constexpr int F2_RING = 12;      // partial slots / counters per group (> 2 LAG)
-constexpr int F2_KB = 3;         // float4 row groups per consumer thread: R <= 3072
-constexpr int64_t F2_RMAX = 1024 * F2_KB;
 constexpr int64_t F2_STAGE_MAX = 48 * 1024;  // bytes of one stage (F2_CW columns x R rows)
 
 typedef unsigned long long f2r;
@@ -77,7 +74,8 @@ struct F2Args {
 };
 
 // F2_AS A stages (HBM), F2_BS B stages (L2), F2_LAG waves between A(w) and B(w)
-template <int F2_AS, int F2_BS, int F2_LAG, int F2_W>
+// F2_CW columns per ring stage, F2_KB float4 row groups per consumer thread (R <= 1024 KB)
+template <int F2_AS, int F2_BS, int F2_LAG, int F2_W, int F2_CW, int F2_KB>
 __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args a) {
   static_assert(F2_RING > 2 * F2_LAG, "partial slots must outlive the lag");
   static_assert(F2_W == 16 || F2_W == 32, "waves of 16 or 32 columns");
@@ -397,14 +395,17 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
     const char* c = getenv("BS_F2_CFG");
     return c ? atoi(c) : 0;
   }();
-  static const int as_[12] = {2, 3, 2, 3, 2, 3, 3, 2, 4, 2, 2, 2}, bs_[12] = {2, 1, 2, 1, 2, 2, 2, 3, 2, 2, 2, 3},
-                   lag_[12] = {2, 2, 3, 3, 4, 3, 2, 2, 2, 1, 2, 1},
-                   w_[12] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 32};
-  const int ci = cfg >= 0 && cfg < 12 ? cfg : 0;
-  const int W = w_[ci];
+  static const int as_[15] = {2, 3, 2, 3, 2, 3, 3, 2, 4, 2, 2, 2, 4, 3, 4},
+                   bs_[15] = {2, 1, 2, 1, 2, 2, 2, 3, 2, 2, 2, 3, 4, 3, 3},
+                   lag_[15] = {2, 2, 3, 3, 4, 3, 2, 2, 2, 1, 2, 1, 2, 2, 2},
+                   w_[15] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 32, 16, 16, 16},
+                   cw_[15] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 2, 2, 2},
+                   kb_[15] = {3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 4, 4, 4};
+  const int ci = cfg >= 0 && cfg < 15 ? cfg : 0;
+  const int W = w_[ci], CW = cw_[ci];
   p.cfg = ci;
   const int nst = as_[ci] + bs_[ci];
-  const int64_t rmax = std::min<int64_t>(F2_RMAX, (4 * F2_STAGE_MAX / nst) / (4 * F2_CW));
+  const int64_t rmax = std::min<int64_t>(1024 * kb_[ci], (4 * F2_STAGE_MAX / nst) / (4 * CW));
   int best_s = 0, best_u = 0;
   for (int S = int(ceil_div(m, rmax)); S <= G; ++S) {
     const int u = S * (G / S);
@@ -422,7 +423,7 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
   p.R = ceil_div(ceil_div(m, p.S), int64_t(4)) * 4;
   if (p.R > rmax) return p;
   p.cpg = ceil_div(n_loc, int64_t(p.Gc));
-  p.smem = size_t(nst * F2_CW * p.R * 4 + 2 * int64_t(p.S) * W * 8 + (lag_[ci] + 1) * W * 8 + 2 * W * 4 +
+  p.smem = size_t(nst * CW * p.R * 4 + 2 * int64_t(p.S) * W * 8 + (lag_[ci] + 1) * W * 8 + 2 * W * 4 +
                   2 * 8 * W * 4 + (2 * nst + 4) * 8 + 64);
   if (int64_t(p.smem) > int64_t(maxsm) - 1024) return p;
   p.ok = true;
@@ -454,22 +455,25 @@ int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const d
   }();
   F2Args a{X, m, n_loc, p.R, p.cpg, p.S, p.Gc, pf, v, grad, beta, sigma, lam, xb_parts, l1_parts, partials, counters, flags};
   const void* k = nullptr;
-#define F2K(A, B, L, W)                                                       \
-  k = reinterpret_cast<const void*>(cox_fused2_kernel<A, B, L, W>);         \
-  smem_attr(cox_fused2_kernel<A, B, L, W>, int(p.smem));
+#define F2K(A, B, L, W, CW, KB)                                                 \
+  k = reinterpret_cast<const void*>(cox_fused2_kernel<A, B, L, W, CW, KB>);   \
+  smem_attr(cox_fused2_kernel<A, B, L, W, CW, KB>, int(p.smem));
   switch (p.cfg) {
-    case 1: F2K(3, 1, 2, 16) break;
-    case 2: F2K(2, 2, 3, 16) break;
-    case 3: F2K(3, 1, 3, 16) break;
-    case 4: F2K(2, 2, 4, 16) break;
-    case 5: F2K(3, 2, 3, 16) break;
-    case 6: F2K(3, 2, 2, 16) break;
-    case 7: F2K(2, 3, 2, 16) break;
-    case 8: F2K(4, 2, 2, 16) break;
-    case 9: F2K(2, 2, 1, 32) break;
-    case 10: F2K(2, 2, 2, 32) break;
-    case 11: F2K(2, 3, 1, 32) break;
-    default: F2K(2, 2, 2, 16) break;
+    case 1: F2K(3, 1, 2, 16, 4, 3) break;
+    case 2: F2K(2, 2, 3, 16, 4, 3) break;
+    case 3: F2K(3, 1, 3, 16, 4, 3) break;
+    case 4: F2K(2, 2, 4, 16, 4, 3) break;
+    case 5: F2K(3, 2, 3, 16, 4, 3) break;
+    case 6: F2K(3, 2, 2, 16, 4, 3) break;
+    case 7: F2K(2, 3, 2, 16, 4, 3) break;
+    case 8: F2K(4, 2, 2, 16, 4, 3) break;
+    case 9: F2K(2, 2, 1, 32, 4, 3) break;
+    case 10: F2K(2, 2, 2, 32, 4, 3) break;
+    case 11: F2K(2, 3, 1, 32, 4, 3) break;
+    case 12: F2K(4, 4, 2, 16, 2, 4) break;
+    case 13: F2K(3, 3, 2, 16, 2, 4) break;
+    case 14: F2K(4, 3, 2, 16, 2, 4) break;
+    default: F2K(2, 2, 2, 16, 4, 3) break;
   }
 #undef F2K
   void* args[] = {&a};
