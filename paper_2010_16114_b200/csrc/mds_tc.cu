@@ -297,9 +297,9 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const uint32_t b = c & 1;
           // lanes could see a phase complete at different instants: decide on lane 0 only,
           // or part of the warp would issue the MMA now and the rest again later
-          const bool go = __shfl_sync(0xffffffffu,
-                                      int(mbar_test(b1_full(s), (c / NB1) & 1) && mbar_test(d1_empty(b), ((c >> 1) & 1) ^ 1)),
-                                      0) != 0;
+          int probe = 0;
+          if (lane == 0) probe = mbar_test(b1_full(s), (c / NB1) & 1) && mbar_test(d1_empty(b), ((c >> 1) & 1) ^ 1);
+          const bool go = __shfl_sync(0xffffffffu, probe, 0) != 0;
           if (go) {
             tc_fence_after();
             const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D1 + b * CHI, 0);
@@ -324,11 +324,11 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const int s = int(c % NB2);
           const bool first = (t2 % a.G) == 0;
           const bool last = ((t2 % a.G) == a.G - 1) || (t2 == nch - 1);
-          const bool go = __shfl_sync(0xffffffffu,
-                                      int(mbar_test(a2_full(b), (c >> 1) & 1) &&
-                                          (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
-                                          mbar_test(b2_full(s), (c / NB2) & 1)),
-                                      0) != 0;
+          int probe = 0;
+          if (lane == 0)
+            probe = mbar_test(a2_full(b), (c >> 1) & 1) && (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
+                    mbar_test(b2_full(s), (c / NB2) & 1);
+          const bool go = __shfl_sync(0xffffffffu, probe, 0) != 0;
           if (go) {
             tc_fence_after();
             const uint32_t d = __shfl_sync(0xffffffffu, tmem + T_D2, 0);
