@@ -222,7 +222,13 @@ def read_matrix(path, comm, dtype=None):
 
 
 def write_matrix(path, array):
-    """Write a DistArray (every rank writes its own byte range) or a plain array (cli.py:63-78)."""
+    """Write a DistArray (every rank writes its own byte range) or a plain array (cli.py:63-78).
+
+    PackedGenotypes are written as the int8 matrix they hold (dtype code 3)."""
+    if getattr(array, "packed", False):
+        from .distarray import unpack_genotypes
+
+        array = unpack_genotypes(array)
     if not isinstance(array, DistArray):
         data = np.asarray(array)
         if data.dtype not in _CODE_BY_DTYPE:

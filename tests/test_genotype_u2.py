@@ -210,3 +210,20 @@ def test_packed_more_ranks_than_columns():
         np.testing.assert_allclose(got[0], one[0], rtol=1e-6)
         np.testing.assert_allclose(got[1], one[1], rtol=1e-5, atol=1e-9)
         np.testing.assert_array_equal(got[2], orc.genotype_fill(m, n, seed))
+
+
+@pytest.mark.gpu
+def test_packed_genotypes_write_as_int8_dsta(tmp_path):
+    from paper_2010_16114_b200 import io as bio
+
+    m, n = 301, 17
+    path = tmp_path / "g.dsta"
+
+    def fn(comm):
+        p = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), 9)
+        bio.write_matrix(path, p)
+        comm.barrier()
+        return bs.gather_full(bio.read_matrix(path, comm, dtype=np.int8))
+
+    for got in bs.run_inproc(3, fn):
+        np.testing.assert_array_equal(got, orc.genotype_fill(m, n, 9))
