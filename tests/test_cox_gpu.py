@@ -418,3 +418,29 @@ def test_long_risk_and_suffix_scans_match_single_cta(dtype, ties):
     np.testing.assert_array_equal(out[1][1], out[0][1])
     np.testing.assert_allclose(out[1][2], out[0][2], rtol=1e-12)
     assert out[1][3] == out[0][3] == 0
+
+
+def test_fused_float32_with_monitor_matches_two_pass(monkeypatch):
+    """A convergence monitor stops before stepping; the fused path (default for float32)
+    must stop at the same iteration with the same trace as the two-pass path, and a
+    follow-up call must not reuse a stale X beta."""
+    gen = np.random.Generator(np.random.Philox(77))
+    m, n = 8000, 600
+    x = gen.standard_normal((m, n)).astype(np.float32)
+    delta = (gen.random(m) < 0.5).astype(np.float64)
+    y = np.arange(m, 0, -1, dtype=np.float64)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=2e-6)
+        mon = bs.ConvergenceMonitor(window=3, rel_tol=1e-3)
+        bs.cox_fit(st, 200, monitor=mon)
+        first = len(st.trace)
+        bs.cox_fit(st, 3)
+        return np.asarray(st.trace), first, bs.gather_full(st.beta)
+
+    fused = bs.run_inproc(1, fn)[0]
+    monkeypatch.setenv("BS_COX_FUSION", "0")
+    two = bs.run_inproc(1, fn)[0]
+    assert fused[1] == two[1] < 200
+    np.testing.assert_allclose(fused[0], two[0], rtol=1e-6)
+    np.testing.assert_allclose(fused[2], two[2], rtol=1e-4, atol=1e-8)
