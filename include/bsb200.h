@@ -38,6 +38,8 @@ extern "C" {
 #define BS_EINVAL 1   /* bad argument (maps to ValueError / ShapeError)       */
 #define BS_ECUDA 2    /* CUDA launch/runtime failure                           */
 #define BS_EWORK 3    /* workspace too small                                   */
+#define BS_ENUMERIC 4 /* nonfinite risk weights (NumericError, solvers.py:388-389) */
+#define BS_ENCCL 5    /* NCCL missing or failed                                  */
 
 /* dtype codes (comm.py:68-72; int8 added) */
 #define BS_F32 0
@@ -272,6 +274,39 @@ int bs_cox_grad_xbeta(const void* X, int xdtype, const double* dmpd, int dtype,
 /* trace entry (solvers.py:438-441): out_dev[0] = -loglik + lam * l1. */
 int bs_cox_objective(const double* loglik_dev, const double* l1_dev, double lam,
                      double* out_dev, void* stream);
+
+/* ---- solver-level runtime (SURVEY.md 8(b) build proposal) ------------------
+ * A per-rank context owns a stream and, for size > 1, an NCCL communicator
+ * (libnccl.so.2 is loaded at run time).  Rank 0 calls bs_nccl_unique_id and ships
+ * the 128 bytes to the other ranks out of band (the Python layer uses its
+ * communicator); every rank then calls bs_ctx_create with the same id.  States own
+ * their workspaces; the caller owns X, delta, cuts, beta and grad (device memory,
+ * column split as in cox_init, solvers.py:337-373).  Every call that communicates is
+ * collective: all ranks issue it in the same order. */
+typedef struct bs_ctx* bs_ctx_t;
+typedef struct bs_cox* bs_cox_t;
+int bs_nccl_unique_id(void* out128);
+int bs_ctx_create(int rank, int size, int device, const void* nccl_unique_id,
+                  void* stream, bs_ctx_t* out);
+int bs_ctx_destroy(bs_ctx_t ctx);
+
+/* CoxState (solvers.py:313-373) with sigma given; float32 X with float32
+ * arithmetic runs the fused one-stream pass, as cox_fit does by default. */
+int bs_cox_state_create(bs_ctx_t ctx, const void* X, int xdtype, int dtype,
+                        int64_t m, int64_t n_loc, const void* delta,
+                        const int64_t* cuts, double lam, double sigma,
+                        void* beta, void* grad, bs_cox_t* out);
+int bs_cox_state_destroy(bs_cox_t state);
+
+/* cox_fit (solvers.py:422-450): iters proximal-gradient steps.  trace_out (host,
+ * >= ceil(iters / trace_every) doubles) receives the objective of the iterate
+ * entering every trace_every-th step; monitor_window > 0 applies the
+ * ConvergenceMonitor rule (solvers.py:54-70) with monitor_tol, which may stop
+ * before stepping.  *iters_run = iterations completed (the first nonfinite one
+ * on BS_ENUMERIC), *flags_out = BS_FLAG_* seen (CLAMPED means warn). */
+int bs_cox_run(bs_cox_t state, int iters, int trace_every, int monitor_window,
+               double monitor_tol, double* trace_out, int* ntrace_out,
+               int* iters_run, int* flags_out);
 
 #ifdef __cplusplus
 }

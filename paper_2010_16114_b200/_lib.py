@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("BS_LIB_PATH", str(PKG / "libbsb200.so")))
 HEADER = PKG.parent / "include" / "bsb200.h"
 
 # status codes (bsb200.h)
-BS_OK, BS_EINVAL, BS_ECUDA, BS_EWORK = 0, 1, 2, 3
+BS_OK, BS_EINVAL, BS_ECUDA, BS_EWORK, BS_ENUMERIC, BS_ENCCL = 0, 1, 2, 3, 4, 5
 # dtype codes (comm.py:68-72 + int8)
 BS_F32, BS_F64, BS_I64, BS_I8, BS_U2 = 0, 1, 2, 3, 4
 # ReduceOp codes (comm.py:54-58 order)
@@ -43,6 +43,12 @@ SIGNATURES = {
     "bs_philox_uniform": (_i, [_p, _i, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_fill": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_packed_bytes": (_i64, [_i64]),
+    "bs_nccl_unique_id": (_i, [_p]),
+    "bs_ctx_create": (_i, [_i, _i, _i, _p, _p, _p]),
+    "bs_ctx_destroy": (_i, [_p]),
+    "bs_cox_state_create": (_i, [_p, _p, _i, _i, _i64, _i64, _p, _p, _d, _d, _p, _p, _p]),
+    "bs_cox_state_destroy": (_i, [_p]),
+    "bs_cox_run": (_i, [_p, _i, _i, _i, _d, _p, _p, _p, _p]),
     "bs_genotype_pack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_unpack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_fill_packed": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),

@@ -1,0 +1,347 @@
+// Solver-level C ABI (SURVEY.md §8(b) "What the C-ABI layer must export"): a per-rank
+// context owning a stream and an NCCL communicator, a Cox state that owns its
+// workspaces, and bs_cox_run, the whole cox_fit loop (solvers.py:422-450) in native code
+// (same kernels and order as paper_2010_16114_b200/solvers.py:cox_fit, collectives over
+// NCCL).  A host without Python can drive a fit with these five calls; the Python package
+// keeps its own loop over the same kernels.
+//
+// NCCL is loaded at run time (dlopen "libnccl.so.2"), so the library still loads where
+// NCCL is absent; a context with size 1 needs no NCCL at all.
+#include "bsb200.cuh"
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+using namespace bs;
+
+namespace {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+  });
+  return api;
+}
+
+}  // namespace
+
+struct bs_ctx {
+  int rank, size, device;
+  cudaStream_t stream;
+  ncclComm_t comm;
+};
+
+struct bs_cox {
+  bs_ctx* ctx;
+  const void* X;
+  int xdtype, dtype;
+  int64_t m, n_loc;
+  const void* delta;
+  const int64_t* cuts;
+  double lam, sigma, clamp;
+  void* beta;
+  void* grad;
+  // owned device buffers
+  double* xb;  // m + 1: X beta (reduced), ||beta||_1
+  void *Xbeta, *w, *W, *pd;
+  double* dmpd;
+  double* loglik;
+  int* flags;
+  void *ws_xb, *ws_risk, *ws_pd, *ws_grad, *ws_fused, *ws_red;
+  int64_t n_xb, n_risk, n_pd, n_grad, n_fused, n_red;
+  bool fused;
+  bool xb_fresh;  // xb holds the last fused pass's local partial for the current beta
+};
+
+namespace {
+
+int nccl_err(const char* what, ncclResult_t r) {
+  set_error("%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "NCCL error");
+  return BS_ENCCL;
+}
+
+int dalloc(void** p, int64_t bytes) {
+  *p = nullptr;
+  if (bytes <= 0) bytes = 256;
+  if (cudaMalloc(p, size_t(bytes)) != cudaSuccess) return BS_ECUDA;
+  return cudaMemset(*p, 0, size_t(bytes)) == cudaSuccess ? BS_OK : BS_ECUDA;
+}
+
+int allreduce_sum_f64(bs_ctx* c, double* buf, int64_t count) {
+  if (c->size <= 1 || count == 0) return BS_OK;
+  const ncclResult_t r = nccl().AllReduce(buf, buf, size_t(count), ncclFloat64, ncclSum, c->comm, c->stream);
+  return r == ncclSuccess ? BS_OK : nccl_err("allreduce", r);
+}
+
+// scn m + ||beta||_1, reduced over ranks (solvers.py:436; _xbeta in solvers.py)
+int cox_xbeta(bs_cox* s) {
+  bs_ctx* c = s->ctx;
+  int rc = bs_reduce(s->beta, s->dtype, s->n_loc, BS_SUM, BS_T_ABS, s->xb + s->m, s->ws_red, s->n_red, c->stream);
+  if (rc) return rc;
+  rc = bs_cox_xbeta(s->X, s->xdtype, s->beta, s->dtype, s->m, s->n_loc, s->xb, s->ws_xb, s->n_xb, c->stream);
+  if (rc) return rc;
+  s->xb_fresh = false;
+  return allreduce_sum_f64(c, s->xb, s->m + 1);
+}
+
+bool converged(std::vector<double>& h, int window, double tol, double f) {  // solvers.py:54-70
+  h.push_back(f);
+  if (int(h.size()) <= window) return false;
+  const double a = h.back(), b = h[h.size() - 1 - size_t(window)];
+  return std::fabs(a - b) / (std::fabs(a) + 1.0) < tol;
+}
+
+}  // namespace
+
+extern "C" int bs_nccl_unique_id(void* out128) {
+  clear_error();
+  if (!out128) { set_error("bs_nccl_unique_id: null output"); return BS_EINVAL; }
+  if (!nccl().ok) { set_error("bs_nccl_unique_id: libnccl.so.2 not loadable"); return BS_ENCCL; }
+  ncclUniqueId id;
+  const ncclResult_t r = nccl().GetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_err("bs_nccl_unique_id", r);
+  std::memcpy(out128, &id, sizeof(id));
+  return BS_OK;
+}
+
+extern "C" int bs_ctx_create(int rank, int size, int device, const void* nccl_unique_id, void* stream,
+                             bs_ctx_t* out) {
+  clear_error();
+  if (!out || size < 1 || rank < 0 || rank >= size || device < 0) {
+    set_error("bs_ctx_create: bad arguments");
+    return BS_EINVAL;
+  }
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) { set_error("bs_ctx_create: cudaSetDevice(%d) failed", device); return BS_ECUDA; }
+  bs_ctx* c = new bs_ctx{rank, size, device, as_stream(stream), nullptr};
+  if (size > 1) {
+    if (!nccl_unique_id) { delete c; set_error("bs_ctx_create: size > 1 needs an NCCL unique id"); return BS_EINVAL; }
+    if (!nccl().ok) { delete c; set_error("bs_ctx_create: libnccl.so.2 not loadable"); return BS_ENCCL; }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    const ncclResult_t r = nccl().CommInitRank(&c->comm, size, id, rank);
+    if (r != ncclSuccess) { delete c; return nccl_err("bs_ctx_create", r); }
+  }
+  *out = c;
+  return BS_OK;
+}
+
+extern "C" int bs_ctx_destroy(bs_ctx_t c) {
+  clear_error();
+  if (!c) return BS_OK;
+  int rc = BS_OK;
+  if (c->comm && nccl().ok) {
+    const ncclResult_t r = nccl().CommDestroy(c->comm);
+    if (r != ncclSuccess) rc = nccl_err("bs_ctx_destroy", r);
+  }
+  delete c;
+  return rc;
+}
+
+extern "C" int bs_cox_state_create(bs_ctx_t ctx, const void* X, int xdtype, int dtype, int64_t m, int64_t n_loc,
+                                   const void* delta, const int64_t* cuts, double lam, double sigma, void* beta,
+                                   void* grad, bs_cox_t* out) {
+  clear_error();
+  if (!ctx || !out || m < 1 || n_loc < 0 || !delta || (dtype != BS_F32 && dtype != BS_F64) || sigma <= 0 ||
+      (n_loc > 0 && (!X || !beta || !grad))) {
+    set_error("bs_cox_state_create: bad arguments");
+    return BS_EINVAL;
+  }
+  *out = nullptr;
+  cudaSetDevice(ctx->device);
+  bs_cox* s = new bs_cox();
+  s->ctx = ctx;
+  s->X = X;
+  s->xdtype = xdtype;
+  s->dtype = dtype;
+  s->m = m;
+  s->n_loc = n_loc;
+  s->delta = delta;
+  s->cuts = cuts;
+  s->lam = lam;
+  s->sigma = sigma;
+  s->clamp = dtype == BS_F64 ? 700.0 : 85.0;  // solvers.py _EXP_CLAMP
+  s->beta = beta;
+  s->grad = grad;
+  // the fused one-stream pass for float32 X with float32 arithmetic, as cox_fit's default
+  s->fused = xdtype == BS_F32 && dtype == BS_F32 && ctx->size >= 1;
+  const int64_t es = dtype == BS_F64 ? 8 : 4;
+  s->n_xb = bs_cox_xbeta_workspace(xdtype, m, n_loc);
+  s->n_risk = bs_cox_risk_workspace(m);
+  s->n_pd = bs_cox_pi_delta_workspace(m);
+  s->n_grad = bs_cox_grad_workspace(xdtype, m, n_loc);
+  s->n_fused = s->fused ? bs_cox_grad_xbeta_workspace(xdtype, m, n_loc) : 0;
+  s->n_red = bs_reduce_workspace(std::max<int64_t>(n_loc, 1));
+  int rc = BS_OK;
+  void* p = nullptr;
+  rc |= dalloc(&p, 8 * (m + 1)); s->xb = static_cast<double*>(p);
+  rc |= dalloc(&s->Xbeta, es * m);
+  rc |= dalloc(&s->w, es * m);
+  rc |= dalloc(&s->W, es * m);
+  rc |= dalloc(&s->pd, es * m);
+  rc |= dalloc(&p, 8 * m); s->dmpd = static_cast<double*>(p);
+  rc |= dalloc(&p, 8); s->loglik = static_cast<double*>(p);
+  rc |= dalloc(&p, 4); s->flags = static_cast<int*>(p);
+  rc |= dalloc(&s->ws_xb, s->n_xb);
+  rc |= dalloc(&s->ws_risk, s->n_risk);
+  rc |= dalloc(&s->ws_pd, s->n_pd);
+  rc |= dalloc(&s->ws_grad, s->n_grad);
+  rc |= dalloc(&s->ws_fused, s->n_fused);
+  rc |= dalloc(&s->ws_red, s->n_red);
+  if (rc != BS_OK) {
+    bs_cox_state_destroy(s);
+    set_error("bs_cox_state_create: device allocation failed");
+    return BS_ECUDA;
+  }
+  s->n_xb = std::max<int64_t>(s->n_xb, 256);
+  s->n_risk = std::max<int64_t>(s->n_risk, 256);
+  s->n_pd = std::max<int64_t>(s->n_pd, 256);
+  s->n_grad = std::max<int64_t>(s->n_grad, 256);
+  s->n_fused = std::max<int64_t>(s->n_fused, 256);
+  s->n_red = std::max<int64_t>(s->n_red, 256);
+  *out = s;
+  return BS_OK;
+}
+
+extern "C" int bs_cox_state_destroy(bs_cox_t s) {
+  clear_error();
+  if (!s) return BS_OK;
+  cudaSetDevice(s->ctx->device);
+  void* bufs[] = {s->xb, s->Xbeta, s->w, s->W, s->pd, s->dmpd, s->loglik, s->flags,
+                  s->ws_xb, s->ws_risk, s->ws_pd, s->ws_grad, s->ws_fused, s->ws_red};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete s;
+  return BS_OK;
+}
+
+extern "C" int bs_cox_run(bs_cox_t s, int iters, int trace_every, int monitor_window, double monitor_tol,
+                          double* trace_out, int* ntrace_out, int* iters_run, int* flags_out) {
+  clear_error();
+  if (!s || iters < 0 || trace_every < 0 || monitor_window < 0) { set_error("bs_cox_run: bad arguments"); return BS_EINVAL; }
+  bs_ctx* c = s->ctx;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  if (ntrace_out) *ntrace_out = 0;
+  if (iters_run) *iters_run = 0;
+  if (flags_out) *flags_out = 0;
+  if (iters == 0) return BS_OK;
+  const int64_t m = s->m;
+  int rc = BS_OK;
+  if (cudaMemsetAsync(s->flags, 0, sizeof(int), st) != cudaSuccess) return BS_ECUDA;
+  double* trace_dev = nullptr;
+  int* fhist = nullptr;
+  if (cudaMalloc(&trace_dev, sizeof(double) * size_t(iters)) != cudaSuccess ||
+      cudaMalloc(&fhist, sizeof(int) * size_t(iters)) != cudaSuccess) {
+    cudaFree(trace_dev);
+    set_error("bs_cox_run: device allocation failed");
+    return BS_ECUDA;
+  }
+  std::vector<double> history, host_trace;
+  const bool monitor = monitor_window > 0;
+  const bool reuse = s->fused && s->xb_fresh;
+  int ran = iters;
+  auto fail = [&](int code) {
+    cudaFree(trace_dev);
+    cudaFree(fhist);
+    return code;
+  };
+  if (s->fused && !reuse && (rc = cox_xbeta(s))) return fail(rc);
+  for (int it = 0; it < iters; ++it) {
+    if (!s->fused) {
+      if ((rc = cox_xbeta(s))) return fail(rc);  // scn m + ||beta||_1 (solvers.py:436)
+    } else if ((it > 0 || reuse) && (rc = allreduce_sum_f64(c, s->xb, m + 1))) {
+      return fail(rc);  // the fused pass's X beta partials
+    }
+    if ((rc = bs_cox_risk(s->xb, s->delta, s->cuts, s->dtype, m, s->clamp, s->Xbeta, s->w, s->W, s->loglik, s->flags,
+                          s->ws_risk, s->n_risk, st)))
+      return fail(rc);
+    cudaMemcpyAsync(fhist + it, s->flags, sizeof(int), cudaMemcpyDeviceToDevice, st);
+    if (trace_every && it % trace_every == 0) {
+      if ((rc = bs_cox_objective(s->loglik, s->xb + m, s->lam, trace_dev + it, st))) return fail(rc);
+      if (monitor) {  // solvers.py:438-441: the monitor may stop before stepping
+        double obj;
+        int fl;
+        cudaMemcpyAsync(&obj, trace_dev + it, sizeof(double), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(&fl, s->flags, sizeof(int), cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return fail(BS_ECUDA);
+        if (fl & BS_FLAG_NONFINITE) { ran = it; break; }
+        host_trace.push_back(obj);
+        if (converged(history, monitor_window, monitor_tol, obj)) { ran = it + 1; break; }
+      }
+    }
+    if ((rc = bs_cox_pi_delta(s->w, s->W, s->delta, s->cuts, s->dtype, m, 0, m, s->pd, s->dmpd, s->flags, s->ws_pd,
+                              s->n_pd, st)))
+      return fail(rc);
+    if (s->fused)
+      rc = bs_cox_grad_xbeta(s->X, s->xdtype, s->dmpd, s->dtype, m, s->n_loc, s->grad, s->beta, s->sigma, s->lam, s->xb,
+                             s->flags, 1, s->ws_fused, s->n_fused, st);
+    else
+      rc = bs_cox_grad_step(s->X, s->xdtype, s->dmpd, s->dtype, m, s->n_loc, s->grad, s->beta, s->sigma, s->lam, 1,
+                            s->xb + m, s->flags, s->ws_grad, s->n_grad, st);
+    if (rc) return fail(rc);
+  }
+  // first iteration whose risk weights went nonfinite, as cox_fit reports it
+  std::vector<int> fl(size_t(std::max(ran, 1)), 0);
+  std::vector<double> tr(size_t(iters), 0.0);
+  int final_flags = 0;
+  if (ran > 0) cudaMemcpyAsync(fl.data(), fhist, sizeof(int) * size_t(ran), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(tr.data(), trace_dev, sizeof(double) * size_t(iters), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&final_flags, s->flags, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(BS_ECUDA);
+  int stop = ran;
+  for (int it = 0; it < ran; ++it)
+    if (fl[size_t(it)] & BS_FLAG_NONFINITE) { stop = it; break; }
+  for (int it = 0; it < ran; ++it) final_flags |= fl[size_t(it)] & BS_FLAG_CLAMPED;
+  if (stop < ran) final_flags |= BS_FLAG_NONFINITE;
+  int nt = 0;
+  if (monitor) {
+    for (int it = 0, k = 0; it < stop; ++it)
+      if (trace_every && it % trace_every == 0) {
+        if (trace_out) trace_out[nt] = host_trace[size_t(k)];
+        ++nt;
+        ++k;
+      }
+  } else {
+    for (int it = 0; it < stop; ++it)
+      if (trace_every && it % trace_every == 0) {
+        if (trace_out) trace_out[nt] = tr[size_t(it)];
+        ++nt;
+      }
+  }
+  s->xb_fresh = s->fused && ran == iters && !(final_flags & BS_FLAG_NONFINITE);
+  if (ntrace_out) *ntrace_out = nt;
+  if (iters_run) *iters_run = stop;
+  if (flags_out) *flags_out = final_flags;
+  fail(BS_OK);
+  if (final_flags & BS_FLAG_NONFINITE) {
+    set_error("bs_cox_run: nonfinite risk weights at iteration %d; rescale X or lower sigma", stop);
+    return BS_ENUMERIC;
+  }
+  return BS_OK;
+}

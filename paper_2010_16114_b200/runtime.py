@@ -1,0 +1,86 @@
+"""Python handle on the solver-level C ABI (bs_ctx_* / bs_cox_*; include/bsb200.h).
+
+``Context(comm)`` creates the per-rank native context: its stream is the current
+torch stream, and for more than one rank an NCCL communicator whose unique id rank 0
+draws and ships over ``comm`` (one process per GPU, as under torchrun; NCCL does not
+put two ranks on one GPU, so in-process multi-rank worlds are refused).
+``cox_run(ctx, state, iters, ...)`` runs ``cox_fit``'s loop (solvers.py:422-450) inside
+the library on a ``CoxState`` made by ``cox_init`` and appends to ``state.trace`` like
+``cox_fit`` does.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+
+import numpy as np
+
+from . import _lib
+from .distarray import _flat_local
+from .solvers import NumericError, _cuts_ptr
+
+
+class Context:
+    def __init__(self, comm):
+        import torch
+
+        self.comm = comm
+        if comm.size > 1 and getattr(comm, "backend", None) == "inproc":
+            raise ValueError("the native runtime needs one process per GPU for more than one rank")
+        uid = np.zeros(16, dtype=np.int64)  # 128-byte ncclUniqueId
+        if comm.size > 1:
+            if comm.rank == 0:
+                _lib.call("bs_nccl_unique_id", uid.ctypes.data_as(C.c_void_p))
+            comm.broadcast(uid, root=0)
+        dev = comm.device.index if comm.device.index is not None else torch.cuda.current_device()
+        h = C.c_void_p()
+        _lib.call("bs_ctx_create", comm.rank, comm.size, dev, uid.ctypes.data_as(C.c_void_p) if comm.size > 1 else None,
+                  _lib.stream_ptr(), C.byref(h))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _lib.call("bs_ctx_destroy", self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
+
+def cox_run(ctx, state, iters, trace_every=1, monitor=None):
+    """``cox_fit(state, iters, monitor, trace_every)`` with the loop in native code."""
+    s = state
+    x = s.X
+    m, n_loc = x.shape[0], x.local.shape[1]
+    xcode = _lib.xcode(x)
+    code = _lib.dtype_code(s.beta.dtype)
+    h = C.c_void_p()
+    _lib.call("bs_cox_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, xcode, code, m, n_loc,
+              _lib.ptr(s.delta), _cuts_ptr(s), float(s.lam), float(s.sigma),
+              _lib.ptr(_flat_local(s.beta)) if n_loc else None, _lib.ptr(_flat_local(s.grad)) if n_loc else None,
+              C.byref(h))
+    try:
+        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+        trace = np.zeros(max(ntr, 1), dtype=np.float64)
+        nt, ran, flags = C.c_int(), C.c_int(), C.c_int()
+        window = monitor.window if monitor is not None else 0
+        tol = monitor.rel_tol if monitor is not None else 0.0
+        rc = _lib.load().bs_cox_run(h, int(iters), int(trace_every), int(window), float(tol),
+                                    trace.ctypes.data_as(C.c_void_p), C.byref(nt), C.byref(ran), C.byref(flags))
+        s.trace.extend(float(v) for v in trace[:nt.value])
+        if monitor is not None:
+            monitor.history.extend(float(v) for v in trace[:nt.value])
+        if flags.value & _lib.BS_FLAG_CLAMPED:
+            warnings.warn("linear predictor clamped before exponentiation", RuntimeWarning, stacklevel=2)
+        if rc == _lib.BS_ENUMERIC:
+            raise NumericError("nonfinite risk weights; rescale X or lower sigma")
+        if rc != _lib.BS_OK:
+            raise _lib.BsError("bs_cox_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
+    finally:
+        _lib.call("bs_cox_state_destroy", h)
+    return s

@@ -92,6 +92,26 @@ def main():
         tr.append(np.asarray(st.trace))
         ok &= check("cox packed/int8: nonzero coefficients", [min(np.count_nonzero(bs.gather_full(st.beta)), 1)], [1], 0)
     ok &= check("cox packed genotypes vs int8 trace", tr[0], tr[1], 2e-5)
+    # the solver-level C ABI (bs_ctx_create over NCCL + bs_cox_run) against cox_fit
+    from paper_2010_16114_b200 import runtime
+
+    for xs_, tol in ((xs, 1e-12), (xf, 1e-9)):
+        res = []
+        for native in (False, True):
+            xd_ = bs.distribute(xs_ if comm.rank == 0 else None, comm)
+            mm = xs_.shape[0]
+            dd = ds if xs_ is xs else df
+            yy = ys if xs_ is xs else yf
+            st = bs.cox_init(xd_, yy, dd, lam=1e-4, sigma=sig if xs_ is xs else sgf)
+            if native:
+                with runtime.Context(comm) as ctx:
+                    runtime.cox_run(ctx, st, 10)
+            else:
+                bs.cox_fit(st, 10)
+            res.append((np.asarray(st.trace), bs.gather_full(st.beta)))
+        name = np.dtype(xs_.dtype).name
+        ok &= check(f"native bs_cox_run {name} trace (NCCL)", res[1][0], res[0][0], tol)
+        ok &= check(f"native bs_cox_run {name} beta (NCCL)", res[1][1], res[0][1], tol * 1e3)
     comm.barrier()
     import torch.distributed as dist
 
