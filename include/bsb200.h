@@ -308,6 +308,20 @@ int bs_cox_run(bs_cox_t state, int iters, int trace_every, int monitor_window,
                double monitor_tol, double* trace_out, int* ntrace_out,
                int* iters_run, int* flags_out);
 
+/* NmfState (solvers.py:73-121) over the caller's X, Vt (r x m_loc, the rank's
+ * partition_of(m) block) and W (r x n_loc); the state owns WXt, the gathered Vt
+ * and the workspaces.  bs_nmf_run = nmf_multiplicative / nmf_apg (solvers.py:
+ * 144-185; algo BS_NMF_MU / BS_NMF_APG): trace_out receives the objective after
+ * every trace_every-th update; BS_EINVAL if X has a negative entry
+ * (solvers.py:139-141). */
+typedef struct bs_nmf* bs_nmf_t;
+int bs_nmf_state_create(bs_ctx_t ctx, const void* X, int dtype, int64_t m,
+                        int64_t n_loc, int r, double eps, void* Vt, void* W,
+                        bs_nmf_t* out);
+int bs_nmf_state_destroy(bs_nmf_t state);
+int bs_nmf_run(bs_nmf_t state, int algo, int iters, int trace_every,
+               double* trace_out, int* ntrace_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,9 @@ SIGNATURES = {
     "bs_cox_state_create": (_i, [_p, _p, _i, _i, _i64, _i64, _p, _p, _d, _d, _p, _p, _p]),
     "bs_cox_state_destroy": (_i, [_p]),
     "bs_cox_run": (_i, [_p, _i, _i, _i, _d, _p, _p, _p, _p]),
+    "bs_nmf_state_create": (_i, [_p, _p, _i, _i64, _i64, _i, _d, _p, _p, _p]),
+    "bs_nmf_state_destroy": (_i, [_p]),
+    "bs_nmf_run": (_i, [_p, _i, _i, _i, _p, _p]),
     "bs_genotype_pack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_unpack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_fill_packed": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),

@@ -30,6 +30,11 @@ struct NcclApi {
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
 };
 
 const NcclApi& nccl() {
@@ -43,7 +48,12 @@ const NcclApi& nccl() {
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(h, "ncclAllReduce"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString;
+    api.Reduce = reinterpret_cast<decltype(api.Reduce)>(dlsym(h, "ncclReduce"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(dlsym(h, "ncclBroadcast"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.GetErrorString &&
+             api.Reduce && api.Broadcast && api.GroupStart && api.GroupEnd;
   });
   return api;
 }
@@ -344,4 +354,217 @@ extern "C" int bs_cox_run(bs_cox_t s, int iters, int trace_every, int monitor_wi
     return BS_ENUMERIC;
   }
   return BS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NMF (solvers.py:73-185): nmf_multiplicative / nmf_apg as one native loop.  The
+// reduce-scatter of scn b (distlinalg.py:251-252) and the all-gather of Vt are NCCL
+// reduces / broadcasts per rank block inside one group, so uneven partition_of blocks
+// need no padding.
+// ---------------------------------------------------------------------------
+struct bs_nmf {
+  bs_ctx* ctx;
+  const void* X;
+  int dtype, r;
+  int64_t m, n_loc, m_loc, m_lo;
+  double eps;
+  void* Vt;  // r x m_loc (caller)
+  void* W;   // r x n_loc (caller)
+  void *WXt, *P, *tmp;  // owned: r x m_loc; r x m (size > 1); r x m (size > 1)
+  double *red, *scan, *VtV;
+  void *ws_gram, *ws_wxt, *ws_scan, *ws_vt, *ws_w;
+  int64_t n_gram, n_wxt, n_scan, n_vt, n_w;
+};
+
+namespace {
+
+void part_of(int64_t ext, int p, int q, int64_t* lo, int64_t* hi) {  // partition_of (distarray.py:55-65)
+  const int64_t base = ext / p, extra = ext % p;
+  *lo = q * base + std::min<int64_t>(q, extra);
+  *hi = *lo + base + (q < extra ? 1 : 0);
+}
+
+ncclDataType_t nccl_type(int dtype) { return dtype == BS_F64 ? ncclFloat64 : ncclFloat32; }
+
+int nmf_reduce_scatter(bs_nmf* s) {  // P (r x m) summed over ranks, block q -> rank q's WXt
+  bs_ctx* c = s->ctx;
+  const int64_t es = s->dtype == BS_F64 ? 8 : 4;
+  const NcclApi& api = nccl();
+  api.GroupStart();
+  for (int q = 0; q < c->size; ++q) {
+    int64_t lo, hi;
+    part_of(s->m, c->size, q, &lo, &hi);
+    if (hi == lo) continue;
+    const ncclResult_t r = api.Reduce(static_cast<char*>(s->P) + lo * s->r * es, s->WXt, size_t((hi - lo) * s->r),
+                                      nccl_type(s->dtype), ncclSum, q, c->comm, c->stream);
+    if (r != ncclSuccess) { api.GroupEnd(); return nccl_err("reduce-scatter", r); }
+  }
+  const ncclResult_t r = api.GroupEnd();
+  return r == ncclSuccess ? BS_OK : nccl_err("reduce-scatter", r);
+}
+
+int nmf_allgather(bs_nmf* s) {  // Vt blocks -> tmp (r x m)
+  bs_ctx* c = s->ctx;
+  const int64_t es = s->dtype == BS_F64 ? 8 : 4;
+  const NcclApi& api = nccl();
+  api.GroupStart();
+  for (int q = 0; q < c->size; ++q) {
+    int64_t lo, hi;
+    part_of(s->m, c->size, q, &lo, &hi);
+    if (hi == lo) continue;
+    const ncclResult_t r = api.Broadcast(s->Vt, static_cast<char*>(s->tmp) + lo * s->r * es, size_t((hi - lo) * s->r),
+                                         nccl_type(s->dtype), q, c->comm, c->stream);
+    if (r != ncclSuccess) { api.GroupEnd(); return nccl_err("all-gather", r); }
+  }
+  const ncclResult_t r = api.GroupEnd();
+  return r == ncclSuccess ? BS_OK : nccl_err("all-gather", r);
+}
+
+int allreduce_f64(bs_ctx* c, double* buf, int64_t count, ncclRedOp_t op) {
+  if (c->size <= 1 || count == 0) return BS_OK;
+  const ncclResult_t r = nccl().AllReduce(buf, buf, size_t(count), ncclFloat64, op, c->comm, c->stream);
+  return r == ncclSuccess ? BS_OK : nccl_err("allreduce", r);
+}
+
+}  // namespace
+
+extern "C" int bs_nmf_state_create(bs_ctx_t ctx, const void* X, int dtype, int64_t m, int64_t n_loc, int r,
+                                   double eps, void* Vt, void* W, bs_nmf_t* out) {
+  clear_error();
+  if (!ctx || !out || m < 1 || n_loc < 0 || r < 1 || (dtype != BS_F32 && dtype != BS_F64) ||
+      (ctx->size == 1 && !Vt) || (n_loc > 0 && (!X || !W))) {
+    set_error("bs_nmf_state_create: bad arguments");
+    return BS_EINVAL;
+  }
+  *out = nullptr;
+  cudaSetDevice(ctx->device);
+  bs_nmf* s = new bs_nmf();
+  s->ctx = ctx;
+  s->X = X;
+  s->dtype = dtype;
+  s->r = r;
+  s->m = m;
+  s->n_loc = n_loc;
+  s->eps = eps;
+  s->Vt = Vt;
+  s->W = W;
+  int64_t hi;
+  part_of(m, ctx->size, ctx->rank, &s->m_lo, &hi);
+  s->m_loc = hi - s->m_lo;
+  const int64_t es = dtype == BS_F64 ? 8 : 4;
+  s->n_gram = std::max<int64_t>(bs_gram_workspace(r, n_loc), 256);
+  s->n_wxt = std::max<int64_t>(bs_nmf_wxt_workspace(dtype, m, n_loc, r), 256);
+  s->n_scan = std::max<int64_t>(bs_nmf_wxt_scan_workspace(dtype, m, n_loc, r), 256);
+  s->n_vt = std::max<int64_t>(bs_nmf_vt_step_workspace(r, s->m_loc), 256);
+  s->n_w = std::max<int64_t>(bs_nmf_w_step_workspace(dtype, m, n_loc, r), 256);
+  int rc = BS_OK;
+  void* p = nullptr;
+  rc |= dalloc(&s->WXt, es * r * std::max<int64_t>(s->m_loc, 1));
+  if (ctx->size > 1) {
+    rc |= dalloc(&s->P, es * r * m);
+    rc |= dalloc(&s->tmp, es * r * m);
+  } else {
+    s->P = s->WXt;  // one rank: scn b lands in WXt, Vt is the full factor
+    s->tmp = Vt;
+  }
+  rc |= dalloc(&p, 8 * (int64_t(r) * r + 1)); s->red = static_cast<double*>(p);
+  rc |= dalloc(&p, 16); s->scan = static_cast<double*>(p);
+  rc |= dalloc(&p, 8 * int64_t(r) * r); s->VtV = static_cast<double*>(p);
+  rc |= dalloc(&s->ws_gram, s->n_gram);
+  rc |= dalloc(&s->ws_wxt, s->n_wxt);
+  rc |= dalloc(&s->ws_scan, s->n_scan);
+  rc |= dalloc(&s->ws_vt, s->n_vt);
+  rc |= dalloc(&s->ws_w, s->n_w);
+  if (rc != BS_OK) {
+    bs_nmf_state_destroy(s);
+    set_error("bs_nmf_state_create: device allocation failed");
+    return BS_ECUDA;
+  }
+  *out = s;
+  return BS_OK;
+}
+
+extern "C" int bs_nmf_state_destroy(bs_nmf_t s) {
+  clear_error();
+  if (!s) return BS_OK;
+  cudaSetDevice(s->ctx->device);
+  void* bufs[] = {s->WXt, s->red, s->scan, s->VtV, s->ws_gram, s->ws_wxt, s->ws_scan, s->ws_vt, s->ws_w};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (s->ctx->size > 1) {
+    if (s->P) cudaFree(s->P);
+    if (s->tmp) cudaFree(s->tmp);
+  }
+  delete s;
+  return BS_OK;
+}
+
+extern "C" int bs_nmf_run(bs_nmf_t s, int algo, int iters, int trace_every, double* trace_out, int* ntrace_out) {
+  clear_error();
+  if (!s || iters < 0 || trace_every < 0 || (algo != BS_NMF_MU && algo != BS_NMF_APG)) {
+    set_error("bs_nmf_run: bad arguments");
+    return BS_EINVAL;
+  }
+  bs_ctx* c = s->ctx;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  if (ntrace_out) *ntrace_out = 0;
+  if (iters == 0) return BS_OK;
+  const int r = s->r;
+  const int64_t rr = int64_t(r) * r;
+  double* trace_dev = nullptr;
+  if (cudaMalloc(&trace_dev, sizeof(double) * size_t(iters)) != cudaSuccess) {
+    set_error("bs_nmf_run: device allocation failed");
+    return BS_ECUDA;
+  }
+  auto done = [&](int code) {
+    cudaFree(trace_dev);
+    return code;
+  };
+  int rc;
+  // WWt of the entering W (scn d, solvers.py:151)
+  if ((rc = bs_gram(s->W, s->dtype, r, s->n_loc, s->red, s->ws_gram, s->n_gram, st))) return done(rc);
+  if ((rc = allreduce_f64(c, s->red, rr, ncclSum))) return done(rc);
+  for (int it = 0; it < iters; ++it) {
+    if (it == 0) {  // scn b with the call's _nmf_check and ||X||^2 (solvers.py:139-141, 147)
+      if ((rc = bs_nmf_wxt_scan(s->X, s->W, s->dtype, s->m, s->n_loc, r, s->P, s->scan, s->ws_scan, s->n_scan, st)))
+        return done(rc);
+      if ((rc = allreduce_f64(c, s->scan, 1, ncclMin)) || (rc = allreduce_f64(c, s->scan + 1, 1, ncclSum)))
+        return done(rc);
+      double mn = 0.0;
+      cudaMemcpyAsync(&mn, s->scan, sizeof(double), cudaMemcpyDeviceToHost, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) return done(BS_ECUDA);
+      if (!(s->n_loc == 0 && c->size == 1) && mn < 0) {
+        set_error("NMF requires nonnegative data");
+        return done(BS_EINVAL);
+      }
+    } else if ((rc = bs_nmf_wxt(s->X, s->W, s->dtype, s->m, s->n_loc, r, s->P, s->ws_wxt, s->n_wxt, st))) {
+      return done(rc);
+    }
+    if (c->size > 1 && (rc = nmf_reduce_scatter(s))) return done(rc);
+    // Vt half-step (solvers.py:152-156 / 173-176)
+    if ((rc = bs_nmf_vt_step(algo, s->Vt, s->WXt, s->red, s->dtype, r, s->m_loc, s->eps, s->VtV, nullptr, s->ws_vt,
+                             s->n_vt, st)))
+      return done(rc);
+    if (c->size > 1 && ((rc = allreduce_f64(c, s->VtV, rr, ncclSum)) || (rc = nmf_allgather(s)))) return done(rc);
+    // W half-step + next WWt + objective cross term (solvers.py:155-159 / 177-182)
+    if ((rc = bs_nmf_w_step(algo, s->X, s->tmp, s->W, s->VtV, s->dtype, s->m, s->n_loc, r, s->eps, s->red, s->ws_w,
+                            s->n_w, st)))
+      return done(rc);
+    if ((rc = allreduce_f64(c, s->red, rr + 1, ncclSum))) return done(rc);
+    if (trace_every && it % trace_every == 0 &&
+        (rc = bs_nmf_objective(s->scan + 1, s->red, s->VtV, r, trace_dev + it, st)))
+      return done(rc);
+  }
+  std::vector<double> tr(size_t(iters), 0.0);
+  cudaMemcpyAsync(tr.data(), trace_dev, sizeof(double) * size_t(iters), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return done(BS_ECUDA);
+  int nt = 0;
+  for (int it = 0; it < iters; ++it)
+    if (trace_every && it % trace_every == 0) {
+      if (trace_out) trace_out[nt] = tr[size_t(it)];
+      ++nt;
+    }
+  if (ntrace_out) *ntrace_out = nt;
+  return done(BS_OK);
 }

@@ -6,7 +6,8 @@ draws and ships over ``comm`` (one process per GPU, as under torchrun; NCCL does
 put two ranks on one GPU, so in-process multi-rank worlds are refused).
 ``cox_run(ctx, state, iters, ...)`` runs ``cox_fit``'s loop (solvers.py:422-450) inside
 the library on a ``CoxState`` made by ``cox_init`` and appends to ``state.trace`` like
-``cox_fit`` does.
+``cox_fit`` does; ``nmf_run(ctx, state, iters, algo)`` does the same for
+``nmf_multiplicative`` / ``nmf_apg`` (solvers.py:144-185) on an ``NmfState``.
 """
 
 from __future__ import annotations
@@ -83,4 +84,32 @@ def cox_run(ctx, state, iters, trace_every=1, monitor=None):
             raise _lib.BsError("bs_cox_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
     finally:
         _lib.call("bs_cox_state_destroy", h)
+    return s
+
+
+def nmf_run(ctx, state, iters, algo="apg", trace_every=1):
+    """``nmf_apg`` / ``nmf_multiplicative(state, iters, trace_every)`` with the loop in native code."""
+    s = state
+    x = s.X
+    m, n_loc = x.shape[0], x.local.shape[1]
+    r = s.Vt.shape[0]
+    code = _lib.dtype_code(x.dtype)
+    a = _lib.BS_NMF_APG if algo == "apg" else _lib.BS_NMF_MU
+    vt = _flat_local(s.Vt)
+    h = C.c_void_p()
+    _lib.call("bs_nmf_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, code, m, n_loc, r,
+              float(s.eps), _lib.ptr(vt) if vt.numel() else None, _lib.ptr(_flat_local(s.W)) if n_loc else None,
+              C.byref(h))
+    try:
+        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+        trace = np.zeros(max(ntr, 1), dtype=np.float64)
+        nt = C.c_int()
+        rc = _lib.load().bs_nmf_run(h, a, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
+        if rc == _lib.BS_EINVAL:
+            raise ValueError(_lib.load().bs_last_error().decode(errors="replace"))
+        if rc != _lib.BS_OK:
+            raise _lib.BsError("bs_nmf_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
+        s.trace.extend(float(v) for v in trace[:nt.value])
+    finally:
+        _lib.call("bs_nmf_state_destroy", h)
     return s

@@ -112,6 +112,20 @@ def main():
         name = np.dtype(xs_.dtype).name
         ok &= check(f"native bs_cox_run {name} trace (NCCL)", res[1][0], res[0][0], tol)
         ok &= check(f"native bs_cox_run {name} beta (NCCL)", res[1][1], res[0][1], tol * 1e3)
+    # bs_nmf_run: grouped NCCL reduces / broadcasts for the uneven blocks (m = 301 over 2 ranks)
+    for dt, tol in ((np.float64, 1e-12), (np.float32, 1e-5)):
+        xn = orc.rand_fill_common((301, 200), 5, dt)
+        res = []
+        for native in (False, True):
+            st = bs.nmf_init(bs.distribute(xn if comm.rank == 0 else None, comm), 6, seed=6)
+            if native:
+                with runtime.Context(comm) as ctx:
+                    runtime.nmf_run(ctx, st, 8, algo="apg")
+            else:
+                bs.nmf_apg(st, 8)
+            res.append((np.asarray(st.trace), bs.gather_full(st.W)))
+        ok &= check(f"native bs_nmf_run {np.dtype(dt).name} trace (NCCL)", res[1][0], res[0][0], tol)
+        ok &= check(f"native bs_nmf_run {np.dtype(dt).name} W (NCCL)", res[1][1], res[0][1], tol * 10)
     comm.barrier()
     import torch.distributed as dist
 

@@ -83,3 +83,43 @@ def test_native_cox_run_monitor_and_numeric_error():
         return True
 
     assert bs.run_inproc(1, bad)[0]
+
+
+@pytest.mark.parametrize("algo", ["mu", "apg"])
+@pytest.mark.parametrize("dt,m,n,r", [(np.float64, 300, 200, 7), (np.float32, 2048, 1500, 20)])
+def test_native_nmf_run_matches_python_loop(algo, dt, m, n, r):
+    x = orc.rand_fill_common((m, n), 3, dt)
+
+    def fn(comm, native):
+        xd = _dist(comm, x)
+        st = bs.nmf_init(xd, r, seed=4)
+        if native:
+            with runtime.Context(comm) as ctx:
+                runtime.nmf_run(ctx, st, 5, algo=algo)
+                runtime.nmf_run(ctx, st, 4, algo=algo, trace_every=2)
+        else:
+            fit = bs.nmf_apg if algo == "apg" else bs.nmf_multiplicative
+            fit(st, 5)
+            fit(st, 4, trace_every=2)
+        return np.asarray(st.trace), bs.gather_full(st.Vt), bs.gather_full(st.W)
+
+    py = bs.run_inproc(1, fn, False)[0]
+    nat = bs.run_inproc(1, fn, True)[0]
+    assert len(nat[0]) == len(py[0]) == 7
+    for a, b in zip(nat, py):
+        np.testing.assert_array_equal(a, b)  # same kernels, same order, one rank
+
+
+def test_native_nmf_rejects_negative_data():
+    x = orc.rand_fill_common((64, 40), 3, np.float64)
+    x[5, 7] = -1.0
+
+    def fn(comm):
+        st = bs.nmf_init(_dist(comm, np.abs(x)), 3, seed=4)
+        st.X.local[5, 7] = -1.0
+        with runtime.Context(comm) as ctx:
+            with pytest.raises(ValueError):
+                runtime.nmf_run(ctx, st, 2)
+        return True
+
+    assert bs.run_inproc(1, fn)[0]
