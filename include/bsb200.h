@@ -40,6 +40,7 @@ extern "C" {
 #define BS_EWORK 3    /* workspace too small                                   */
 #define BS_ENUMERIC 4 /* nonfinite risk weights (NumericError, solvers.py:388-389) */
 #define BS_ENCCL 5    /* NCCL missing or failed                                  */
+#define BS_EDEGEN 6   /* coincident embedding points (DegenerateConfigError)     */
 
 /* dtype codes (comm.py:68-72; int8 added) */
 #define BS_F32 0
@@ -321,6 +322,19 @@ int bs_nmf_state_create(bs_ctx_t ctx, const void* X, int dtype, int64_t m,
 int bs_nmf_state_destroy(bs_nmf_t state);
 int bs_nmf_run(bs_nmf_t state, int algo, int iters, int trace_every,
                double* trace_out, int* ntrace_out);
+
+/* MdsState (solvers.py:193-234) over the caller's Y (n x n_loc) and theta
+ * (q x n_loc); bs_mds_run = mds_fit (solvers.py:269-305): trace_out receives the
+ * stress of the iterate entering every trace_every-th update; BS_EDEGEN when a
+ * zero off-diagonal distance appears without perturb (traces up to that
+ * iteration are returned). */
+typedef struct bs_mds* bs_mds_t;
+int bs_mds_state_create(bs_ctx_t ctx, const void* Y, int dtype, int64_t n,
+                        int64_t n_loc, int q, int perturb, void* theta,
+                        bs_mds_t* out);
+int bs_mds_state_destroy(bs_mds_t state);
+int bs_mds_run(bs_mds_t state, int iters, int trace_every, double* trace_out,
+               int* ntrace_out);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("BS_LIB_PATH", str(PKG / "libbsb200.so")))
 HEADER = PKG.parent / "include" / "bsb200.h"
 
 # status codes (bsb200.h)
-BS_OK, BS_EINVAL, BS_ECUDA, BS_EWORK, BS_ENUMERIC, BS_ENCCL = 0, 1, 2, 3, 4, 5
+BS_OK, BS_EINVAL, BS_ECUDA, BS_EWORK, BS_ENUMERIC, BS_ENCCL, BS_EDEGEN = 0, 1, 2, 3, 4, 5, 6
 # dtype codes (comm.py:68-72 + int8)
 BS_F32, BS_F64, BS_I64, BS_I8, BS_U2 = 0, 1, 2, 3, 4
 # ReduceOp codes (comm.py:54-58 order)
@@ -52,6 +52,9 @@ SIGNATURES = {
     "bs_nmf_state_create": (_i, [_p, _p, _i, _i64, _i64, _i, _d, _p, _p, _p]),
     "bs_nmf_state_destroy": (_i, [_p]),
     "bs_nmf_run": (_i, [_p, _i, _i, _i, _p, _p]),
+    "bs_mds_state_create": (_i, [_p, _p, _i, _i64, _i64, _i, _i, _p, _p]),
+    "bs_mds_state_destroy": (_i, [_p]),
+    "bs_mds_run": (_i, [_p, _i, _i, _p, _p]),
     "bs_genotype_pack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_unpack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_fill_packed": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),

@@ -568,3 +568,148 @@ extern "C" int bs_nmf_run(bs_nmf_t s, int algo, int iters, int trace_every, doub
   if (ntrace_out) *ntrace_out = nt;
   return done(BS_OK);
 }
+
+// ---------------------------------------------------------------------------
+// MDS (solvers.py:188-305): mds_fit as one native loop; theta is all-gathered with
+// grouped NCCL broadcasts per rank block.
+// ---------------------------------------------------------------------------
+struct bs_mds {
+  bs_ctx* ctx;
+  const void* Y;
+  int dtype, q, perturb;
+  int64_t n, lo, n_loc;
+  double wsum;
+  void* theta;                 // q x n_loc (caller)
+  void *full, *zsum, *T;       // owned: q x n (size > 1), n_loc, q x n_loc
+  double* red;
+  int* flags;
+  void* ws;
+  int64_t n_ws;
+};
+
+extern "C" int bs_mds_state_create(bs_ctx_t ctx, const void* Y, int dtype, int64_t n, int64_t n_loc, int q,
+                                   int perturb, void* theta, bs_mds_t* out) {
+  clear_error();
+  if (!ctx || !out || n < 2 || n_loc < 0 || q < 1 || (dtype != BS_F32 && dtype != BS_F64) ||
+      (n_loc > 0 && (!Y || !theta))) {
+    set_error("bs_mds_state_create: bad arguments");
+    return BS_EINVAL;
+  }
+  *out = nullptr;
+  cudaSetDevice(ctx->device);
+  bs_mds* s = new bs_mds();
+  s->ctx = ctx;
+  s->Y = Y;
+  s->dtype = dtype;
+  s->q = q;
+  s->perturb = perturb ? 1 : 0;
+  s->n = n;
+  s->n_loc = n_loc;
+  s->wsum = double(n - 1);  // W_sums (solvers.py:231)
+  s->theta = theta;
+  int64_t hi;
+  part_of(n, ctx->size, ctx->rank, &s->lo, &hi);
+  if (hi - s->lo != n_loc) {
+    delete s;
+    set_error("bs_mds_state_create: n_loc %lld is not this rank's partition_of(n) block", (long long)n_loc);
+    return BS_EINVAL;
+  }
+  const int64_t es = dtype == BS_F64 ? 8 : 4;
+  s->n_ws = std::max<int64_t>(bs_mds_pass_workspace(dtype, n, n_loc, q), 256);
+  int rc = BS_OK;
+  void* p = nullptr;
+  if (ctx->size > 1) rc |= dalloc(&s->full, es * q * n);
+  else s->full = theta;
+  rc |= dalloc(&s->zsum, es * std::max<int64_t>(n_loc, 1));
+  rc |= dalloc(&s->T, es * q * std::max<int64_t>(n_loc, 1));
+  rc |= dalloc(&p, 16); s->red = static_cast<double*>(p);
+  rc |= dalloc(&p, 4); s->flags = static_cast<int*>(p);
+  rc |= dalloc(&s->ws, s->n_ws);
+  if (rc != BS_OK) {
+    bs_mds_state_destroy(s);
+    set_error("bs_mds_state_create: device allocation failed");
+    return BS_ECUDA;
+  }
+  *out = s;
+  return BS_OK;
+}
+
+extern "C" int bs_mds_state_destroy(bs_mds_t s) {
+  clear_error();
+  if (!s) return BS_OK;
+  cudaSetDevice(s->ctx->device);
+  if (s->ctx->size > 1 && s->full) cudaFree(s->full);
+  void* bufs[] = {s->zsum, s->T, s->red, s->flags, s->ws};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete s;
+  return BS_OK;
+}
+
+extern "C" int bs_mds_run(bs_mds_t s, int iters, int trace_every, double* trace_out, int* ntrace_out) {
+  clear_error();
+  if (!s || iters < 0 || trace_every < 0) { set_error("bs_mds_run: bad arguments"); return BS_EINVAL; }
+  bs_ctx* c = s->ctx;
+  cudaSetDevice(c->device);
+  cudaStream_t st = c->stream;
+  if (ntrace_out) *ntrace_out = 0;
+  if (iters == 0) return BS_OK;
+  const int64_t es = s->dtype == BS_F64 ? 8 : 4;
+  double* hist = nullptr;
+  if (cudaMalloc(&hist, sizeof(double) * 2 * size_t(iters)) != cudaSuccess) {
+    set_error("bs_mds_run: device allocation failed");
+    return BS_ECUDA;
+  }
+  auto done = [&](int code) {
+    cudaFree(hist);
+    return code;
+  };
+  if (cudaMemsetAsync(s->flags, 0, sizeof(int), st) != cudaSuccess) return done(BS_ECUDA);
+  int rc;
+  for (int it = 0; it < iters; ++it) {
+    if (c->size > 1) {  // all-gather theta (solvers.py:272, _theta_full)
+      const NcclApi& api = nccl();
+      api.GroupStart();
+      for (int qr = 0; qr < c->size; ++qr) {
+        int64_t lo, hi;
+        part_of(s->n, c->size, qr, &lo, &hi);
+        if (hi == lo) continue;
+        const ncclResult_t r = api.Broadcast(s->theta, static_cast<char*>(s->full) + lo * s->q * es,
+                                             size_t((hi - lo) * s->q), nccl_type(s->dtype), qr, c->comm, st);
+        if (r != ncclSuccess) { api.GroupEnd(); return done(nccl_err("all-gather", r)); }
+      }
+      const ncclResult_t r = api.GroupEnd();
+      if (r != ncclSuccess) return done(nccl_err("all-gather", r));
+    }
+    if ((rc = bs_mds_pass(s->Y, s->full, s->dtype, s->n, s->lo, s->n_loc, s->q, s->perturb, 0, s->red, s->zsum, s->T,
+                          s->ws, s->n_ws, st)))
+      return done(rc);
+    if ((rc = allreduce_f64(c, s->red, 2, ncclSum))) return done(rc);
+    cudaMemcpyAsync(hist + 2 * it, s->red, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st);
+    if ((rc = bs_mds_update(s->theta, s->zsum, s->T, s->dtype, s->q, s->n_loc, s->wsum, s->red, s->perturb, s->flags,
+                            st)))
+      return done(rc);
+  }
+  std::vector<double> h(2 * size_t(iters));
+  int fl = 0;
+  cudaMemcpyAsync(h.data(), hist, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&fl, s->flags, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return done(BS_ECUDA);
+  int last = iters;
+  const bool failed = fl & BS_FLAG_DEGENERATE;
+  if (failed)
+    for (int it = 0; it < iters; ++it)
+      if (h[2 * size_t(it) + 1] > 0) { last = it + 1; break; }
+  int nt = 0;
+  for (int it = 0; it < last; ++it)
+    if (trace_every && it % trace_every == 0) {
+      if (trace_out) trace_out[nt] = h[2 * size_t(it)];
+      ++nt;
+    }
+  if (ntrace_out) *ntrace_out = nt;
+  if (failed) {
+    set_error("coincident embedding points; rerun with perturb=True");
+    return done(BS_EDEGEN);
+  }
+  return done(BS_OK);
+}

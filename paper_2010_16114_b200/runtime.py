@@ -7,7 +7,8 @@ put two ranks on one GPU, so in-process multi-rank worlds are refused).
 ``cox_run(ctx, state, iters, ...)`` runs ``cox_fit``'s loop (solvers.py:422-450) inside
 the library on a ``CoxState`` made by ``cox_init`` and appends to ``state.trace`` like
 ``cox_fit`` does; ``nmf_run(ctx, state, iters, algo)`` does the same for
-``nmf_multiplicative`` / ``nmf_apg`` (solvers.py:144-185) on an ``NmfState``.
+``nmf_multiplicative`` / ``nmf_apg`` (solvers.py:144-185) on an ``NmfState`` and
+``mds_run`` for ``mds_fit`` (solvers.py:269-305) on an ``MdsState``.
 """
 
 from __future__ import annotations
@@ -19,7 +20,7 @@ import numpy as np
 
 from . import _lib
 from .distarray import _flat_local
-from .solvers import NumericError, _cuts_ptr
+from .solvers import DegenerateConfigError, NumericError, _cuts_ptr
 
 
 class Context:
@@ -112,4 +113,29 @@ def nmf_run(ctx, state, iters, algo="apg", trace_every=1):
         s.trace.extend(float(v) for v in trace[:nt.value])
     finally:
         _lib.call("bs_nmf_state_destroy", h)
+    return s
+
+
+def mds_run(ctx, state, iters, trace_every=1):
+    """``mds_fit(state, iters, trace_every)`` with the loop in native code."""
+    s = state
+    y = s.Y
+    n, n_loc = y.shape[0], y.local.shape[1]
+    q = s.theta.shape[0]
+    code = _lib.dtype_code(y.dtype)
+    h = C.c_void_p()
+    _lib.call("bs_mds_state_create", ctx.handle, _lib.ptr(_flat_local(y)) if n_loc else None, code, n, n_loc, q,
+              1 if s.perturb else 0, _lib.ptr(_flat_local(s.theta)) if n_loc else None, C.byref(h))
+    try:
+        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+        trace = np.zeros(max(ntr, 1), dtype=np.float64)
+        nt = C.c_int()
+        rc = _lib.load().bs_mds_run(h, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
+        s.trace.extend(float(v) for v in trace[:nt.value])
+        if rc == _lib.BS_EDEGEN:
+            raise DegenerateConfigError("coincident embedding points; rerun with perturb=True")
+        if rc != _lib.BS_OK:
+            raise _lib.BsError("bs_mds_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
+    finally:
+        _lib.call("bs_mds_state_destroy", h)
     return s

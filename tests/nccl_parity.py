@@ -126,6 +126,18 @@ def main():
             res.append((np.asarray(st.trace), bs.gather_full(st.W)))
         ok &= check(f"native bs_nmf_run {np.dtype(dt).name} trace (NCCL)", res[1][0], res[0][0], tol)
         ok &= check(f"native bs_nmf_run {np.dtype(dt).name} W (NCCL)", res[1][1], res[0][1], tol * 10)
+    # bs_mds_run: theta all-gather by grouped broadcasts (n = 301 over 2 ranks)
+    res = []
+    for native in (False, True):
+        st = bs.mds_init(yd, 3, seed=8)
+        if native:
+            with runtime.Context(comm) as ctx:
+                runtime.mds_run(ctx, st, 12)
+        else:
+            bs.mds_fit(st, 12)
+        res.append((np.asarray(st.trace), bs.gather_full(st.theta)))
+    ok &= check("native bs_mds_run trace (NCCL)", res[1][0], res[0][0], 1e-12)
+    ok &= check("native bs_mds_run theta (NCCL)", res[1][1], res[0][1], 1e-11)
     comm.barrier()
     import torch.distributed as dist
 

@@ -123,3 +123,50 @@ def test_native_nmf_rejects_negative_data():
         return True
 
     assert bs.run_inproc(1, fn)[0]
+
+
+@pytest.mark.parametrize("dt,n,q", [(np.float64, 200, 3), (np.float32, 516, 8)])
+def test_native_mds_run_matches_mds_fit(dt, n, q):
+    x = orc.rand_fill_common((6, n), 9, dt)
+    y = orc.pairwise_euclidean(x).astype(dt)
+
+    def fn(comm, native):
+        st = bs.mds_init(_dist(comm, y), q, seed=10)
+        if native:
+            with runtime.Context(comm) as ctx:
+                runtime.mds_run(ctx, st, 5)
+                runtime.mds_run(ctx, st, 4, trace_every=2)
+        else:
+            bs.mds_fit(st, 5)
+            bs.mds_fit(st, 4, trace_every=2)
+        return np.asarray(st.trace), bs.gather_full(st.theta)
+
+    py = bs.run_inproc(1, fn, False)[0]
+    nat = bs.run_inproc(1, fn, True)[0]
+    assert len(nat[0]) == len(py[0]) == 7
+    np.testing.assert_array_equal(nat[0], py[0])
+    np.testing.assert_array_equal(nat[1], py[1])
+
+
+def test_native_mds_degenerate_raises():
+    pts = np.zeros((2, 6))
+    pts[:, 1] = pts[:, 0] = 0.5  # points 0 and 1 coincide
+    pts[:, 2:] = np.arange(8, dtype=np.float64).reshape(2, 4)
+    y = orc.pairwise_euclidean(pts)
+    y[0, 1] = y[1, 0] = 1.0  # target distance nonzero, embedding distance zero
+
+    def fn(comm, native):
+        st = bs.mds_init(_dist(comm, y), 2, seed=1)
+        st.theta.local[:, 1] = st.theta.local[:, 0]
+        with pytest.raises(bs.DegenerateConfigError):
+            if native:
+                with runtime.Context(comm) as ctx:
+                    runtime.mds_run(ctx, st, 3)
+            else:
+                bs.mds_fit(st, 3)
+        return np.asarray(st.trace)
+
+    py = bs.run_inproc(1, fn, False)[0]
+    nat = bs.run_inproc(1, fn, True)[0]
+    assert 1 <= len(py) < 3
+    np.testing.assert_array_equal(nat, py)
