@@ -40,8 +40,36 @@ class Context:
         _lib.call("bs_ctx_create", comm.rank, comm.size, dev, uid.ctypes.data_as(C.c_void_p) if comm.size > 1 else None,
                   _lib.stream_ptr(), C.byref(h))
         self.handle = h
+        self._states = []  # (python state, destroy fn name, handle): native states cached per solver state
+
+    def _native(self, state, kind, create, tensors):
+        """The native state for ``state``, created on first use and kept until close().
+
+        It holds raw pointers to ``tensors`` (and, for Cox, a cached X beta for the
+        current beta), so it is rebuilt when any of them was replaced or written by
+        torch since the last call (storage pointer or in-place version changed)."""
+        key = ("native", kind, id(self))
+        sig = tuple((t.data_ptr(), t._version) for t in tensors)
+        entry = state._dev.get(key)
+        if entry is not None and entry[1] != sig:
+            self._drop(state, key)
+            entry = None
+        if entry is None:
+            entry = (create(), sig, f"bs_{kind}_state_destroy")
+            state._dev[key] = entry
+            self._states.append((state, key))
+        return entry[0]
+
+    def _drop(self, state, key):
+        entry = state._dev.pop(key, None)
+        if entry is not None:
+            _lib.call(entry[2], entry[0])
+        self._states = [(s, k) for s, k in self._states if not (s is state and k == key)]
 
     def close(self):
+        for state, key in list(self._states):
+            self._drop(state, key)
+        self._states = []
         if self.handle:
             _lib.call("bs_ctx_destroy", self.handle)
             self.handle = None
@@ -61,30 +89,31 @@ def cox_run(ctx, state, iters, trace_every=1, monitor=None):
     m, n_loc = x.shape[0], x.local.shape[1]
     xcode = _lib.xcode(x)
     code = _lib.dtype_code(s.beta.dtype)
-    h = C.c_void_p()
-    _lib.call("bs_cox_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, xcode, code, m, n_loc,
-              _lib.ptr(s.delta), _cuts_ptr(s), float(s.lam), float(s.sigma),
-              _lib.ptr(_flat_local(s.beta)) if n_loc else None, _lib.ptr(_flat_local(s.grad)) if n_loc else None,
-              C.byref(h))
-    try:
-        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
-        trace = np.zeros(max(ntr, 1), dtype=np.float64)
-        nt, ran, flags = C.c_int(), C.c_int(), C.c_int()
-        window = monitor.window if monitor is not None else 0
-        tol = monitor.rel_tol if monitor is not None else 0.0
-        rc = _lib.load().bs_cox_run(h, int(iters), int(trace_every), int(window), float(tol),
-                                    trace.ctypes.data_as(C.c_void_p), C.byref(nt), C.byref(ran), C.byref(flags))
-        s.trace.extend(float(v) for v in trace[:nt.value])
-        if monitor is not None:
-            monitor.history.extend(float(v) for v in trace[:nt.value])
-        if flags.value & _lib.BS_FLAG_CLAMPED:
-            warnings.warn("linear predictor clamped before exponentiation", RuntimeWarning, stacklevel=2)
-        if rc == _lib.BS_ENUMERIC:
-            raise NumericError("nonfinite risk weights; rescale X or lower sigma")
-        if rc != _lib.BS_OK:
-            raise _lib.BsError("bs_cox_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
-    finally:
-        _lib.call("bs_cox_state_destroy", h)
+    def create():
+        h = C.c_void_p()
+        _lib.call("bs_cox_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, xcode, code, m,
+                  n_loc, _lib.ptr(s.delta), _cuts_ptr(s), float(s.lam), float(s.sigma),
+                  _lib.ptr(_flat_local(s.beta)) if n_loc else None, _lib.ptr(_flat_local(s.grad)) if n_loc else None,
+                  C.byref(h))
+        return h
+
+    h = ctx._native(s, "cox", create, [x.local, s.beta.local, s.grad.local, s.delta])
+    ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+    trace = np.zeros(max(ntr, 1), dtype=np.float64)
+    nt, ran, flags = C.c_int(), C.c_int(), C.c_int()
+    window = monitor.window if monitor is not None else 0
+    tol = monitor.rel_tol if monitor is not None else 0.0
+    rc = _lib.load().bs_cox_run(h, int(iters), int(trace_every), int(window), float(tol),
+                                trace.ctypes.data_as(C.c_void_p), C.byref(nt), C.byref(ran), C.byref(flags))
+    s.trace.extend(float(v) for v in trace[:nt.value])
+    if monitor is not None:
+        monitor.history.extend(float(v) for v in trace[:nt.value])
+    if flags.value & _lib.BS_FLAG_CLAMPED:
+        warnings.warn("linear predictor clamped before exponentiation", RuntimeWarning, stacklevel=2)
+    if rc == _lib.BS_ENUMERIC:
+        raise NumericError("nonfinite risk weights; rescale X or lower sigma")
+    if rc != _lib.BS_OK:
+        raise _lib.BsError("bs_cox_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
     return s
 
 
@@ -97,22 +126,24 @@ def nmf_run(ctx, state, iters, algo="apg", trace_every=1):
     code = _lib.dtype_code(x.dtype)
     a = _lib.BS_NMF_APG if algo == "apg" else _lib.BS_NMF_MU
     vt = _flat_local(s.Vt)
-    h = C.c_void_p()
-    _lib.call("bs_nmf_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, code, m, n_loc, r,
-              float(s.eps), _lib.ptr(vt) if vt.numel() else None, _lib.ptr(_flat_local(s.W)) if n_loc else None,
-              C.byref(h))
-    try:
-        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
-        trace = np.zeros(max(ntr, 1), dtype=np.float64)
-        nt = C.c_int()
-        rc = _lib.load().bs_nmf_run(h, a, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
-        if rc == _lib.BS_EINVAL:
-            raise ValueError(_lib.load().bs_last_error().decode(errors="replace"))
-        if rc != _lib.BS_OK:
-            raise _lib.BsError("bs_nmf_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
-        s.trace.extend(float(v) for v in trace[:nt.value])
-    finally:
-        _lib.call("bs_nmf_state_destroy", h)
+
+    def create():
+        h = C.c_void_p()
+        _lib.call("bs_nmf_state_create", ctx.handle, _lib.ptr(_flat_local(x)) if n_loc else None, code, m, n_loc, r,
+                  float(s.eps), _lib.ptr(vt) if vt.numel() else None, _lib.ptr(_flat_local(s.W)) if n_loc else None,
+                  C.byref(h))
+        return h
+
+    h = ctx._native(s, "nmf", create, [x.local, s.Vt.local, s.W.local])
+    ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+    trace = np.zeros(max(ntr, 1), dtype=np.float64)
+    nt = C.c_int()
+    rc = _lib.load().bs_nmf_run(h, a, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
+    if rc == _lib.BS_EINVAL:
+        raise ValueError(_lib.load().bs_last_error().decode(errors="replace"))
+    if rc != _lib.BS_OK:
+        raise _lib.BsError("bs_nmf_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
+    s.trace.extend(float(v) for v in trace[:nt.value])
     return s
 
 
@@ -123,19 +154,20 @@ def mds_run(ctx, state, iters, trace_every=1):
     n, n_loc = y.shape[0], y.local.shape[1]
     q = s.theta.shape[0]
     code = _lib.dtype_code(y.dtype)
-    h = C.c_void_p()
-    _lib.call("bs_mds_state_create", ctx.handle, _lib.ptr(_flat_local(y)) if n_loc else None, code, n, n_loc, q,
-              1 if s.perturb else 0, _lib.ptr(_flat_local(s.theta)) if n_loc else None, C.byref(h))
-    try:
-        ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
-        trace = np.zeros(max(ntr, 1), dtype=np.float64)
-        nt = C.c_int()
-        rc = _lib.load().bs_mds_run(h, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
-        s.trace.extend(float(v) for v in trace[:nt.value])
-        if rc == _lib.BS_EDEGEN:
-            raise DegenerateConfigError("coincident embedding points; rerun with perturb=True")
-        if rc != _lib.BS_OK:
-            raise _lib.BsError("bs_mds_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
-    finally:
-        _lib.call("bs_mds_state_destroy", h)
+    def create():
+        h = C.c_void_p()
+        _lib.call("bs_mds_state_create", ctx.handle, _lib.ptr(_flat_local(y)) if n_loc else None, code, n, n_loc, q,
+                  1 if s.perturb else 0, _lib.ptr(_flat_local(s.theta)) if n_loc else None, C.byref(h))
+        return h
+
+    h = ctx._native(s, "mds", create, [y.local, s.theta.local])
+    ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
+    trace = np.zeros(max(ntr, 1), dtype=np.float64)
+    nt = C.c_int()
+    rc = _lib.load().bs_mds_run(h, int(iters), int(trace_every), trace.ctypes.data_as(C.c_void_p), C.byref(nt))
+    s.trace.extend(float(v) for v in trace[:nt.value])
+    if rc == _lib.BS_EDEGEN:
+        raise DegenerateConfigError("coincident embedding points; rerun with perturb=True")
+    if rc != _lib.BS_OK:
+        raise _lib.BsError("bs_mds_run", rc, _lib.load().bs_last_error().decode(errors="replace"))
     return s
