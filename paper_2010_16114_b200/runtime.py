@@ -49,7 +49,8 @@ class Context:
         current beta), so it is rebuilt when any of them was replaced or written by
         torch since the last call (storage pointer or in-place version changed)."""
         key = ("native", kind, id(self))
-        sig = tuple((t.data_ptr(), t._version) for t in tensors)
+        # py_epoch: bumped by the Python cox_fit, which moves beta through raw pointers
+        sig = tuple((t.data_ptr(), t._version) for t in tensors) + (state._dev.get("py_epoch", 0),)
         entry = state._dev.get(key)
         if entry is not None and entry[1] != sig:
             self._drop(state, key)
@@ -98,6 +99,7 @@ def cox_run(ctx, state, iters, trace_every=1, monitor=None):
         return h
 
     h = ctx._native(s, "cox", create, [x.local, s.beta.local, s.grad.local, s.delta])
+    s._dev.pop("xb_beta", None)  # the native loop moves beta: cox_fit's X beta reuse no longer applies
     ntr = (iters + trace_every - 1) // trace_every if trace_every else 0
     trace = np.zeros(max(ntr, 1), dtype=np.float64)
     nt, ran, flags = C.c_int(), C.c_int(), C.c_int()

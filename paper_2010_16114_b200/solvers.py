@@ -682,6 +682,7 @@ def cox_fit(state, iters, monitor=None, trace_every=1):
     s = state
     if iters <= 0:
         return s
+    s._dev["py_epoch"] = s._dev.get("py_epoch", 0) + 1  # a native state's cached X beta is stale now
     torch = _torch()
     x = s.X
     m = x.shape[0]

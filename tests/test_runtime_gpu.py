@@ -170,3 +170,30 @@ def test_native_mds_degenerate_raises():
     nat = bs.run_inproc(1, fn, True)[0]
     assert 1 <= len(py) < 3
     np.testing.assert_array_equal(nat, py)
+
+
+def test_native_and_python_cox_calls_interleave():
+    """cox_fit and runtime.cox_run on one state, alternating: each must notice that the
+    other moved beta (neither may reuse a cached X beta) and the trace must equal one
+    long cox_fit."""
+    gen = np.random.Generator(np.random.Philox(21))
+    m, n = 8000, 400
+    x = gen.standard_normal((m, n)).astype(np.float32)
+    delta = (gen.random(m) < 0.5).astype(np.float64)
+    y = np.arange(m, 0, -1, dtype=np.float64)
+
+    def fn(comm, mixed):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=2e-5)
+        if mixed:
+            with runtime.Context(comm) as ctx:
+                runtime.cox_run(ctx, st, 3)
+                bs.cox_fit(st, 3)
+                runtime.cox_run(ctx, st, 3)
+                bs.cox_fit(st, 3)
+        else:
+            bs.cox_fit(st, 12)
+        return np.asarray(st.trace)
+
+    one = bs.run_inproc(1, fn, False)[0]
+    mixed = bs.run_inproc(1, fn, True)[0]
+    np.testing.assert_allclose(mixed, one, rtol=1e-9)
