@@ -197,3 +197,36 @@ def test_native_and_python_cox_calls_interleave():
     one = bs.run_inproc(1, fn, False)[0]
     mixed = bs.run_inproc(1, fn, True)[0]
     np.testing.assert_allclose(mixed, one, rtol=1e-9)
+
+
+def test_c_host_program_matches_cox_fit(tmp_path):
+    """examples/cox_host.c (plain C, no Python) drives a fit through the solver-level ABI;
+    its trace equals cox_fit on the same inputs."""
+    import pathlib
+    import subprocess
+
+    from paper_2010_16114_b200.distarray import philox_key
+
+    root = pathlib.Path(__file__).resolve().parents[1]
+    exe = tmp_path / "cox_host"
+    lib = root / "paper_2010_16114_b200"
+    subprocess.run(["gcc", "-O2", "-I", str(root / "include"), "-I", "/usr/local/cuda/include",
+                    str(root / "examples" / "cox_host.c"), "-o", str(exe), "-L", str(lib), "-lbsb200",
+                    "-L/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{lib}", "-Wl,-rpath,/usr/local/cuda/lib64"],
+                   check=True)
+    k0, k1 = philox_key(1234)
+    out = subprocess.run([str(exe), str(k0), str(k1), "8"], check=True, capture_output=True, text=True).stdout
+    got = np.array([float(v) for v in out.split()])
+    m, n = 4096, 256
+    x = orc.rand_fill_common((m, n), 1234, np.float32)
+    delta = np.array([float((i * 7919) % 10 < 6) for i in range(m)])
+    y = np.arange(m, 0, -1, dtype=np.float64)
+
+    def fn(comm):
+        st = bs.cox_init(_dist(comm, x), y, delta, lam=1e-4, sigma=1e-5)
+        bs.cox_fit(st, 8)
+        return np.asarray(st.trace)
+
+    want = bs.run_inproc(1, fn)[0]
+    assert len(got) == 8
+    np.testing.assert_allclose(got, want, rtol=1e-9)
