@@ -401,6 +401,21 @@ def _cpu_sample(wl):
 
 
 def _cpu_baseline(wl, samples=1):
+    """The oracle leg with every host core given to BLAS (torchrun exports
+    OMP_NUM_THREADS=1 to its workers; the reference arm should not inherit that)."""
+    cores = _cores()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+    except ImportError:  # pragma: no cover
+        return _cpu_baseline_run(wl, samples)
+    with threadpool_limits(limits=cores):
+        out = _cpu_baseline_run(wl, samples)
+        used = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
+    out["threads"] = f"BLAS {used[0] if used else '?'} of {cores} cores"
+    return out
+
+
+def _cpu_baseline_run(wl, samples=1):
     from oracle import blockstat_oracle as orc
 
     s = _cpu_sample(wl)
