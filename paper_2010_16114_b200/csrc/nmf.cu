@@ -625,11 +625,174 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
   }
 }
 
+// The same tile, fragment mapping and k order as dmma_gemm_kernel (so the sums are
+// bitwise identical), but X and B move global -> shared with cp.async through NS
+// stages instead of a register double buffer: no staging registers, and NS-1 tiles in
+// flight per CTA instead of one.  C1 (10k x 10k, r = 20) was latency-bound at 3 CTAs per
+// SM with 16 KB in flight each (profiles/r01_launches_nmf_mu_c1.txt).  Needs 16-byte
+// aligned X rows (even ldx); partial chunks at the M / k_end edges zero-fill through the
+// cp.async src-size operand.
+template <int RP, bool A_MN, int NS>
+struct DmmaAsyncCfg {
+  using B = DmmaCfg<RP, A_MN>;
+  static constexpr int STAGE = B::A_ELEMS + B::B_ELEMS;  // doubles per stage
+  static constexpr int SMEM = NS * STAGE * 8;
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+
+template <int RP, bool A_MN, int NS>
+__global__ void __launch_bounds__(128)
+dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, int64_t M, int64_t ldx, int r,
+                  int64_t K, int64_t k_per_split, double* __restrict__ out) {
+  using C = DmmaCfg<RP, A_MN>;
+  using CA = DmmaAsyncCfg<RP, A_MN, NS>;
+  constexpr int BM = C::BM, BK = C::BK, V = 2, NF = RP / 8, PB = C::PB;
+  constexpr int SA = A_MN ? BM + 8 : BK + 4;
+  extern __shared__ __align__(16) double dm_smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t m0 = int64_t(blockIdx.x) * BM;
+  const int64_t k_begin = int64_t(blockIdx.y) * k_per_split;
+  const int64_t k_end = min(K, k_begin + k_per_split);
+  constexpr int A_CH = BM * BK / V / 128;  // 16-byte chunks per thread
+  constexpr int B_PER = (BK * RP + 127) / 128;
+  auto issue = [&](int64_t k0, int stage) {
+    double* at = dm_smem + stage * CA::STAGE;
+    double* bt = at + C::A_ELEMS;
+#pragma unroll
+    for (int u = 0; u < A_CH; ++u) {
+      const int e = tid + 128 * u;
+      if constexpr (A_MN) {
+        const int kk = e / (BM / V), mv = (e % (BM / V)) * V;
+        const int64_t k = k0 + kk, mrow = m0 + mv;
+        const int64_t left = M - mrow;
+        const int valid = k < k_end && left > 0 ? (left < V ? int(left) : V) : 0;
+        const double* src = valid ? X + k * ldx + mrow : X;
+        cp_async16(at + kk * SA + mv, src, valid * 8);
+      } else {
+        const int row = e / (BK / V), c = e % (BK / V);
+        const int64_t mrow = m0 + row, k = k0 + V * c;
+        const int64_t left = k_end - k;
+        const int valid = mrow < M && left > 0 ? (left < V ? int(left) : V) : 0;
+        const double* src = valid ? X + mrow * ldx + k : X;
+        cp_async16(at + row * SA + V * c, src, valid * 8);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B_PER; ++u) {
+      const int e = tid + 128 * u;
+      if (e < BK * RP) {
+        const int kk = e / RP, c = e % RP;
+        const int64_t k = k0 + kk;
+        const bool ok = k < k_end && c < r;
+        cp_async8(bt + kk * (RP + PB) + c, ok ? B + k * r + c : B, ok ? 8 : 0);
+      }
+    }
+  };
+  double acc[4][NF][2];
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int g = 0; g < NF; ++g) acc[f][g][0] = acc[f][g][1] = 0.0;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int64_t ntiles = k_begin < k_end ? (k_end - k_begin + BK - 1) / BK : 0;
+#pragma unroll
+  for (int s = 0; s < NS - 1; ++s) {
+    if (s < ntiles) issue(k_begin + int64_t(s) * BK, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int64_t t = 0; t < ntiles; ++t) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    __syncthreads();  // tile t landed for every thread; stage (t-1) % NS is free
+    const int64_t tn = t + NS - 1;
+    if (tn < ntiles) issue(k_begin + tn * BK, int(tn % NS));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* at = dm_smem + int(t % NS) * CA::STAGE;
+    const double* bt = at + C::A_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 4) {
+      double a[4], b[NF];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        const int row = 32 * warp + 8 * f + fr;
+        a[f] = A_MN ? at[(ks + fk) * SA + row] : at[row * SA + ks + fk];
+      }
+#pragma unroll
+      for (int g = 0; g < NF; ++g) b[g] = bt[(ks + fk) * (RP + PB) + 8 * g + fr];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int g = 0; g < NF; ++g)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+              : "+d"(acc[f][g][0]), "+d"(acc[f][g][1])
+              : "d"(a[f]), "d"(b[g]));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  double* dst = out + int64_t(blockIdx.y) * M * r;
+#pragma unroll
+  for (int f = 0; f < 4; ++f) {
+    const int64_t row = m0 + 32 * warp + 8 * f + fr;
+    if (row >= M) continue;
+#pragma unroll
+    for (int g = 0; g < NF; ++g) {
+      const int c = 8 * g + 2 * fk;
+      if (c < r) dst[row * r + c] = acc[f][g][0];
+      if (c + 1 < r) dst[row * r + c + 1] = acc[f][g][1];
+    }
+  }
+}
+
+static int dmma_stages() {
+  // BS_DMMA_STAGES=0 selects the register double-buffered kernel (A/B switch)
+  static const int ns = [] {
+    const char* s = getenv("BS_DMMA_STAGES");
+    const int v = s ? atoi(s) : 3;
+    return (v == 0 || v == 3 || v == 4) ? v : 3;
+  }();
+  return ns;
+}
+
 template <bool A_MN>
 static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx, int r, int64_t K, int64_t kps,
                         dim3 grid, double* out, cudaStream_t st) {
   static const bool disabled = getenv("BS_DISABLE_DMMA") != nullptr;  // A/B switch for benchmarks
   if (disabled) return false;
+  const int ns = dmma_stages();
+  const bool async_ok = ns != 0 && (ldx % 2) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(B) & 7) == 0 && (A_MN || kps % 2 == 0);
+  if (async_ok && r <= 32) {
+    const int rpa = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : 32;
+#define BS_DMMA_A(RPV, NSV)                                                                                    \
+  {                                                                                                            \
+    smem_attr(dmma_async_kernel<RPV, A_MN, NSV>, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM);                        \
+    dmma_async_kernel<RPV, A_MN, NSV>                                                                          \
+        <<<grid, 128, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);               \
+    return true;                                                                                               \
+  }
+    if (ns == 4) {
+      switch (rpa) {
+        case 8: BS_DMMA_A(8, 4)
+        case 16: BS_DMMA_A(16, 4)
+        case 24: BS_DMMA_A(24, 4)
+        default: BS_DMMA_A(32, 4)
+      }
+    }
+    switch (rpa) {
+      case 8: BS_DMMA_A(8, 3)
+      case 16: BS_DMMA_A(16, 3)
+      case 24: BS_DMMA_A(24, 3)
+      default: BS_DMMA_A(32, 3)
+    }
+#undef BS_DMMA_A
+  }
   // N padded to the next multiple of 8 the DMMA fragments need (r = 20 -> 24, not 32)
   const int rp = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : r <= 32 ? 32 : r <= 48 ? 48 : r <= 64 ? 64 : 0;
 #define BS_DMMA(RPV)                                                                                         \

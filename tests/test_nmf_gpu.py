@@ -187,3 +187,44 @@ def test_nmf_more_ranks_than_columns():
     ovt, ow, otr = orc.nmf_apg(x, vt0, w0, 10)
     np.testing.assert_allclose(tr, otr, rtol=1e-10)
     np.testing.assert_allclose(vt, ovt, rtol=1e-9, atol=1e-12)
+
+
+_DMMA_SCRIPT = r"""
+import sys, numpy as np
+import paper_2010_16114_b200 as bs
+from oracle import blockstat_oracle as orc
+out = {}
+for i, (m, n, r) in enumerate([(1000, 777, 20), (257, 131, 7), (129, 380, 30), (3000, 2001, 24)]):
+    x = orc.rand_fill_common((m, n), 400 + r, np.float64)
+    vt0, w0 = orc.nmf_init(x, r, 500 + r)
+    def fn(comm):
+        xd = bs.distribute(x if comm.rank == 0 else None, comm)
+        st = bs.nmf_init(xd, r, seed=1)
+        st.Vt.local[...] = bs.distribute(vt0 if comm.rank == 0 else None, comm).local
+        st.W.local[...] = bs.distribute(w0 if comm.rank == 0 else None, comm).local
+        bs.nmf_multiplicative(st, 5, trace_every=1)
+        return np.asarray(st.trace), bs.gather_full(st.Vt), bs.gather_full(st.W)
+    tr, vt, w = bs.run_inproc(1 + i % 2, fn)[0]
+    out[f"tr{i}"], out[f"vt{i}"], out[f"w{i}"] = tr, vt, w
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_dmma_cp_async_pipeline_is_bitwise_equal_to_register_pipeline(tmp_path):
+    """The cp.async-staged float64 DMMA GEMM (BS_DMMA_STAGES = 3 / 4) keeps the tile, fragment
+    mapping and k order of the register double-buffered one (BS_DMMA_STAGES = 0): same bits."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    res = {}
+    for ns in ("0", "3", "4"):
+        f = tmp_path / f"ns{ns}.npz"
+        env = dict(os.environ, BS_DMMA_STAGES=ns, PYTHONPATH=str(root))
+        subprocess.run([sys.executable, "-c", _DMMA_SCRIPT, str(f)], check=True, env=env, cwd=root, timeout=600)
+        res[ns] = np.load(f)
+    for ns in ("3", "4"):
+        for k in res["0"].files:
+            np.testing.assert_array_equal(res[ns][k], res["0"][k], err_msg=f"stages={ns} {k}")
