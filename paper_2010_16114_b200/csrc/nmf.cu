@@ -860,6 +860,23 @@ static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, i
 static int wxt_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(m, 128), n_loc, 256); }
 static int vtx_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(n_loc, 128), m, 512); }
 
+// float64 split count <= s_max that fills whole waves of the DMMA kernel (3 CTAs per SM):
+// C1 has 79 row tiles, where the default 8 splits give 632 CTAs = 1.42 waves of 444 and 5
+// give 395 = 0.89 of one.  Ties go to the larger count.  BS_DMMA_SPLITS overrides (A/B).
+static int f64_splits(int64_t tiles, int s_max) {
+  static const int forced = [] { const char* e = getenv("BS_DMMA_SPLITS"); return e ? atoi(e) : 0; }();
+  if (forced > 0) return std::min(forced, s_max);
+  const int64_t slots = int64_t(num_sms()) * 3;
+  int best = s_max;
+  double best_eff = 0.0;
+  for (int s = s_max; s >= 1; --s) {
+    const int64_t ctas = tiles * s;
+    const double eff = double(ctas) / double(ceil_div(ctas, slots) * slots);
+    if (eff > best_eff + 0.02) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
 static int dsize(int dtype) { return dtype == BS_F64 ? 8 : 4; }
 
 extern "C" int64_t bs_nmf_wxt_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
@@ -921,7 +938,7 @@ static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int6
       if (rc != BS_OK) return rc;
     }
   }
-  const int S = wxt_splits(m, n_loc);
+  const int S = dtype == BS_F64 ? f64_splits(ceil_div(m, 128), wxt_splits(m, n_loc)) : wxt_splits(m, n_loc);
   const int64_t cps = ceil_div(ceil_div(n_loc, S), 32) * 32;
   const int Seff = int(ceil_div(n_loc, cps));
   if (dtype == BS_F64) {
@@ -1365,7 +1382,7 @@ extern "C" int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void*
   }
   Workspace ws(work, work_bytes);
   Workspace upd = ws.split(upd_workspace(r, n_loc));
-  const int S = vtx_splits(m, n_loc);
+  const int S = dtype == BS_F64 ? f64_splits(ceil_div(n_loc, 128), vtx_splits(m, n_loc)) : vtx_splits(m, n_loc);
   const int64_t rps = std::max<int64_t>(1, ceil_div(ceil_div(std::max<int64_t>(m, 1), S), 32) * 32);
   const int Seff = int(std::max<int64_t>(1, ceil_div(m, rps)));
   if (dtype == BS_F64) {
