@@ -754,8 +754,8 @@ static int dmma_stages() {
   // BS_DMMA_STAGES=0 selects the register double-buffered kernel (A/B switch)
   static const int ns = [] {
     const char* s = getenv("BS_DMMA_STAGES");
-    const int v = s ? atoi(s) : 3;
-    return (v == 0 || v == 3 || v == 4) ? v : 3;
+    const int v = s ? atoi(s) : 2;
+    return (v == 0 || v == 2 || v == 3 || v == 4) ? v : 2;
   }();
   return ns;
 }
@@ -777,6 +777,14 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
         <<<grid, 128, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);               \
     return true;                                                                                               \
   }
+    if (ns == 2) {
+      switch (rpa) {
+        case 8: BS_DMMA_A(8, 2)
+        case 16: BS_DMMA_A(16, 2)
+        case 24: BS_DMMA_A(24, 2)
+        default: BS_DMMA_A(32, 2)
+      }
+    }
     if (ns == 4) {
       switch (rpa) {
         case 8: BS_DMMA_A(8, 4)
@@ -863,10 +871,12 @@ static int vtx_splits(int64_t m, int64_t n_loc) { return pick_splits(ceil_div(n_
 // float64 split count <= s_max that fills whole waves of the DMMA kernel (3 CTAs per SM):
 // C1 has 79 row tiles, where the default 8 splits give 632 CTAs = 1.42 waves of 444 and 5
 // give 395 = 0.89 of one.  Ties go to the larger count.  BS_DMMA_SPLITS overrides (A/B).
+static int dmma_stages();
+
 static int f64_splits(int64_t tiles, int s_max) {
   static const int forced = [] { const char* e = getenv("BS_DMMA_SPLITS"); return e ? atoi(e) : 0; }();
   if (forced > 0) return std::min(forced, s_max);
-  const int64_t slots = int64_t(num_sms()) * 3;
+  const int64_t slots = int64_t(num_sms()) * (dmma_stages() == 2 ? 4 : 3);  // resident CTAs per SM (smem)
   int best = s_max;
   double best_eff = 0.0;
   for (int s = s_max; s >= 1; --s) {
