@@ -489,7 +489,9 @@ cc_gemm_kernel(const T* __restrict__ X, const T* __restrict__ B, int64_t M, int6
 
 template <int RP, bool A_MN>
 struct DmmaCfg {
-  static constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, PB = 8;
+  // B row stride RP + PB must be 8 doubles mod 16 (64 B mod 128), or the 4 k rows a
+  // fragment load touches share banks: RP = 8 / 24 pad by 0, the others by 8.
+  static constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, PB = RP % 16 == 8 ? 0 : 8;
   // A tile: [k][m] (m contiguous) for scn b; [m][k] (k contiguous, +4 pad) for scn a
   static constexpr int A_ELEMS = A_MN ? BK * (BM + 8) : BM * (BK + 4);
   static constexpr int B_ELEMS = BK * (RP + PB);
