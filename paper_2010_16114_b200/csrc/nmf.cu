@@ -1116,24 +1116,39 @@ factor_update_kernel(int algo, T* __restrict__ F, const TN* __restrict__ num, in
   (void)red;  // folded by fold_rows_kernel
 }
 
-// out[e] = sum_p parts[p * len + e], p ascending (deterministic); one thread per output with
-// eight loads in flight, so a (grid x (r^2 + 1)) partial block folds in a few L2 round trips
-// instead of one CTA walking it (C2: 296 x 3601 partials).
-__global__ void __launch_bounds__(128) fold_rows_kernel(const double* __restrict__ parts, int np, int len,
-                                                        double* __restrict__ out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= len) return;
+// out[e] = sum_p parts[p * len + e] (deterministic).  A CTA owns 32 consecutive outputs;
+// its 8 warps each sum a contiguous run of p ascending (lane = output, so every load is a
+// coalesced 256-byte row segment, eight in flight), then warp partials fold in warp order
+// through shared memory.  C1's 157 x 401 partials took 15 us as one thread per output
+// walking all p; this spreads them over 13 CTAs x 8 warps.
+constexpr int FOLD_WARPS = 8;
+__global__ void __launch_bounds__(32 * FOLD_WARPS) fold_rows_kernel(const double* __restrict__ parts, int np,
+                                                                    int len, double* __restrict__ out) {
+  __shared__ double part[FOLD_WARPS][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  const int per = (np + FOLD_WARPS - 1) / FOLD_WARPS;
+  const int p0 = w * per, p1 = min(np, p0 + per);
   double s = 0.0;
-  int p = 0;
-  for (; p + 8 <= np; p += 8) {
-    double t[8];
+  if (e < len) {
+    int p = p0;
+    for (; p + 8 <= p1; p += 8) {
+      double t[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = parts[int64_t(p + u) * len + e];
+      for (int u = 0; u < 8; ++u) t[u] = parts[int64_t(p + u) * len + e];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s += t[u];
+      for (int u = 0; u < 8; ++u) s += t[u];
+    }
+    for (; p < p1; ++p) s += parts[int64_t(p) * len + e];
   }
-  for (; p < np; ++p) s += parts[int64_t(p) * len + e];
-  out[e] = s;
+  part[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && e < len) {
+    double t = part[0][lane];
+#pragma unroll
+    for (int u = 1; u < FOLD_WARPS; ++u) t += part[u][lane];
+    out[e] = t;
+  }
 }
 
 // Register-blocked variant (RP <= 64): per stage of UPD_COLS columns the old factor
@@ -1329,7 +1344,7 @@ static int launch_update(int algo, T* F, const TN* num, int S, int64_t slab, con
   }
 #undef BS_UPD_RB
 #undef BS_UPD
-  fold_rows_kernel<<<(r * r + 1 + 127) / 128, 128, 0, st>>>(parts, grid, r * r + 1, red);
+  fold_rows_kernel<<<(r * r + 1 + 31) / 32, 32 * FOLD_WARPS, 0, st>>>(parts, grid, r * r + 1, red);
   return check_launch("factor update", 2);
 }
 
