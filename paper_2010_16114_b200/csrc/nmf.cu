@@ -1286,9 +1286,11 @@ factor_update_rb_kernel(int algo, T* __restrict__ F, const TN* __restrict__ num,
   if (tid == 0) mine[rr] = csum;
 }
 
-// >= 64 columns per block, at most 2 blocks per SM (the last block folds grid x (r^2 + 1) partials)
+// >= 32 columns (one stage) per block, at most 3 blocks per SM; fold_rows_kernel folds the
+// grid x (r^2 + 1) partials.  C1 (10,000 columns): 313 one-stage blocks instead of 157
+// two-stage ones, which halves each block's serial load -> den -> Gram chain.
 static int upd_grid(int64_t ncols) {
-  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 64), int64_t(num_sms()) * 2)));
+  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(ncols, 32), int64_t(num_sms()) * 3)));
 }
 
 static int64_t upd_workspace(int r, int64_t ncols) {
