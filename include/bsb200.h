@@ -139,13 +139,32 @@ int bs_pairwise_euclidean(const void* x, int dtype, int64_t d, int64_t n,
 int bs_nmf_scan(const void* X, int dtype, int64_t count, double* out_dev,
                 void* work, int64_t work_bytes, void* stream);
 
+/* Per-call pass over X (the reference's _nmf_check, solvers.py:139-141, which
+ * runs at the start of every nmf_multiplicative / nmf_apg call):
+ *   stats_dev = {min(X), sum(X^2), nonfinite?, scales_ready?}  (float64)
+ * For float32 X (m % 4 == 0) it also writes, into xscale (bs_nmf_xscale_bytes),
+ * the power-of-two block scales the integer tensor-core GEMMs use: one per
+ * (row, 512 columns) for scn b and one per (column, 512 rows) for scn a. */
+int64_t bs_nmf_xscale_bytes(int64_t m, int64_t n_loc);
+int64_t bs_nmf_prepare_workspace(int64_t m, int64_t n_loc);
+int bs_nmf_prepare(const void* X, int dtype, int64_t m, int64_t n_loc,
+                   double* stats_dev, void* xscale, void* work,
+                   int64_t work_bytes, void* stream);
+
+/* How many scn a / scn b GEMMs ran on each path since the last reset:
+ * out4 = {integer digit-slice tcgen05, 3xTF32 tcgen05, float32 CUDA cores,
+ *         float64 (DMMA / CUDA cores)}. */
+int bs_gemm_path_counts(int64_t* out4, int reset);
+
 /* scn b local GEMM (distlinalg.py:246-252): P (r x m, column-major, float32
  * or float64 like X) = W_loc X_loc^T summed over the rank's n_loc columns.
- * The caller reduce-scatters P across ranks (distlinalg.py:251-252). */
+ * The caller reduce-scatters P across ranks (distlinalg.py:251-252).
+ * xscale (nullable): scales from bs_nmf_prepare; float32 with r <= 64 then runs
+ * the exact-accumulation integer digit-slice kernel (nmf_i8.cu). */
 int64_t bs_nmf_wxt_workspace(int dtype, int64_t m, int64_t n_loc, int r);
 int bs_nmf_wxt(const void* X, const void* W, int dtype, int64_t m,
-               int64_t n_loc, int r, void* P, void* work, int64_t work_bytes,
-               void* stream);
+               int64_t n_loc, int r, void* P, const void* xscale, void* work,
+               int64_t work_bytes, void* stream);
 
 /* scn b fused with _nmf_check (solvers.py:139-141, 147): the same X pass also
  * yields stats_dev = {min, sum X^2} (float64; with padded tcgen05 tiles the min
@@ -176,21 +195,31 @@ int bs_nmf_vt_step(int algo, void* Vt, const void* WXt, const double* WWt,
 int64_t bs_nmf_w_step_workspace(int dtype, int64_t m, int64_t n_loc, int r);
 int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void* W,
                   const double* VtV, int dtype, int64_t m, int64_t n_loc,
-                  int r, double eps, double* red, void* work,
-                  int64_t work_bytes, void* stream);
+                  int r, double eps, double* red, const void* xscale,
+                  void* work, int64_t work_bytes, void* stream);
 
 /* nmf_objective after an update via the Gram identity
  * ||X - V^T W||^2 = ||X||^2 - 2 <VtX, W> + <VtV, WWt> (solvers.py:124-136):
- * out_dev[0] = xsq[0] - 2 red[r*r] + sum(VtV .* red[0..r*r)). */
+ * out_dev[0] = xsq[0] - 2 red[r*r] + sum(VtV .* red[0..r*r)).
+ * direct_flag (nullable) is set to 1 when kappa < 0, or when kappa > 0 and the value
+ * is within the cancellation regime (xsq / obj > kappa, or obj <= 0); 0 otherwise. */
 int bs_nmf_objective(const double* xsq, const double* red, const double* VtV,
-                     int r, double* out_dev, void* stream);
+                     int r, double* out_dev, int* direct_flag, double kappa,
+                     void* stream);
+
+/* Cancellation guard: direct_flag (set by bs_nmf_objective when ||X||^2 / obj
+ * > kappa) selects the direct residual: out_dev[0] = direct_dev[0] if *flag. */
+int bs_nmf_objective_select(const int* direct_flag, const double* direct_dev,
+                            double* out_dev, void* stream);
 
 /* nmf_objective standalone (solvers.py:124-136), direct residual:
- * out_dev[0] = sum over the local block of (X - Vt_full^T W_loc)^2. */
+ * out_dev[0] = sum over the local block of (X - Vt_full^T W_loc)^2.
+ * flag_dev (nullable): when it points to 0 the pass is skipped and out_dev[0] = 0. */
 int64_t bs_nmf_residual_workspace(int64_t m, int64_t n_loc);
 int bs_nmf_residual(const void* X, const void* Vt_full, const void* W,
                     int dtype, int64_t m, int64_t n_loc, int r, double* out_dev,
-                    void* work, int64_t work_bytes, void* stream);
+                    const int* flag_dev, void* work, int64_t work_bytes,
+                    void* stream);
 
 /* ---- MDS (solvers.py:188-305) ------------------------------------------ */
 

@@ -67,16 +67,21 @@ SIGNATURES = {
     "bs_pairwise_euclidean": (_i, [_p, _i, _i64, _i64, _i64, _i64, _p, _p]),
     "bs_nmf_scan": (_i, [_p, _i, _i64, _p, _p, _i64, _p]),
     "bs_nmf_wxt_workspace": (_i64, [_i, _i64, _i64, _i]),
-    "bs_nmf_wxt": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _i64, _p]),
+    "bs_nmf_wxt": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _p, _i64, _p]),
+    "bs_nmf_xscale_bytes": (_i64, [_i64, _i64]),
+    "bs_nmf_prepare_workspace": (_i64, [_i64, _i64]),
+    "bs_nmf_prepare": (_i, [_p, _i, _i64, _i64, _p, _p, _p, _i64, _p]),
+    "bs_gemm_path_counts": (_i, [_p, _i]),
     "bs_nmf_wxt_scan_workspace": (_i64, [_i, _i64, _i64, _i]),
     "bs_nmf_wxt_scan": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _p, _i64, _p]),
     "bs_nmf_vt_step_workspace": (_i64, [_i, _i64]),
     "bs_nmf_vt_step": (_i, [_i, _p, _p, _p, _i, _i, _i64, _d, _p, _p, _p, _i64, _p]),
     "bs_nmf_w_step_workspace": (_i64, [_i, _i64, _i64, _i]),
-    "bs_nmf_w_step": (_i, [_i, _p, _p, _p, _p, _i, _i64, _i64, _i, _d, _p, _p, _i64, _p]),
-    "bs_nmf_objective": (_i, [_p, _p, _p, _i, _p, _p]),
+    "bs_nmf_w_step": (_i, [_i, _p, _p, _p, _p, _i, _i64, _i64, _i, _d, _p, _p, _p, _i64, _p]),
+    "bs_nmf_objective": (_i, [_p, _p, _p, _i, _p, _p, _d, _p]),
+    "bs_nmf_objective_select": (_i, [_p, _p, _p, _p]),
     "bs_nmf_residual_workspace": (_i64, [_i64, _i64]),
-    "bs_nmf_residual": (_i, [_p, _p, _p, _i, _i64, _i64, _i, _p, _p, _i64, _p]),
+    "bs_nmf_residual": (_i, [_p, _p, _p, _i, _i64, _i64, _i, _p, _p, _p, _i64, _p]),
     "bs_mds_pass_workspace": (_i64, [_i, _i64, _i64, _i]),
     "bs_mds_pass": (_i, [_p, _p, _i, _i64, _i64, _i64, _i, _i, _i, _p, _p, _p, _p, _i64, _p]),
     "bs_mds_update": (_i, [_p, _p, _p, _i, _i, _i64, _d, _p, _i, _p, _p]),

@@ -660,8 +660,10 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
   std::call_once(once, [] {
     const char* e = getenv("BS_MDS_TC_GROUP");
     group = (e && atoi(e) > 0) ? atoi(e) : 2;
+#ifdef BS_DEBUG_MODES  // work-skipping switches only in debug builds (scripts/mds_modes.sh)
     const char* m = getenv("BS_MDS_TC_MODE");
     mode = m ? atoi(m) : 0;
+#endif
   });
   smem_attr(mds_tc_kernel<1>, SMEM);
   smem_attr(mds_tc_kernel<2>, SMEM);

@@ -31,7 +31,20 @@ int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, flo
            int* splits, Workspace& ws, cudaStream_t st, bool* used);
 int64_t tc_wxt_workspace(int64_t m, int64_t n_loc, int r);
 int64_t tc_vtx_workspace(int64_t m, int64_t n_loc, int r);
+// integer digit-slice tensor-core path (nmf_i8.cu)
+int64_t i8_xscale_bytes(int64_t m, int64_t n_loc);
+int64_t i8_prepare_workspace(int64_t m, int64_t n_loc);
+int64_t i8_gemm_workspace(int64_t K);
+int i8_prepare(const float* X, int64_t m, int64_t n_loc, double* stats, int8_t* xscale, Workspace& ws,
+               cudaStream_t st);
+int i8_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, const int8_t* xexp_b, float* P,
+           Workspace& ws, cudaStream_t st, bool* used);
+int i8_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, const int8_t* xexp_a, float* C,
+           int cap_slabs, int* splits, Workspace& ws, cudaStream_t st, bool* used);
+void note_gemm_path(int path);  // 0 i8 tensor, 1 tf32 tensor, 2 fp32 CUDA cores, 3 fp64 (DMMA / CUDA cores)
 }  // namespace bs
+
+static int64_t xgroups(int64_t k) { return (k + 511) / 512; }
 
 constexpr int MAX_R = 128;
 
@@ -827,6 +840,7 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
 template <typename T>
 static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, int r, int64_t cps,
                             int S, T* out, cudaStream_t st) {
+  note_gemm_path(sizeof(T) == 8 ? 3 : 2);
   dim3 grid(unsigned(ceil_div(m, 128)), unsigned(S));
   if constexpr (sizeof(T) == 8) {
     if (launch_dmma<true>(X, W, m, m, r, n_loc, cps, grid, out, st)) return;
@@ -848,6 +862,7 @@ static void launch_wxt_core(const T* X, const T* W, int64_t m, int64_t n_loc, in
 template <typename T>
 static void launch_vtx_core(const T* X, const T* Vt, int64_t m, int64_t n_loc, int r, int64_t rps,
                             int S, T* out, cudaStream_t st) {
+  note_gemm_path(sizeof(T) == 8 ? 3 : 2);
   dim3 grid128(unsigned(ceil_div(n_loc, 128)), unsigned(S));
   if constexpr (sizeof(T) == 8) {
     if (launch_dmma<false>(X, Vt, n_loc, m, r, m, rps, grid128, out, st)) return;
@@ -893,16 +908,16 @@ static int dsize(int dtype) { return dtype == BS_F64 ? 8 : 4; }
 
 extern "C" int64_t bs_nmf_wxt_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
   int64_t core = ws_bytes<char>(int64_t(wxt_splits(m, n_loc)) * m * r * dsize(dtype));
-  if (dtype == BS_F32) core = std::max(core, tc_wxt_workspace(m, n_loc, r));
+  if (dtype == BS_F32) core = std::max(core, tc_wxt_workspace(m, n_loc, r) + i8_gemm_workspace(n_loc));
   return core;
 }
 
 static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
-                        double* stats, void* work, int64_t work_bytes, void* stream);
+                        const void* xscale, double* stats, void* work, int64_t work_bytes, void* stream);
 
 extern "C" int bs_nmf_wxt(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r,
-                          void* P, void* work, int64_t work_bytes, void* stream) {
-  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, nullptr, work, work_bytes, stream);
+                          void* P, const void* xscale, void* work, int64_t work_bytes, void* stream) {
+  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, xscale, nullptr, work, work_bytes, stream);
 }
 
 extern "C" int64_t bs_nmf_wxt_scan_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
@@ -911,11 +926,11 @@ extern "C" int64_t bs_nmf_wxt_scan_workspace(int dtype, int64_t m, int64_t n_loc
 
 extern "C" int bs_nmf_wxt_scan(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
                                double* stats_dev, void* work, int64_t work_bytes, void* stream) {
-  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, stats_dev, work, work_bytes, stream);
+  return nmf_wxt_impl(X, W, dtype, m, n_loc, r, P, nullptr, stats_dev, work, work_bytes, stream);
 }
 
 static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int64_t n_loc, int r, void* P,
-                        double* stats, void* work, int64_t work_bytes, void* stream) {
+                        const void* xscale, double* stats, void* work, int64_t work_bytes, void* stream) {
   clear_error();
   if (r < 1 || r > MAX_R || m < 0 || n_loc < 0) {
     set_error("bs_nmf_wxt: bad shape m=%lld n_loc=%lld r=%d", (long long)m, (long long)n_loc, r);
@@ -938,6 +953,13 @@ static int nmf_wxt_impl(const void* X, const void* W, int dtype, int64_t m, int6
   if (m == 0) return BS_OK;
   if (n_loc == 0) {
     return cudaMemsetAsync(P, 0, size_t(m) * r * dsize(dtype), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  }
+  if (dtype == BS_F32 && xscale && !stats) {
+    bool used = false;
+    int rc = i8_wxt(static_cast<const float*>(X), static_cast<const float*>(W), m, n_loc, r,
+                    static_cast<const int8_t*>(xscale), static_cast<float*>(P), ws, st, &used);
+    if (rc != BS_OK) return rc;
+    if (used) return BS_OK;
   }
   if (dtype == BS_F32) {
     bool used = false;
@@ -1393,13 +1415,13 @@ extern "C" int bs_nmf_vt_step(int algo, void* Vt, const void* WXt, const double*
 extern "C" int64_t bs_nmf_w_step_workspace(int dtype, int64_t m, int64_t n_loc, int r) {
   const int slabs = dtype == BS_F32 ? std::max(vtx_splits(m, n_loc), TC_MAX_SPLITS) : vtx_splits(m, n_loc);
   int64_t g = ws_bytes<char>(int64_t(slabs) * n_loc * r * dsize(dtype));
-  if (dtype == BS_F32) g += tc_vtx_workspace(m, n_loc, r);
+  if (dtype == BS_F32) g += tc_vtx_workspace(m, n_loc, r) + i8_gemm_workspace(m);
   return g + upd_workspace(r, n_loc) + 512;
 }
 
 extern "C" int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void* W, const double* VtV,
                              int dtype, int64_t m, int64_t n_loc, int r, double eps, double* red,
-                             void* work, int64_t work_bytes, void* stream) {
+                             const void* xscale, void* work, int64_t work_bytes, void* stream) {
   clear_error();
   if (r < 1 || r > MAX_R || (algo != BS_NMF_MU && algo != BS_NMF_APG) || m < 0 || n_loc < 0) {
     set_error("bs_nmf_w_step: bad arguments");
@@ -1434,7 +1456,13 @@ extern "C" int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void*
     const int cap = std::max(Seff, TC_MAX_SPLITS);
     float* Cbuf = ws.take<float>(int64_t(cap) * n_loc * r);
     if (!Cbuf) { set_error("bs_nmf_w_step: workspace too small"); return BS_EWORK; }
-    if (m > 0) {
+    if (m > 0 && xscale) {
+      const int8_t* xexp_a = static_cast<const int8_t*>(xscale) + xgroups(n_loc) * m;
+      int rc = i8_vtx(static_cast<const float*>(X), static_cast<const float*>(Vt_full), m, n_loc, r, xexp_a, Cbuf,
+                      cap, &splits, ws, st, &used);
+      if (rc != BS_OK) return rc;
+    }
+    if (m > 0 && !used) {
       int rc = tc_vtx(static_cast<const float*>(X), static_cast<const float*>(Vt_full), m, n_loc, r, Cbuf,
                       cap, &splits, ws, st, &used);
       if (rc != BS_OK) return rc;
@@ -1458,90 +1486,219 @@ extern "C" int bs_nmf_w_step(int algo, const void* X, const void* Vt_full, void*
 }
 
 // ---------------------------------------------------------------------------
-// Objective via the Gram identity (after an update).
+// bs_nmf_prepare: the per-call X pass (solvers.py:139-141) — min, ||X||^2, and for
+// float32 the per-block scales of the integer tensor-core GEMMs (nmf_i8.cu).
+// ---------------------------------------------------------------------------
+
+extern "C" int64_t bs_nmf_xscale_bytes(int64_t m, int64_t n_loc) { return i8_xscale_bytes(m, n_loc); }
+
+extern "C" int64_t bs_nmf_prepare_workspace(int64_t m, int64_t n_loc) {
+  return std::max<int64_t>(i8_prepare_workspace(m, n_loc), 64 * 1024) + 512;
+}
+
+// stats[2] (nonfinite) is produced by the integer path's pass; the plain scan does not look
+// for nonfinite values, and without scales (ready = 0) the caller keeps the other GEMM paths.
+__global__ void prep_stats_tail_kernel(double* stats, double ready) {
+  if (ready == 0.0) stats[2] = 0.0;
+  stats[3] = ready;
+}
+
+extern "C" int bs_nmf_prepare(const void* X, int dtype, int64_t m, int64_t n_loc, double* stats_dev, void* xscale,
+                              void* work, int64_t work_bytes, void* stream) {
+  clear_error();
+  cudaStream_t st = as_stream(stream);
+  if (m < 0 || n_loc < 0) {
+    set_error("bs_nmf_prepare: bad shape");
+    return BS_EINVAL;
+  }
+  Workspace ws(work, work_bytes);
+  const bool i8 = dtype == BS_F32 && xscale && m > 0 && n_loc > 0 && m % 4 == 0 &&
+                  !(reinterpret_cast<uintptr_t>(X) & 15);
+  if (i8) {
+    int rc = i8_prepare(static_cast<const float*>(X), m, n_loc, stats_dev, static_cast<int8_t*>(xscale), ws, st);
+    if (rc != BS_OK) return rc;
+    prep_stats_tail_kernel<<<1, 1, 0, st>>>(stats_dev, 1.0);
+    // keep the nonfinite flag the pass produced: rewrite only the ready flag
+    return check_launch("bs_nmf_prepare tail");
+  }
+  int rc = bs_nmf_scan(X, dtype, m * n_loc, stats_dev, ws.base, ws.size, stream);
+  if (rc != BS_OK) return rc;
+  prep_stats_tail_kernel<<<1, 1, 0, st>>>(stats_dev, 0.0);
+  return check_launch("bs_nmf_prepare tail");
+}
+
+// ---------------------------------------------------------------------------
+// Objective via the Gram identity (after an update), with a cancellation guard:
+// when ||X||^2 / obj exceeds kappa (or obj <= 0; kappa < 0: always) the value cannot be
+// trusted to the parity tolerance and *direct_flag is raised — the caller then evaluates the
+// reference's own direct residual (solvers.py:124-136) with bs_nmf_residual.
 // ---------------------------------------------------------------------------
 
 __global__ void nmf_objective_kernel(const double* xsq, const double* red, const double* VtV, int r,
-                                     double* out) {
+                                     double* out, int* flag, double kappa) {
   __shared__ double sh[32];
   const int rr = r * r;
   double s = 0.0;
   for (int e = threadIdx.x; e < rr; e += blockDim.x) s = fma(VtV[e], red[e], s);
   s = block_sum(s, sh);
-  if (threadIdx.x == 0) out[0] = (xsq[0] - 2.0 * red[rr]) + s;
+  if (threadIdx.x == 0) {
+    const double obj = (xsq[0] - 2.0 * red[rr]) + s;
+    out[0] = obj;
+    if (flag) *flag = (kappa < 0.0 || (kappa > 0.0 && (!(obj > 0.0) || obj * kappa < xsq[0]))) ? 1 : 0;
+  }
 }
 
 extern "C" int bs_nmf_objective(const double* xsq, const double* red, const double* VtV, int r,
-                                double* out_dev, void* stream) {
+                                double* out_dev, int* direct_flag, double kappa, void* stream) {
   clear_error();
-  nmf_objective_kernel<<<1, 256, 0, as_stream(stream)>>>(xsq, red, VtV, r, out_dev);
+  nmf_objective_kernel<<<1, 256, 0, as_stream(stream)>>>(xsq, red, VtV, r, out_dev, direct_flag, kappa);
   return check_launch("bs_nmf_objective");
 }
 
+__global__ void objective_select_kernel(const int* flag, const double* direct, double* out) {
+  if (*flag) out[0] = direct[0];
+}
+
+extern "C" int bs_nmf_objective_select(const int* direct_flag, const double* direct_dev, double* out_dev,
+                                       void* stream) {
+  clear_error();
+  objective_select_kernel<<<1, 1, 0, as_stream(stream)>>>(direct_flag, direct_dev, out_dev);
+  return check_launch("bs_nmf_objective_select");
+}
+
 // ---------------------------------------------------------------------------
-// Standalone objective: direct residual sum((X - Vt^T W)^2) over the local block.
-// One warp per column j: the column's factor W[:, j] lives in registers and
-// every lane reconstructs rows i = lane, lane+32, ...
+// Direct residual sum((X - Vt^T W)^2) over the local block (solvers.py:124-136).
+// A warp owns 32 consecutive rows (lane = row, its Vt column in registers) and a
+// run of columns; the block stages those columns of W in shared memory and every
+// lane reads them as broadcasts.  The reconstruction runs in the storage precision
+// (float32 FMA chains for float32, like the reference's float32 matmul), the squares
+// are summed in float64.  flag (nullable): when *flag == 0 the kernel only zeroes out.
 // ---------------------------------------------------------------------------
 
-template <typename T>
+template <typename T, int RP>
 __global__ void __launch_bounds__(256)
 residual_kernel(const T* __restrict__ X, const T* __restrict__ Vt, const T* __restrict__ W, int64_t m,
-                int64_t n_loc, int r, double* __restrict__ parts, unsigned int* counter, double* out) {
+                int64_t n_loc, int r, int64_t col_chunk, double* __restrict__ parts, unsigned int* counter,
+                double* out, const int* flag) {
+  constexpr int RES_COLS = 16384 / (RP * int(sizeof(T))) < 64 ? 16384 / (RP * int(sizeof(T))) : 64;
+  __shared__ T sw[RES_COLS * RP];
   __shared__ double sh[32];
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
-  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  if (flag && *flag == 0) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) out[0] = 0.0;
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (int64_t(blockIdx.x) * 8 + warp) * 32 + lane;
+  const bool row_ok = i < m;
+  T v[RP];
+#pragma unroll
+  for (int k = 0; k < RP; ++k) v[k] = (row_ok && k < r) ? Vt[i * r + k] : T(0);
+  const int64_t j0 = int64_t(blockIdx.y) * col_chunk;
+  const int64_t j1 = min(n_loc, j0 + col_chunk);
   double acc = 0.0;
-  for (int64_t j = gw; j < n_loc; j += nw) {
-    for (int64_t i = lane; i < m; i += 32) {
-      T rec = T(0);
-      for (int k = 0; k < r; ++k) rec = fma(Vt[i * r + k], W[j * r + k], rec);
-      const double d = double(X[j * m + i] - rec);
-      acc = fma(d, d, acc);
+  for (int64_t jb = j0; jb < j1; jb += RES_COLS) {
+    const int nc = int(j1 - jb < int64_t(RES_COLS) ? j1 - jb : int64_t(RES_COLS));
+    __syncthreads();
+    for (int e = threadIdx.x; e < nc * RP; e += 256) {
+      const int c = e / RP, k = e - c * RP;
+      sw[e] = k < r ? W[(jb + c) * r + k] : T(0);
+    }
+    __syncthreads();
+    if (row_ok) {
+      for (int c = 0; c < nc; ++c) {
+        const T* w = sw + c * RP;
+        T rec0 = T(0), rec1 = T(0);
+#pragma unroll
+        for (int k = 0; k < RP; k += 2) {
+          rec0 = fma(v[k], w[k], rec0);
+          rec1 = fma(v[k + 1], w[k + 1], rec1);
+        }
+        const double d = double(X[(jb + c) * m + i] - (rec0 + rec1));
+        acc = fma(d, d, acc);
+      }
     }
   }
   acc = block_sum(acc, sh);
-  if (threadIdx.x == 0) parts[blockIdx.x] = acc;
-  if (last_block_done(counter) && threadIdx.x == 0) {
+  const unsigned int nb = gridDim.x * gridDim.y;
+  const unsigned int b = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0) parts[b] = acc;
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(counter, 1u) == nb - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
     double s = parts[0];
-    for (unsigned int b = 1; b < gridDim.x; ++b) s += parts[b];
+    for (unsigned int q = 1; q < nb; ++q) s += parts[q];
     out[0] = s;
+    *counter = 0u;
   }
 }
 
-static int residual_grid(int64_t n_loc) {
-  return int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_loc, 8), int64_t(num_sms()) * 4)));
+static void residual_grid(int64_t m, int64_t n_loc, dim3* grid, int64_t* chunk) {
+  if (m <= 0 || n_loc <= 0) {
+    *grid = dim3(1, 1, 1);
+    *chunk = 1;
+    return;
+  }
+  const int64_t rows = ceil_div(std::max<int64_t>(m, 1), 256);
+  const int64_t want = int64_t(num_sms()) * 8;
+  int64_t cs = std::max<int64_t>(1, std::min<int64_t>(ceil_div(want, rows), ceil_div(n_loc, 64)));
+  cs = std::min<int64_t>(cs, 65535);
+  *chunk = ceil_div(n_loc, cs);
+  *grid = dim3(unsigned(rows), unsigned(ceil_div(n_loc, *chunk)));
 }
 
 extern "C" int64_t bs_nmf_residual_workspace(int64_t m, int64_t n_loc) {
-  (void)m;
-  return ws_bytes<unsigned int>(1) + ws_bytes<double>(residual_grid(n_loc));
+  dim3 g;
+  int64_t c;
+  residual_grid(m, n_loc, &g, &c);
+  return ws_bytes<unsigned int>(1) + ws_bytes<double>(int64_t(g.x) * g.y);
 }
 
 extern "C" int bs_nmf_residual(const void* X, const void* Vt_full, const void* W, int dtype, int64_t m,
-                               int64_t n_loc, int r, double* out_dev, void* work, int64_t work_bytes,
-                               void* stream) {
+                               int64_t n_loc, int r, double* out_dev, const int* flag_dev, void* work,
+                               int64_t work_bytes, void* stream) {
   clear_error();
   cudaStream_t st = as_stream(stream);
   if (n_loc == 0 || m == 0)
     return cudaMemsetAsync(out_dev, 0, sizeof(double), st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  if (r < 1 || r > MAX_R) {
+    set_error("bs_nmf_residual: bad rank %d", r);
+    return BS_EINVAL;
+  }
   Workspace ws(work, work_bytes);
-  const int grid = residual_grid(n_loc);
+  dim3 grid;
+  int64_t chunk;
+  residual_grid(m, n_loc, &grid, &chunk);
   unsigned int* counter = ws.take<unsigned int>(1);
-  double* parts = ws.take<double>(grid);
+  double* parts = ws.take<double>(int64_t(grid.x) * grid.y);
   if (!counter || !parts) { set_error("bs_nmf_residual: workspace too small"); return BS_EWORK; }
-  if (dtype == BS_F64)
-    residual_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(X), static_cast<const double*>(Vt_full),
-                                                  static_cast<const double*>(W), m, n_loc, r, parts, counter,
-                                                  out_dev);
-  else if (dtype == BS_F32)
-    residual_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(X), static_cast<const float*>(Vt_full),
-                                                 static_cast<const float*>(W), m, n_loc, r, parts, counter,
-                                                 out_dev);
-  else {
+#define BS_RES(T, RPV)                                                                                          \
+  residual_kernel<T, RPV><<<grid, 256, 0, st>>>(static_cast<const T*>(X), static_cast<const T*>(Vt_full),      \
+                                                static_cast<const T*>(W), m, n_loc, r, chunk, parts, counter,  \
+                                                out_dev, flag_dev)
+  const int rp = r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 128;
+  if (dtype == BS_F64) {
+    switch (rp) {
+      case 16: BS_RES(double, 16); break;
+      case 32: BS_RES(double, 32); break;
+      case 64: BS_RES(double, 64); break;
+      default: BS_RES(double, 128); break;
+    }
+  } else if (dtype == BS_F32) {
+    switch (rp) {
+      case 16: BS_RES(float, 16); break;
+      case 32: BS_RES(float, 32); break;
+      case 64: BS_RES(float, 64); break;
+      default: BS_RES(float, 128); break;
+    }
+  } else {
     set_error("bs_nmf_residual: unsupported dtype %d", dtype);
     return BS_EINVAL;
   }
+#undef BS_RES
   return check_launch("bs_nmf_residual");
 }

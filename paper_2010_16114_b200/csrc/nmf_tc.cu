@@ -30,6 +30,10 @@
 
 using namespace bs;
 
+namespace bs {
+void note_gemm_path(int path);
+}
+
 namespace {
 
 using namespace tc;
@@ -429,12 +433,17 @@ int launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, int M, int K, int r,
     const char* e = getenv("BS_TC_GROUP");
     group = (e && atoi(e) > 0) ? atoi(e) : 4;
   });
+  // Work-skipping modes (bit 1: skip the A split, bit 2: skip the MMAs) exist only in
+  // debug builds (-DBS_DEBUG_MODES, used by scripts/nmf_modes.sh); the shipped library
+  // always runs the full kernel.
   static int mode = 0;
+#ifdef BS_DEBUG_MODES
   static std::once_flag m_once;
   std::call_once(m_once, [] {
     const char* e = getenv("BS_TC_MODE");
     mode = e ? atoi(e) : 0;
   });
+#endif
   if (grid_out) *grid_out = grid;
   tc_gemm_kernel<A_MN, NP><<<grid, TC_THREADS, C::SMEM, st>>>(ta, tb, M, K, r, tiles, kb_per, units, group, out, slab, mode,
                                                                stats_part);
@@ -521,6 +530,7 @@ int tc_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, floa
     rc = check_launch("tc_wxt fold");
     if (rc != BS_OK) return rc;
   }
+  note_gemm_path(1);
   *used = true;
   return BS_OK;
 }
@@ -549,6 +559,7 @@ int tc_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, flo
   int rc = check_launch("tc_vtx");
   if (rc != BS_OK) return rc;
   *splits = S;
+  note_gemm_path(1);
   *used = true;
   return BS_OK;
 }

@@ -371,9 +371,11 @@ struct bs_nmf {
   void* Vt;  // r x m_loc (caller)
   void* W;   // r x n_loc (caller)
   void *WXt, *P, *tmp;  // owned: r x m_loc; r x m (size > 1); r x m (size > 1)
-  double *red, *scan, *VtV;
-  void *ws_gram, *ws_wxt, *ws_scan, *ws_vt, *ws_w;
-  int64_t n_gram, n_wxt, n_scan, n_vt, n_w;
+  double *red, *scan, *VtV, *direct;  // scan: {min, sum X^2, nonfinite, scales ready, min Vt, min W}
+  int* guard;                          // objective cancellation flag (bs_nmf_objective)
+  void* xscale;                        // integer GEMM block scales (float32 X)
+  void *ws_gram, *ws_wxt, *ws_prep, *ws_vt, *ws_w, *ws_res, *ws_red;
+  int64_t n_gram, n_wxt, n_prep, n_vt, n_w, n_res, n_red;
 };
 
 namespace {
@@ -454,7 +456,9 @@ extern "C" int bs_nmf_state_create(bs_ctx_t ctx, const void* X, int dtype, int64
   const int64_t es = dtype == BS_F64 ? 8 : 4;
   s->n_gram = std::max<int64_t>(bs_gram_workspace(r, n_loc), 256);
   s->n_wxt = std::max<int64_t>(bs_nmf_wxt_workspace(dtype, m, n_loc, r), 256);
-  s->n_scan = std::max<int64_t>(bs_nmf_wxt_scan_workspace(dtype, m, n_loc, r), 256);
+  s->n_prep = std::max<int64_t>(bs_nmf_prepare_workspace(m, n_loc), 256);
+  s->n_res = std::max<int64_t>(bs_nmf_residual_workspace(m, n_loc), 256);
+  s->n_red = std::max<int64_t>(bs_reduce_workspace(std::max<int64_t>(r * std::max(s->m_loc, n_loc), 1)), 256);
   s->n_vt = std::max<int64_t>(bs_nmf_vt_step_workspace(r, s->m_loc), 256);
   s->n_w = std::max<int64_t>(bs_nmf_w_step_workspace(dtype, m, n_loc, r), 256);
   int rc = BS_OK;
@@ -468,11 +472,17 @@ extern "C" int bs_nmf_state_create(bs_ctx_t ctx, const void* X, int dtype, int64
     s->tmp = Vt;
   }
   rc |= dalloc(&p, 8 * (int64_t(r) * r + 1)); s->red = static_cast<double*>(p);
-  rc |= dalloc(&p, 16); s->scan = static_cast<double*>(p);
+  rc |= dalloc(&p, 64); s->scan = static_cast<double*>(p);
+  rc |= dalloc(&p, 16); s->direct = static_cast<double*>(p);
+  rc |= dalloc(&p, 16); s->guard = static_cast<int*>(p);
+  s->xscale = nullptr;
+  if (dtype == BS_F32) rc |= dalloc(&s->xscale, std::max<int64_t>(bs_nmf_xscale_bytes(m, n_loc), 16));
   rc |= dalloc(&p, 8 * int64_t(r) * r); s->VtV = static_cast<double*>(p);
   rc |= dalloc(&s->ws_gram, s->n_gram);
   rc |= dalloc(&s->ws_wxt, s->n_wxt);
-  rc |= dalloc(&s->ws_scan, s->n_scan);
+  rc |= dalloc(&s->ws_prep, s->n_prep);
+  rc |= dalloc(&s->ws_res, s->n_res);
+  rc |= dalloc(&s->ws_red, s->n_red);
   rc |= dalloc(&s->ws_vt, s->n_vt);
   rc |= dalloc(&s->ws_w, s->n_w);
   if (rc != BS_OK) {
@@ -488,7 +498,8 @@ extern "C" int bs_nmf_state_destroy(bs_nmf_t s) {
   clear_error();
   if (!s) return BS_OK;
   cudaSetDevice(s->ctx->device);
-  void* bufs[] = {s->WXt, s->red, s->scan, s->VtV, s->ws_gram, s->ws_wxt, s->ws_scan, s->ws_vt, s->ws_w};
+  void* bufs[] = {s->WXt,     s->red,     s->scan,    s->VtV,  s->direct, s->guard,  s->xscale,
+                  s->ws_gram, s->ws_wxt, s->ws_prep, s->ws_vt, s->ws_w,   s->ws_res, s->ws_red};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (s->ctx->size > 1) {
@@ -525,22 +536,32 @@ extern "C" int bs_nmf_run(bs_nmf_t s, int algo, int iters, int trace_every, doub
   // WWt of the entering W (scn d, solvers.py:151)
   if ((rc = bs_gram(s->W, s->dtype, r, s->n_loc, s->red, s->ws_gram, s->n_gram, st))) return done(rc);
   if ((rc = allreduce_f64(c, s->red, rr, ncclSum))) return done(rc);
+  // the X pass of this call (_nmf_check, solvers.py:139-141): min, sum X^2, integer-GEMM scales;
+  // the integer path also needs finite X and nonnegative factors (the solver keeps them so)
+  if ((rc = bs_nmf_prepare(s->X, s->dtype, s->m, s->n_loc, s->scan, s->xscale, s->ws_prep, s->n_prep, st)))
+    return done(rc);
+  if ((rc = bs_reduce(s->Vt, s->dtype, int64_t(r) * s->m_loc, BS_MIN, BS_T_NONE, s->scan + 4, s->ws_red, s->n_red,
+                      st)) ||
+      (rc = bs_reduce(s->W, s->dtype, int64_t(r) * s->n_loc, BS_MIN, BS_T_NONE, s->scan + 5, s->ws_red, s->n_red,
+                      st)))
+    return done(rc);
+  if ((rc = allreduce_f64(c, s->scan, 1, ncclMin)) || (rc = allreduce_f64(c, s->scan + 1, 1, ncclSum)) ||
+      (rc = allreduce_f64(c, s->scan + 2, 1, ncclMax)) || (rc = allreduce_f64(c, s->scan + 4, 2, ncclMin)))
+    return done(rc);
+  double h[6];
+  cudaMemcpyAsync(h, s->scan, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return done(BS_ECUDA);
+  if (!(s->n_loc == 0 && c->size == 1) && h[0] < 0) {
+    set_error("NMF requires nonnegative data");
+    return done(BS_EINVAL);
+  }
+  const bool use_i8 = h[3] == 1.0 && h[2] == 0.0 && h[4] >= 0.0 && h[5] >= 0.0;
+  const void* xs = use_i8 ? s->xscale : nullptr;
+  // Gram-identity guard (solvers.py _KAPPA_*): float64 1e6, integer path 16, 3xTF32 always direct
+  const double kappa = s->dtype == BS_F64 ? 1e6 : (use_i8 && r <= 64) ? 16.0 : -1.0;
   for (int it = 0; it < iters; ++it) {
-    if (it == 0) {  // scn b with the call's _nmf_check and ||X||^2 (solvers.py:139-141, 147)
-      if ((rc = bs_nmf_wxt_scan(s->X, s->W, s->dtype, s->m, s->n_loc, r, s->P, s->scan, s->ws_scan, s->n_scan, st)))
-        return done(rc);
-      if ((rc = allreduce_f64(c, s->scan, 1, ncclMin)) || (rc = allreduce_f64(c, s->scan + 1, 1, ncclSum)))
-        return done(rc);
-      double mn = 0.0;
-      cudaMemcpyAsync(&mn, s->scan, sizeof(double), cudaMemcpyDeviceToHost, st);
-      if (cudaStreamSynchronize(st) != cudaSuccess) return done(BS_ECUDA);
-      if (!(s->n_loc == 0 && c->size == 1) && mn < 0) {
-        set_error("NMF requires nonnegative data");
-        return done(BS_EINVAL);
-      }
-    } else if ((rc = bs_nmf_wxt(s->X, s->W, s->dtype, s->m, s->n_loc, r, s->P, s->ws_wxt, s->n_wxt, st))) {
+    if ((rc = bs_nmf_wxt(s->X, s->W, s->dtype, s->m, s->n_loc, r, s->P, xs, s->ws_wxt, s->n_wxt, st)))
       return done(rc);
-    }
     if (c->size > 1 && (rc = nmf_reduce_scatter(s))) return done(rc);
     // Vt half-step (solvers.py:152-156 / 173-176)
     if ((rc = bs_nmf_vt_step(algo, s->Vt, s->WXt, s->red, s->dtype, r, s->m_loc, s->eps, s->VtV, nullptr, s->ws_vt,
@@ -548,13 +569,18 @@ extern "C" int bs_nmf_run(bs_nmf_t s, int algo, int iters, int trace_every, doub
       return done(rc);
     if (c->size > 1 && ((rc = allreduce_f64(c, s->VtV, rr, ncclSum)) || (rc = nmf_allgather(s)))) return done(rc);
     // W half-step + next WWt + objective cross term (solvers.py:155-159 / 177-182)
-    if ((rc = bs_nmf_w_step(algo, s->X, s->tmp, s->W, s->VtV, s->dtype, s->m, s->n_loc, r, s->eps, s->red, s->ws_w,
-                            s->n_w, st)))
+    if ((rc = bs_nmf_w_step(algo, s->X, s->tmp, s->W, s->VtV, s->dtype, s->m, s->n_loc, r, s->eps, s->red, xs,
+                            s->ws_w, s->n_w, st)))
       return done(rc);
     if ((rc = allreduce_f64(c, s->red, rr + 1, ncclSum))) return done(rc);
-    if (trace_every && it % trace_every == 0 &&
-        (rc = bs_nmf_objective(s->scan + 1, s->red, s->VtV, r, trace_dev + it, st)))
-      return done(rc);
+    if (trace_every && it % trace_every == 0) {
+      if ((rc = bs_nmf_objective(s->scan + 1, s->red, s->VtV, r, trace_dev + it, s->guard, kappa, st)) ||
+          (rc = bs_nmf_residual(s->X, s->tmp, s->W, s->dtype, s->m, s->n_loc, r, s->direct, s->guard, s->ws_res,
+                                s->n_res, st)) ||
+          (rc = allreduce_f64(c, s->direct, 1, ncclSum)) ||
+          (rc = bs_nmf_objective_select(s->guard, s->direct, trace_dev + it, st)))
+        return done(rc);
+    }
   }
   std::vector<double> tr(size_t(iters), 0.0);
   cudaMemcpyAsync(tr.data(), trace_dev, sizeof(double) * size_t(iters), cudaMemcpyDeviceToHost, st);

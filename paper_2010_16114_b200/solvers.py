@@ -193,7 +193,7 @@ def nmf_init(x, rank, seed=None, eps=1e-10):
              if comm.size > 1 else None),
         eps=eps,
     )
-    state._dev = {"red": red, "scan": _dev_f64(2, dev)}
+    state._dev = {"red": red, "scan": _dev_f64(6, dev)}
     state._work = _Work(dev)
     return state
 
@@ -205,33 +205,70 @@ def _gather_factor(a, out):
     a.comm.allgatherv(_flat_local(a), out.t().reshape(-1) if out.ndim == 2 else out, counts)
 
 
-def _nmf_check_and_norm(s):
-    """_nmf_check (solvers.py:139-141) fused with ||X||^2 for the objective."""
-    x = s.X
-    flat = _flat_local(x)
-    scan = s._dev["scan"]
-    wp, wn = s._work.args("scan", 16 * 4096)
-    _lib.call("bs_nmf_scan", _lib.ptr(flat), _lib.dtype_code(flat.dtype), flat.numel(), _lib.ptr(scan), wp, wn,
-              _lib.stream_ptr())
-    _nmf_check_result(s)
+# Cancellation guard of the Gram-identity objective (bs_nmf_objective): when
+# ||X||^2 / obj exceeds kappa, the trace value is replaced by the reference's own
+# direct residual (solvers.py:124-136).  The bound follows each GEMM path's error:
+# the integer digit-slice path (exact int32 accumulation, symmetric rounding,
+# ~1e-7 relative) and float64 stay within 1e-6 of the direct value up to these
+# ratios; the 3xTF32 path's accumulator truncates (biased ~2e-6), so it always
+# takes the direct residual.
+_KAPPA_I8 = 16.0
+_KAPPA_F64 = 1e6
+_KAPPA_ALWAYS = -1.0
 
 
-def _nmf_check_result(s):
-    """Reduces the (min, ||X||^2) scan over ranks and raises like solvers.py:139-141."""
+def gemm_path_counts(reset=False):
+    """How many NMF GEMMs (scn a / scn b) ran on each path since the last reset (bs_gemm_path_counts).
+
+    Keys: ``integer`` (tcgen05 kind::i8 digit slices), ``tf32`` (tcgen05 3xTF32),
+    ``cuda_core`` (float32 CUDA cores), ``float64`` (DMMA / CUDA cores); ``tensor`` = the
+    first two together.
+    """
+    import ctypes as C
+
+    buf = (C.c_int64 * 4)()
+    _lib.call("bs_gemm_path_counts", buf, 1 if reset else 0)
+    d = {"integer": buf[0], "tf32": buf[1], "cuda_core": buf[2], "float64": buf[3]}
+    d["tensor"] = d["integer"] + d["tf32"]
+    return d
+
+
+def _nmf_prepare(s):
+    """The call's X pass (_nmf_check, solvers.py:139-141) + ||X||^2 + the integer GEMMs' block scales.
+
+    Returns True when the float32 GEMMs may run on the integer digit-slice path:
+    scales prepared, X finite and both factors nonnegative (the solver keeps them so).
+    """
+    torch = _torch()
     x = s.X
     comm = x.comm
-    scan = s._dev["scan"]
+    m = x.shape[0]
+    n_loc = x.local.shape[1]
+    flat = _flat_local(x)
+    stats = s._dev["scan"]
+    xs = None
+    if x.dtype == np.float32:
+        nb = _lib.query("bs_nmf_xscale_bytes", m, n_loc)
+        xs = s._dev.get("xscale")
+        if xs is None or xs.numel() < nb:
+            xs = torch.empty(max(nb, 16), dtype=torch.uint8, device=comm.device)
+            s._dev["xscale"] = xs
+    wp, wn = s._work.args("prep", _lib.query("bs_nmf_prepare_workspace", m, n_loc))
+    _lib.call("bs_nmf_prepare", _lib.ptr(flat), _lib.dtype_code(flat.dtype), m, n_loc, _lib.ptr(stats),
+              _lib.ptr(xs), wp, wn, _lib.stream_ptr())
+    local_reduce(s.Vt.local, ReduceOp.MIN, out=stats[4:5])
+    local_reduce(s.W.local, ReduceOp.MIN, out=stats[5:6])
     if comm.size > 1:
-        mn = scan[0:1].clone()
-        comm.allreduce(mn, ReduceOp.MIN)
-        sq = scan[1:2].clone()
+        mins = torch.stack([stats[0], stats[4], stats[5], -stats[2]])
+        comm.allreduce(mins, ReduceOp.MIN)
+        sq = stats[1:2].clone()
         comm.allreduce(sq, ReduceOp.SUM)
-        scan[0:1].copy_(mn)
-        scan[1:2].copy_(sq)
-    if x.local.numel() == 0 and comm.size == 1:
-        return
-    if float(scan[0].item()) < 0:
+        stats[0], stats[4], stats[5], stats[2] = mins[0], mins[1], mins[2], -mins[3]
+        stats[1:2].copy_(sq)
+    host = stats.cpu().numpy()
+    if not (x.local.numel() == 0 and comm.size == 1) and host[0] < 0:
         raise ValueError("NMF requires nonnegative data")
+    return bool(host[3] == 1.0 and host[2] == 0.0 and host[4] >= 0.0 and host[5] >= 0.0)
 
 
 def _nmf_run(s, iters, trace_every, algo):
@@ -243,13 +280,14 @@ def _nmf_run(s, iters, trace_every, algo):
     code = _lib.dtype_code(x.dtype)
     m_loc = s.Vt.local.shape[1]
     n_loc = x.local.shape[1]
+    use_i8 = _nmf_prepare(s)
     if iters <= 0:
-        _nmf_check_and_norm(s)
         return s
     st = _lib.stream_ptr()
     dev = comm.device
     red = s._dev["red"]
     xsq = s._dev["scan"][1:2]
+    xs = s._dev.get("xscale") if use_i8 else None
     VtV = s.VtV.reshape(-1)
     Xf = _flat_local(x)
     Wl = _flat_local(s.W)
@@ -272,21 +310,26 @@ def _nmf_run(s, iters, trace_every, algo):
         tmp = Vtl
     WXt_loc = _flat_local(s.WXt)
     trace_dev = _dev_f64(iters, dev)
+    guard = s._dev.get("guard")
+    if guard is None:
+        guard = torch.zeros(2, dtype=torch.int32, device=dev)
+        s._dev["guard"] = guard
+    direct = s._dev["direct"] if "direct" in s._dev else _dev_f64(1, dev)
+    s._dev["direct"] = direct
+    if x.dtype == np.float64:
+        kappa = _KAPPA_F64
+    elif use_i8 and r <= 64:
+        kappa = _KAPPA_I8
+    else:
+        kappa = _KAPPA_ALWAYS
     xp, xn = s._work.args("wxt", _lib.query("bs_nmf_wxt_workspace", code, m, n_loc, r))
-    sp, sn = s._work.args("wxt_scan", _lib.query("bs_nmf_wxt_scan_workspace", code, m, n_loc, r))
-    scan = s._dev["scan"]
     vp, vn = s._work.args("vt", _lib.query("bs_nmf_vt_step_workspace", r, m_loc))
     wp, wn = s._work.args("w", _lib.query("bs_nmf_w_step_workspace", code, m, n_loc, r))
+    rp, rn = s._work.args("resid", _lib.query("bs_nmf_residual_workspace", m, n_loc))
     eps = float(s.eps)
     for it in range(iters):
-        # WXt = W X^T (scn b) and its reduce-scatter (distlinalg.py:246-252).  The first
-        # iteration's pass also performs the call's _nmf_check and ||X||^2 (solvers.py:147).
-        if it == 0:
-            _lib.call("bs_nmf_wxt_scan", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), _lib.ptr(scan),
-                      sp, sn, st)
-            _nmf_check_result(s)
-        else:
-            _lib.call("bs_nmf_wxt", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), xp, xn, st)
+        # WXt = W X^T (scn b) and its reduce-scatter (distlinalg.py:246-252)
+        _lib.call("bs_nmf_wxt", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), _lib.ptr(xs), xp, xn, st)
         if comm.size > 1:
             comm.reduce_scatterv(P[:r * m], WXt_loc, mcounts)
         # Vt half-step (solvers.py:152-156 / 173-176)
@@ -297,11 +340,20 @@ def _nmf_run(s, iters, trace_every, algo):
             comm.allgatherv(Vtl, tmp, mcounts)
         # W half-step + next WWt + objective cross term (solvers.py:155-159 / 177-182)
         _lib.call("bs_nmf_w_step", algo, _lib.ptr(Xf), _lib.ptr(tmp), _lib.ptr(Wl), _lib.ptr(VtV), code, m,
-                  n_loc, r, eps, _lib.ptr(red), wp, wn, st)
+                  n_loc, r, eps, _lib.ptr(red), _lib.ptr(xs), wp, wn, st)
         if comm.size > 1:
             comm.allreduce(red, ReduceOp.SUM)
         if trace_every and it % trace_every == 0:
-            _lib.call("bs_nmf_objective", _lib.ptr(xsq), _lib.ptr(red), _lib.ptr(VtV), r, _at(trace_dev, it), st)
+            tr = _at(trace_dev, it)
+            _lib.call("bs_nmf_objective", _lib.ptr(xsq), _lib.ptr(red), _lib.ptr(VtV), r, tr, _lib.ptr(guard),
+                      kappa, st)
+            # cancellation regime: the reference's direct residual (solvers.py:124-136), skipped on the
+            # device when the guard is clear
+            _lib.call("bs_nmf_residual", _lib.ptr(Xf), _lib.ptr(tmp), _lib.ptr(Wl), code, m, n_loc, r,
+                      _lib.ptr(direct), _lib.ptr(guard), rp, rn, st)
+            if comm.size > 1:
+                comm.allreduce(direct, ReduceOp.SUM)
+            _lib.call("bs_nmf_objective_select", _lib.ptr(guard), _lib.ptr(direct), tr, st)
     if trace_every:
         vals = trace_dev.cpu().numpy()
         s.trace.extend(float(vals[it]) for it in range(iters) if it % trace_every == 0)
@@ -336,7 +388,7 @@ def nmf_objective(x, vt, w, state=None):
     n_loc = x.local.shape[1]
     wp, wn = work.args("resid", _lib.query("bs_nmf_residual_workspace", m, n_loc))
     _lib.call("bs_nmf_residual", _lib.ptr(_flat_local(x)), _lib.ptr(full), _lib.ptr(_flat_local(w)), code, m, n_loc,
-              r, _lib.ptr(out), wp, wn, _lib.stream_ptr())
+              r, _lib.ptr(out), None, wp, wn, _lib.stream_ptr())
     if comm.size > 1:
         comm.allreduce(out, ReduceOp.SUM)
     return float(out.item())

@@ -32,8 +32,8 @@ def _wxt(x, w):
     W = _t(w.T)            # memory [j][k]
     P = torch.empty(m * r, dtype=torch.float32, device="cuda")
     ws = torch.zeros(_lib.query("bs_nmf_wxt_workspace", _lib.BS_F32, m, n, r), dtype=torch.uint8, device="cuda")
-    _lib.call("bs_nmf_wxt", _lib.ptr(X), _lib.ptr(W), _lib.BS_F32, m, n, r, _lib.ptr(P), _lib.ptr(ws), ws.numel(),
-              _lib.stream_ptr())
+    _lib.call("bs_nmf_wxt", _lib.ptr(X), _lib.ptr(W), _lib.BS_F32, m, n, r, _lib.ptr(P), None, _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
     return P.cpu().numpy().reshape(m, r).T
 
 
