@@ -273,18 +273,29 @@ def _bytes_per_launch(kernel, wl, comm, data):
     return int(local.numel()) * local.element_size()
 
 
-def _run_b200(args, wl):
+def _config(wl, n_gpus, steps):
+    """The workload description both arms print verbatim (the driver compares the two)."""
+    if wl["kind"] == "mds":
+        per_gpu = wl["n"] * -(-wl["n"] // n_gpus) * np.dtype(wl["dtype"]).itemsize
+    elif wl.get("storage") == "u2":
+        per_gpu = -(-wl["m"] // 64) * 16 * -(-wl["n"] // n_gpus)
+    else:
+        per_gpu = wl["m"] * -(-wl["n"] // n_gpus) * np.dtype(wl["dtype"]).itemsize
+    return {"workload": wl["desc"], "iterations_timed": steps, "trace_every": 1,
+            "partition": f"columns of the data matrix split over {n_gpus} GPU(s) (partition_of)",
+            "l2_flush": f"inputs ({per_gpu / 1e9:.1f} GB per GPU) exceed the 126 MB L2"}
+
+
+def _measure(comm, wl, steps, warmup):
+    """W untimed warm-up iterations, then K timed ones bracketed by barriers (max over ranks)."""
     import torch
 
-    import paper_2010_16114_b200 as bs
     from paper_2010_16114_b200 import _lib
 
-    comm = _world()
     st, step, kernels, data = _setup(comm, wl)
     _barrier(comm)
-    step(args.warmup)  # W untimed warm-up iterations (one call, like a user would)
+    step(warmup)  # untimed warm-up iterations (one call, like a user would)
     _barrier(comm)
-    # ---- timed: K iterations through the public API, inputs resident in HBM ----
     launches0 = _lib.load().bs_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -292,50 +303,96 @@ def _run_b200(args, wl):
     with Clocks(dev_index) as clk, _lib.profile(kernels) as prof:
         _barrier(comm)
         ev0.record()
-        step(args.steps)
+        step(steps)
         ev1.record()
         _barrier(comm)
     launches = _lib.load().bs_launch_count() - launches0
-    ms = ev0.elapsed_time(ev1)
-    ms = _max_over_ranks(comm, ms)
+    ms = _max_over_ranks(comm, ev0.elapsed_time(ev1))
     per = prof.elapsed_ms()
     tot = {k: float(np.sum(v)) for k, v in per.items() if v}
     dom = max(tot, key=tot.get)
-    avg_ms = float(np.mean(per[dom]))
+    avg_ms = _max_over_ranks(comm, float(np.mean(per[dom])))
     bytes_launch = _bytes_per_launch(dom, wl, comm, data)
-    avg_ms = _max_over_ranks(comm, avg_ms)
     peak, peak_kind = _peaks()
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
-    value = args.steps / (ms * 1e-3)
-    out = {
-        "metric": "iterations/sec", "value": value, "unit": "it/s", "n_gpus": comm.size,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": _arith_dtype(wl), "data": "synthetic (numpy-exact Philox rand_fill on device)" if wl["kind"] != "cox"
-        else "synthetic (device normal/genotype draws)",
-        "config": {"workload": wl["desc"], "iterations_timed": args.steps, "trace_every": 1,
-                   "partition": f"columns of X split over {comm.size} GPU(s) (partition_of)",
-                   "l2_flush": f"inputs ({data.local.numel() * data.local.element_size() / 1e9:.1f} GB per GPU) "
-                               "exceed the 126 MB L2"},
+    res = {
+        "value": steps / (ms * 1e-3), "ms_per_step": ms / steps,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
-                     "avg_launch_ms": avg_ms,
-                     "share_of_step": tot[dom] / ms},
-        "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+                     "avg_launch_ms": avg_ms, "share_of_step": tot[dom] / ms},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    return res, st, step, data
+
+
+def _free(*objs):
+    import gc
+
+    import torch
+
+    del objs
+    gc.collect()
+    torch.cuda.empty_cache()
+
+
+EXTRAS = ("nmf_mu_c1", "mds_c3", "cox_c4", "cox_c5")
+
+
+def _run_b200(args, wl):
+    import paper_2010_16114_b200 as bs  # noqa: F401
+
+    comm = _world()
+    res, st, step, data = _measure(comm, wl, args.steps, args.warmup)
+    out = {
+        "metric": "iterations/sec", "value": res["value"], "unit": "it/s", "n_gpus": comm.size,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": _arith_dtype(wl), "data": _data_desc(wl),
+        "config": _config(wl, comm.size, args.steps),
+        "roofline": res["roofline"], "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
     }
     if comm.rank == 0 and comm.size == 1 and not args.no_cpu:
-        out["cpu_baseline"] = _cpu_baseline(wl, samples=1)
+        out["cpu_baseline"] = _cpu_baseline(wl, steps=1)
     if not args.no_e2e:
         try:
             out["e2e"] = _e2e(args, wl, comm, st, step, data)
         except Exception as exc:  # noqa: BLE001 - report, do not lose the kernel numbers
             out["e2e"] = {"value": None, "unit": "it/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
+    _free(st, step, data)
+    st = step = data = None
+    if not args.no_extra:
+        # the other BASELINE configs, measured in the same run (same timing rules, fewer steps)
+        extra = {}
+        for key in EXTRAS:
+            if key == wl["key"]:
+                continue
+            w2 = dict(WORKLOADS[key], key=key)
+            k2 = 20 if key == "nmf_mu_c1" else 5
+            try:
+                r2, st2, step2, data2 = _measure(comm, w2, k2, 3)
+                extra[key] = {"workload": w2["desc"], "value": r2["value"], "unit": "it/s",
+                              "ms_per_step": r2["ms_per_step"], "steps": k2, "warmup": 3,
+                              "dtype": _arith_dtype(w2), "data": _data_desc(w2), "roofline": r2["roofline"],
+                              "gpu_launches": r2["gpu_launches"], "clocks": r2["clocks"]}
+                _free(st2, step2, data2)
+                st2 = step2 = data2 = None
+            except Exception as exc:  # noqa: BLE001
+                extra[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                _free()
+        out["workloads"] = extra
     if comm.rank == 0:
         print(json.dumps(out), flush=True)
     comm.barrier()
     comm.close()
+
+
+def _data_desc(wl):
+    if wl["kind"] == "cox" and wl["dtype"] != "int8":
+        return "synthetic (device normal draws)"
+    if wl["kind"] == "cox":
+        return "synthetic (counter-based Philox genotypes, rank-count independent)"
+    return "synthetic (numpy-exact Philox rand_fill on device)"
 
 
 def _arith_dtype(wl):
@@ -388,109 +445,145 @@ def _e2e(args, wl, comm, st, step, data):
 # CPU legs: the oracle port of the reference algorithm on the host cores
 # ---------------------------------------------------------------------------
 
-
-def _cpu_sample(wl):
-    """A bounded sample of the workload for the host (same aspect, ~seconds per iteration)."""
-    if wl["kind"] == "nmf":
-        f = 10 if wl["m"] * wl["n"] > 5e8 else 1
-        return dict(m=wl["m"] // f, n=wl["n"] // f)
-    if wl["kind"] == "cox":
-        f = 10 if wl["m"] * wl["n"] > 5e8 else 1
-        return dict(m=wl["m"] // f, n=wl["n"] // f)
-    return dict(n=5000, d=wl["d"])
+NMF_BLOCK_COLS = 1000
 
 
-def _cpu_baseline(wl, samples=1):
-    """The oracle leg with every host core given to BLAS (torchrun exports
-    OMP_NUM_THREADS=1 to its workers; the reference arm should not inherit that)."""
-    cores = _cores()
-    try:
-        from threadpoolctl import threadpool_info, threadpool_limits
-    except ImportError:  # pragma: no cover
-        return _cpu_baseline_run(wl, samples)
-    with threadpool_limits(limits=cores):
-        out = _cpu_baseline_run(wl, samples)
-        used = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
-    out["threads"] = f"BLAS {used[0] if used else '?'} of {cores} cores"
-    return out
+def _ref_sample(wl):
+    """A bounded, exactly-defined sample of one iteration of the workload for the host.
 
-
-def _cpu_baseline_run(wl, samples=1):
+    NMF: the reference iteration is column-separable (scn b sums W_blk X_blk^T, scn a and
+    the W update are per column, the objective is a sum over columns; distlinalg.py:239-252,
+    solvers.py:124-185), so one step = one APG/MU iteration of the oracle on the first
+    NMF_BLOCK_COLS columns of THE C2 matrix (the exact rand_fill stream, full m rows) with
+    the matching columns of the nmf_init factors, and the full-iteration time is
+    (n / NMF_BLOCK_COLS) x the block time.  That counts the r x m Vt half-step (1-2 % of a
+    block iteration) n/NMF_BLOCK_COLS times, i.e. it slightly overstates the reference's time.
+    Cox / MDS: a same-aspect shape scaled down per element (labelled below).
+    Returns (step() -> None, fraction of one full iteration per step, description).
+    """
     from oracle import blockstat_oracle as orc
 
-    s = _cpu_sample(wl)
-    cores = _cores()
     if wl["kind"] == "nmf":
-        m, n, r = s["m"], s["n"], wl["r"]
+        m, n, r = wl["m"], wl["n"], wl["r"]
         dt = np.float32 if wl["dtype"] == "float32" else np.float64
-        x = np.random.Generator(np.random.Philox(2010)).random((m, n), dtype=dt)
-        vt, w = orc.nmf_init(x, r, 2011)
+        nb = min(n, NMF_BLOCK_COLS)
+        x = np.random.Generator(np.random.Philox(2010)).random(m * nb, dtype=dt).reshape((m, nb), order="F")
+        vt = np.random.Generator(np.random.Philox(2011)).random(r * m, dtype=dt).reshape((r, m), order="F")
+        w = np.random.Generator(np.random.Philox(2012)).random(r * nb, dtype=dt).reshape((r, nb), order="F")
         fn = orc.nmf_apg if wl["algo"] == "apg" else orc.nmf_multiplicative
-        fn(x, vt, w, 1)
-        t0 = time.perf_counter()
-        fn(x, vt, w, samples)
-        dt_s = (time.perf_counter() - t0) / samples
-        scale = (m * n) / (wl["m"] * wl["n"])
-        desc = f"oracle nmf_{wl['algo']} on a {m}x{n} rank-{r} {np.dtype(dt).name} sample, objective every " \
-               f"iteration; it/s scaled by elements ({scale:.3g})"
-    elif wl["kind"] == "cox":
-        m, n = s["m"], s["n"]
+        state = [vt, w]
+
+        def step():
+            state[0], state[1], _ = fn(x, state[0], state[1], 1)
+
+        return step, nb / n, (f"oracle nmf_{wl['algo']} iteration (objective traced) on columns 0..{nb - 1} of the "
+                              f"{m}x{n} matrix ({m}x{nb} {np.dtype(dt).name}, the exact rand_fill stream) with the "
+                              f"matching nmf_init factor columns; full iteration = {n // nb} x this block")
+    if wl["kind"] == "cox":
+        f = 10 if wl["m"] * wl["n"] > 5e8 else 1
+        m, n = wl["m"] // f, wl["n"] // f
         gen = np.random.Generator(np.random.Philox(2012))
         if wl["dtype"] != "int8":
             x = gen.standard_normal((m, n), dtype=np.float32)
             delta = (gen.random(m) > 0.3).astype(np.float32)
             cuts = np.arange(m)
-        else:  # genotypes, tied times (Breslow cuts, solvers.py:332-334), 4.5% events
+        else:
             x = orc.genotype_fill(m, n, 2016).astype(np.float32)
             delta = (gen.random(m) < 0.045).astype(np.float32)
             y = np.floor(np.arange(m, 0, -1, dtype=np.float64) / 4.0)
             cuts = np.searchsorted(-y, -y, side="right") - 1
-        orc.cox_fit(x, delta, cuts, wl["lam"], 1e-7, 1)
-        t0 = time.perf_counter()
-        orc.cox_fit(x, delta, cuts, wl["lam"], 1e-7, samples)
-        dt_s = (time.perf_counter() - t0) / samples
-        scale = (m * n) / (wl["m"] * wl["n"])
-        desc = f"oracle cox_fit on a {m}x{n} float32 sample; it/s scaled by elements ({scale:.3g})"
-    else:
-        n, d = s["n"], s["d"]
-        pts = np.random.Generator(np.random.Philox(2014)).random((d, n), dtype=np.float32).astype(np.float64)
-        g = pts.T @ pts
-        nr = np.diag(g)
-        y = np.sqrt(np.maximum(nr[:, None] + nr[None, :] - 2 * g, 0))
-        np.fill_diagonal(y, 0)
-        th = orc.mds_init(y, wl["q"], 2015)
-        orc.mds_fit(y, th, 1)
-        t0 = time.perf_counter()
-        orc.mds_fit(y, th, samples)
-        dt_s = (time.perf_counter() - t0) / samples
-        scale = (n * n) / (wl["n"] * wl["n"])
-        desc = f"oracle mds_fit on n={n} points (q={wl['q']}); it/s scaled by pairs ({scale:.3g})"
-    return {"value": scale / dt_s, "unit": "it/s", "cores": cores, "kind": "port",
-            "sample": desc, "sample_seconds_per_iteration": dt_s,
-            "threads": os.environ.get("OPENBLAS_NUM_THREADS", f"default ({cores})")}
+        state = [None]
+
+        def step():
+            state[0], _, _ = orc.cox_fit(x, delta, cuts, wl["lam"], 1e-7, 1, beta0=state[0])
+
+        return step, (m * n) / (wl["m"] * wl["n"]), (f"oracle cox_fit iteration on a {m}x{n} float32 same-aspect "
+                                                      f"sample; per-element extrapolation")
+    n, d = 5000, wl["d"]
+    pts = np.random.Generator(np.random.Philox(2014)).random((d, n), dtype=np.float32).astype(np.float64)
+    g = pts.T @ pts
+    nr = np.diag(g)
+    yv = np.sqrt(np.maximum(nr[:, None] + nr[None, :] - 2 * g, 0))
+    np.fill_diagonal(yv, 0)
+    state = [orc.mds_init(yv, wl["q"], 2015)]
+
+    def step():
+        state[0], _ = orc.mds_fit(yv, state[0], 1)
+
+    return step, (n * n) / (wl["n"] * wl["n"]), (f"oracle mds_fit iteration on n={n} points (q={wl['q']}); "
+                                                  f"per-pair extrapolation")
+
+
+def _with_all_cores(fn):
+    """Run with every host core given to BLAS (torchrun exports OMP_NUM_THREADS=1 to its workers)."""
+    cores = _cores()
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+    except ImportError:  # pragma: no cover
+        return fn(), f"default ({cores})"
+    with threadpool_limits(limits=cores):
+        out = fn()
+        used = [p.get("num_threads") for p in threadpool_info() if p.get("user_api") == "blas"]
+    return out, f"BLAS {used[0] if used else '?'} of {cores} cores"
+
+
+def _cpu_baseline(wl, steps=1, warmup=1):
+    """Times `steps` sample steps after `warmup` untimed ones; returns the extrapolated it/s."""
+
+    def run():
+        step, frac, desc = _ref_sample(wl)
+        for _ in range(max(warmup, 0)):
+            step()
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            step()
+            times.append(time.perf_counter() - t0)
+        return times, frac, desc
+
+    (times, frac, desc), threads = _with_all_cores(run)
+    per = float(np.mean(times))
+    return {"value": frac / per, "unit": "it/s", "cores": _cores(), "kind": "port", "sample": desc,
+            "sample_seconds_per_step": per, "sample_fraction_of_iteration": frac, "extrapolated": frac < 1.0,
+            "threads": threads}
 
 
 def _run_reference(args, wl):
+    """The reference arm: the oracle port of blockstat's algorithm on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return
-    for _ in range(max(args.warmup, 0)):
-        pass  # the oracle warms up inside _cpu_baseline (one untimed iteration)
     t0 = time.perf_counter()
-    base = _cpu_baseline(wl, samples=max(args.steps, 1))
+    base = _cpu_baseline(wl, steps=max(args.steps, 1), warmup=max(args.warmup, 0))
     wall = time.perf_counter() - t0
     out = {
         "impl": "reference", "metric": "iterations/sec", "value": base["value"], "unit": "it/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / base["value"], "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": _arith_dtype(wl), "data": "synthetic",
-        "config": {"workload": wl["desc"], "iterations_timed": args.steps},
-        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        # the measured per-step time of the bounded sample (what the timed region really took)
+        "ms_per_step": 1e3 * base["sample_seconds_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": _arith_dtype(wl), "data": "synthetic (the same generators, drawn on the host)",
+        "config": _config(wl, world, args.steps),
+        "extrapolated": base["extrapolated"],
+        "sample_fraction_of_iteration": base["sample_fraction_of_iteration"],
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample", "threads")},
         "e2e": {"value": base["value"], "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
     print(json.dumps(out), flush=True)
+
+
+def _self_launch(args, argv):
+    """--gpus N without a torchrun environment: launch N ranks of this script (one per GPU)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
 
 
 def main(argv=None):
@@ -502,7 +595,14 @@ def main(argv=None):
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="nmf_apg_c2")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end leg")
+    ap.add_argument("--no-extra", action="store_true", help="skip the other BASELINE configs (workloads key)")
+    argv = sys.argv[1:] if argv is None else list(argv)
     args = ap.parse_args(argv)
+    world = os.environ.get("WORLD_SIZE")
+    if args.impl == "b200" and world is None and args.gpus > 1:
+        sys.exit(_self_launch(args, argv))
+    if args.impl == "b200" and world is not None and int(world) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     wl = dict(WORKLOADS[args.workload], key=args.workload)

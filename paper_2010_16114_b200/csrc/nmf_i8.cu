@@ -59,12 +59,17 @@ constexpr int BM = 128;
 constexpr int BK = 32;
 constexpr int G = 16;               // k-blocks per scale group = accumulation run
 constexpr int GROUP = G * BK;       // 512 K values
-constexpr int THREADS = 448;        // producer, MMA, 4 epilogue warps, 2 x 4 converter warps
+constexpr int THREADS = 480;        // X producer, MMA, 4 epilogue warps, 2 x 4 converter warps, B producer
 constexpr int RAW_BYTES = BM * BK * 4;   // 16 KB fp32 tile
 constexpr int PLANE = BM * BK;           // 4 KB: one digit plane of the A tile
 constexpr int A_BYTES = 3 * PLANE;
-constexpr int RS = 6, BS = 4, CS = 4;
-constexpr int8_t EXP_BAD = -128;    // factor group holds a nonfinite / negative value
+#ifndef I8_RS
+#define I8_RS 7
+#endif
+#ifndef I8_BS
+#define I8_BS 6
+#endif
+constexpr int RS = I8_RS, BS = I8_BS, CS = 4;
 
 // scale exponent for a block whose largest |value| has float bits `bits`:
 // t = 149 - E puts the maximum in [2^22, 2^23) (N <= 2^23 after rounding).
@@ -73,6 +78,16 @@ __host__ __device__ __forceinline__ int exp_code(uint32_t bits) {
   return min(149 - e, 126);
 }
 __device__ __forceinline__ float pow2f(int t) { return __int_as_float((127 + t) << 23); }
+
+// (x0, x1) * m + 2^23 for two values at once (packed f32x2 FMA)
+__device__ __forceinline__ void fma2_shift(uint32_t& a, uint32_t& b, float m) {
+  uint64_t v = (uint64_t(b) << 32) | a, r;
+  const uint64_t mm = (uint64_t(__float_as_uint(m)) << 32) | __float_as_uint(m);
+  const uint64_t cc = (uint64_t(0x4B000000u) << 32) | 0x4B000000u;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(v), "l"(mm), "l"(cc));
+  a = uint32_t(r);
+  b = uint32_t(r >> 32);
+}
 
 // canonical K-major SWIZZLE_NONE operand: core matrix = 8 rows x 16 B, K chunk stride 128 B,
 // 8-row group stride 256 B (probed: scripts/i8_probe.cu)
@@ -236,12 +251,13 @@ __global__ void __launch_bounds__(1024) prep_fold_kernel(const double* __restric
 // ---------------------------------------------------------------------------
 // Factor slicing: F (r x K, column-major: F[k + r i]) -> per 32-wide k-block a
 // digit image [plane][NP rows][32 B] in the canonical K-major layout (what the MMA
-// reads as B = [B0|B1|B2]) and per (group, k) scale codes.  CTA = one 512-wide group.
+// reads as B = [B0|B1|B2]) and per (group, k) unscaling factors 2^(16 - t) (NaN when
+// the group holds a nonfinite or negative value).  CTA = one 512-wide group.
 // ---------------------------------------------------------------------------
 
 template <int NP>
 __global__ void __launch_bounds__(256) fslice_kernel(const float* __restrict__ F, int r, int64_t K,
-                                                     uint8_t* __restrict__ img, int8_t* __restrict__ fexp) {
+                                                     uint8_t* __restrict__ img, float* __restrict__ fmul) {
   extern __shared__ __align__(16) uint8_t simg[];  // G k-blocks x 3 NP x 32 B
   constexpr int KB_BYTES = 3 * NP * BK;
   __shared__ uint32_t kmax[NP], kbad[NP];
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(256) fslice_kernel(const float* __restrict__ F
   for (int k = t; k < NP; k += 256) {
     int code = k < r ? exp_code(kmax[k]) : 0;
     const bool bad = k < r && kbad[k];
-    fexp[g * NP + k] = bad ? EXP_BAD : int8_t(code);
+    fmul[g * NP + k] = bad ? CUDART_NAN_F : pow2f(16 - code);  // the epilogue's unscaling factor
     kmul[k] = bad ? 0.f : pow2f(code);
   }
   __syncthreads();
@@ -321,7 +337,7 @@ struct I8Cfg {
 template <bool A_MN, int NP>
 __global__ void __launch_bounds__(THREADS, 1)
 i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restrict__ bimg,
-               const int8_t* __restrict__ xexp, int64_t ldx, const int8_t* __restrict__ fexp, int M, int K, int r,
+               const int8_t* __restrict__ xexp, int64_t ldx, const float* __restrict__ fmul, int M, int K, int r,
                int tiles, int kb_per_split, int units, float* __restrict__ out, int64_t slab) {
   using C = I8Cfg<NP>;
   extern __shared__ uint8_t smem_raw[];
@@ -362,30 +378,34 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ---------------- producer ----------------
+  if (warp == 0 || warp == 14) {
+    // ---------------- producers: X tiles (warp 0) and factor digit images (warp 14) ----------------
     if (lane == 0) {
-      int rs = 0, bs = 0;
-      uint32_t rph = 0, bph = 0;
+      int st = 0;
+      uint32_t ph = 0;
+      const bool xprod = warp == 0;
+      const int S = xprod ? RS : BS;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int split = u / tiles, tile = u - split * tiles;
         const int kb0 = split * kb_per_split, kb1 = min(kb_total, kb0 + kb_per_split);
         const int m0 = tile * BM;
         for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(raw_empty(rs), rph ^ 1);
-          mbar_expect_tx(raw_full(rs), RAW_BYTES);
-          const uint32_t dst = smem_u32(smem + rs * RAW_BYTES);
-          if constexpr (A_MN) {
+          if (xprod) {
+            mbar_wait_sleep(raw_empty(st), ph ^ 1);
+            mbar_expect_tx(raw_full(st), RAW_BYTES);
+            const uint32_t dst = smem_u32(smem + st * RAW_BYTES);
+            if constexpr (A_MN) {
 #pragma unroll
-            for (int a = 0; a < BM / 32; ++a) tma_load_2d(dst + a * 4096, &tmA, m0 + 32 * a, kb * BK, raw_full(rs));
+              for (int a = 0; a < BM / 32; ++a) tma_load_2d(dst + a * 4096, &tmA, m0 + 32 * a, kb * BK, raw_full(st));
+            } else {
+              tma_load_2d(dst, &tmA, kb * BK, m0, raw_full(st));
+            }
           } else {
-            tma_load_2d(dst, &tmA, kb * BK, m0, raw_full(rs));
+            mbar_wait_sleep(b_empty(st), ph ^ 1);
+            mbar_expect_tx(b_full(st), C::B_BYTES);
+            bulk_g2s(smem_u32(b_base + st * C::B_BYTES), bimg + int64_t(kb) * C::B_BYTES, C::B_BYTES, b_full(st));
           }
-          if (++rs == RS) { rs = 0; rph ^= 1; }
-          mbar_wait(b_empty(bs), bph ^ 1);
-          mbar_expect_tx(b_full(bs), C::B_BYTES);
-          bulk_g2s(smem_u32(b_base + bs * C::B_BYTES), bimg + int64_t(kb) * C::B_BYTES, C::B_BYTES, b_full(bs));
-          if (++bs == BS) { bs = 0; bph ^= 1; }
+          if (++st == S) { st = 0; ph ^= 1; }
         }
       }
     }
@@ -441,7 +461,7 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         const int gg = kb0 / G + g;  // global scale group
         const int tx = row < M ? int(xexp[int64_t(gg) * ldx + row]) : 0;
         const float sx = pow2f(16 - tx);
-        const int8_t* fe = fexp + int64_t(gg) * NP;
+        const float* fm = fmul + int64_t(gg) * NP;
         const uint32_t buf = gi & 1;
         mbar_wait(acc_full(buf), (gi >> 1) & 1);
         tc_fence_after();
@@ -457,16 +477,15 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
                          : "r"(base + uint32_t(w * NP + c0)));
           }
           tmem_wait_ld();
-          const int2 fw = *reinterpret_cast<const int2*>(fe + c0);
-          const int8_t* fb = reinterpret_cast<const int8_t*>(&fw);
+          const float4 f0 = *reinterpret_cast<const float4*>(fm + c0);
+          const float4 f1 = *reinterpret_cast<const float4*>(fm + c0 + 4);
+          const float sf[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             float s = fmaf(__int2float_rn(int(v[3][i])), 0.00390625f, __int2float_rn(int(v[2][i])));
             s = fmaf(s, 0.00390625f, __int2float_rn(int(v[1][i])));
             s = fmaf(s, 0.00390625f, __int2float_rn(int(v[0][i])));
-            const int tf = fb[i];
-            const float sf = tf == EXP_BAD ? CUDART_NAN_F : pow2f(16 - tf);
-            acc[c0 + i] = fmaf(s * sx, sf, acc[c0 + i]);
+            acc[c0 + i] = fmaf(s * sx, sf[i], acc[c0 + i]);
           }
         }
         tc_fence_before();
@@ -486,19 +505,24 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
     const int row_in_tile = q * 32 + lane;
     // this thread's 32 bytes of each plane: chunk 0 at kmaj_off(row, 0), chunk 1 at +128
     const uint32_t dig_off = kmaj_off(row_in_tile, 0);
-    uint32_t j = 0;
+    uint32_t j0 = 0;  // CTA-local sequence number of the unit's first k-block
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int split = u / tiles, tile = u - split * tiles;
       const int kb0 = split * kb_per_split, kb1 = min(kb_total, kb0 + kb_per_split);
       const int row = tile * BM + row_in_tile;
-      float mul = 0.f;
-      int cur_g = -1;
-      for (int kb = kb0; kb < kb1; ++kb, ++j) {
-        if (int(j & 1) != set) continue;
-        const int gg = kb / G;
-        if (gg != cur_g) {
-          cur_g = gg;
-          mul = row < M ? pow2f(int(xexp[int64_t(gg) * ldx + row])) : 0.f;
+      const int nk = kb1 - kb0;
+      const int g0 = kb0 / G, ng = (nk + G - 1) / G;
+      // row scales of this unit's first two groups; later ones are fetched a group ahead
+      const int8_t e_cur = row < M ? xexp[int64_t(g0) * ldx + row] : int8_t(0);
+      int8_t e_nxt = (row < M && ng > 1) ? xexp[int64_t(g0 + 1) * ldx + row] : int8_t(0);
+      int cur_g = 0;
+      float mul = row < M ? pow2f(int(e_cur)) : 0.f;
+      for (int t = int((uint32_t(set) - j0) & 1u); t < nk; t += 2) {
+        const uint32_t j = j0 + uint32_t(t);
+        if (t / G != cur_g) {
+          cur_g = t / G;
+          mul = row < M ? pow2f(int(e_nxt)) : 0.f;
+          e_nxt = (row < M && cur_g + 1 < ng) ? xexp[int64_t(g0 + cur_g + 1) * ldx + row] : int8_t(0);
         }
         const int rst = int(j % RS), cst = int(j % CS);
         mbar_wait(raw_full(rst), (j / RS) & 1);
@@ -521,10 +545,13 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
             x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
           }
         }
-        mbar_arrive(raw_empty(rst));  // raw values are in registers: TMA may refill
         // N = RN(x 2^t) sits in the low 24 bits of fma(x, 2^t, 2^23); bytes 2, 1, 0 are the digits
 #pragma unroll
+#ifndef I8_NOFMA2
+        for (int k = 0; k < 32; k += 2) fma2_shift(x[k], x[k + 1], mul);
+#else
         for (int k = 0; k < 32; ++k) x[k] = __float_as_uint(fmaf(__uint_as_float(x[k]), mul, 8388608.0f));
+#endif
         uint32_t p0[8], p1[8], p2[8];
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
@@ -544,9 +571,14 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         st_shared_v4(ad + PLANE + 128, make_uint4(p1[4], p1[5], p1[6], p1[7]));
         st_shared_v4(ad + 2 * PLANE, make_uint4(p2[0], p2[1], p2[2], p2[3]));
         st_shared_v4(ad + 2 * PLANE + 128, make_uint4(p2[4], p2[5], p2[6], p2[7]));
+        // The raw stage is released only here, behind stores that depend on every value read
+        // from it: an arrive issued right behind the LDS does not wait for them to return
+        // (seen on B200: refilled stages read back stale when it did).
+        mbar_arrive(raw_empty(rst));
         fence_proxy_async_smem();
         mbar_arrive(a_full(cst));
       }
+      j0 += uint32_t(nk);
     }
   }
   __syncthreads();
@@ -582,15 +614,15 @@ int i8_splits(int64_t tiles, int64_t K) {
 }
 
 template <int NP>
-int launch_fslice(const float* F, int r, int64_t K, uint8_t* img, int8_t* fexp, cudaStream_t st) {
+int launch_fslice(const float* F, int r, int64_t K, uint8_t* img, float* fmul, cudaStream_t st) {
   constexpr int SM = G * 3 * NP * BK;
   smem_attr(fslice_kernel<NP>, SM);
-  fslice_kernel<NP><<<int(groups_of(K)), 256, SM, st>>>(F, r, K, img, fexp);
+  fslice_kernel<NP><<<int(groups_of(K)), 256, SM, st>>>(F, r, K, img, fmul);
   return check_launch("i8 factor slice");
 }
 
 template <bool A_MN, int NP>
-int launch_i8(const CUtensorMap& ta, const uint8_t* img, const int8_t* xexp, int64_t ldx, const int8_t* fexp, int M,
+int launch_i8(const CUtensorMap& ta, const uint8_t* img, const int8_t* xexp, int64_t ldx, const float* fexp, int M,
               int K, int r, int splits, float* out, int64_t slab, cudaStream_t st) {
   using C = I8Cfg<NP>;
   smem_attr(i8_gemm_kernel<A_MN, NP>, C::SMEM);
@@ -633,7 +665,7 @@ int i8_prepare(const float* X, int64_t m, int64_t n_loc, double* stats, int8_t* 
 }
 
 int64_t i8_gemm_workspace(int64_t K) {
-  return ws_bytes<uint8_t>(ceil_div(K, BK) * 3 * 64 * BK) + ws_bytes<int8_t>(groups_of(K) * 64);
+  return ws_bytes<uint8_t>(ceil_div(K, BK) * 3 * 64 * BK) + ws_bytes<float>(groups_of(K) * 64);
 }
 
 // scn b: P (r x m) = W X^T; S slabs folded into P.  xexp_b: [groups(n_loc)][m].
@@ -645,7 +677,7 @@ int i8_wxt(const float* X, const float* W, int64_t m, int64_t n_loc, int r, cons
   CUtensorMap ta;
   if (!make_map_f32(&ta, X, uint64_t(m), uint64_t(n_loc), 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return BS_OK;
   uint8_t* img = ws.take<uint8_t>(ceil_div(n_loc, BK) * 3 * np * BK);
-  int8_t* fexp = ws.take<int8_t>(groups_of(n_loc) * np);
+  float* fexp = ws.take<float>(groups_of(n_loc) * np);
   if (!img || !fexp) { set_error("i8_wxt: workspace too small"); return BS_EWORK; }
   int rc = np == 32 ? launch_fslice<32>(W, r, n_loc, img, fexp, st) : launch_fslice<64>(W, r, n_loc, img, fexp, st);
   if (rc != BS_OK) return rc;
@@ -681,7 +713,7 @@ int i8_vtx(const float* X, const float* Vt, int64_t m, int64_t n_loc, int r, con
   CUtensorMap ta;
   if (!make_map_f32(&ta, X, uint64_t(m), uint64_t(n_loc), 32, 128, CU_TENSOR_MAP_SWIZZLE_128B)) return BS_OK;
   uint8_t* img = ws.take<uint8_t>(ceil_div(m, BK) * 3 * np * BK);
-  int8_t* fexp = ws.take<int8_t>(groups_of(m) * np);
+  float* fexp = ws.take<float>(groups_of(m) * np);
   if (!img || !fexp) { set_error("i8_vtx: workspace too small"); return BS_EWORK; }
   int rc = np == 32 ? launch_fslice<32>(Vt, r, m, img, fexp, st) : launch_fslice<64>(Vt, r, m, img, fexp, st);
   if (rc != BS_OK) return rc;
