@@ -7,28 +7,31 @@
 // nonnegative (X is checked every call, solvers.py:139-141; MU and APG keep the
 // factors >= 0).  Every operand block of 512 consecutive K values of one row
 // (the "scale group") gets a power-of-two scale 2^t chosen so the block maximum
-// lands in [2^22, 2^23); each value becomes the integer N = RN(x 2^t) < 2^23+1,
-// which is exactly the low 24 bits of the float fma(x, 2^t, 2^23).  Its three
-// bytes are unsigned digits: N = d0 2^16 + d1 2^8 + d2.  The products
-//   acc0 = a0 b0,  acc1 = a0 b1 + a1 b0,  acc2 = a0 b2 + a1 b1 + a2 b0,  acc3 = a1 b2 + a2 b1
-// are formed by tcgen05 kind::i8 MMAs (u8 x u8 -> s32) and accumulate EXACTLY in
-// int32 over the group (only the a2 b2 term, 2^-32 of the leading one, is dropped).
-// So the only rounding is the per-value RN to 24 bits (<= 2^-23 of the block max,
-// symmetric) and the float32 fold of the group partials — no truncation bias
-// (the tf32 accumulator of the 3xTF32 kernel truncates: nmf_tc.cu).
+// lands in [2^21, 2^22); each value becomes the integer N = RN(x 2^t) <= 2^22.  With
+// M = N + 0x8080 — exactly the low 24 bits of the float fma(x, 2^t, 2^23 + 0x8080) —
+// N = d0 2^16 + d1 2^8 + d2 with signed digits d0 = byte2(M) in [0, 64] and
+// d1, d2 = byte(M) - 128 in [-128, 127].  The products
+//   acc0 = a0 b0,  acc1 = a0 b1 + a1 b0,  acc2 = a0 b2 + a1 b1 + a2 b0
+// are formed by tcgen05 kind::i8 MMAs (s8 x s8 -> s32) and accumulate EXACTLY in int32
+// over the group.  The dropped terms (a1 b2 + a2 b1 at 2^-24, a2 b2 at 2^-32) are
+// products of zero-mean signed digits, so every rounding in the scheme is symmetric:
+// RN to 22 bits per value (<= 2^-22 of the block maximum) and the float32 fold of the
+// group partials.  No truncation bias (the tf32 accumulator of nmf_tc.cu truncates).
 //
-// Tensor work per 32-wide k-block (M = 128, r padded to NP = 64):
-//   A0 x [B0|B1|B2] (N = 3 NP) into acc0..acc2, A1 x [B0|B1|B2] into acc1..acc3,
-//   A2 x [B0|B1] into acc2..acc3 — 3 MMAs, 4 NP + 3 NP + 2 NP ... = 256 tensor cycles
-//   (tcgen05 floor N/2 per MMA) against ~600-700 cycles of HBM time per 16 KB tile.
+// Tensor work per 32-wide k-block (M = 128, r padded to NP = 64), A from TMEM:
+//   A0 x [B0|B1|B2] (N = 3 NP) -> acc0..2,  A1 x [B0|B1] -> acc1..2,  A2 x B0 -> acc2
+//   = 192 tensor cycles (floor N/2 per MMA) against ~640 cycles of HBM time per 16 KB tile.
+// The digits of A live in TMEM (TS-form MMA): shared memory then carries only the TMA
+// tiles, the converters' reads and the B operand (~50 KB per k-block instead of ~78 KB
+// with A in shared memory, which made the SS form shared-memory-bandwidth bound).
 //
 // Data flow (one CTA per SM, persistent over (tile, k-split) units):
-//   warp 0      producer: raw X tile (16 KB TMA) into a 6-deep ring, the factor's
-//               pre-sliced digit image (3 x NP x 32 B, cp.async.bulk) into a 4-deep ring
+//   warp 0      producer: raw X tile (16 KB TMA) into a deep ring
+//   warp 14     producer: the factor's pre-sliced digit image (3 x NP x 32 B, cp.async.bulk)
 //   warps 6-13  two converter sets (alternate k-blocks): one X row per thread ->
-//               3 digit planes (1 FFMA + byte permutes per value) -> smem A ring
+//               3 digit planes (1 packed FMA per 2 values + byte permutes) -> TMEM
 //   warp 1      MMA issuer (one elected lane)
-//   warps 2-5   epilogue: every group drains the 4 int32 accumulators, scales by
+//   warps 2-5   epilogue: every group drains the 3 int32 accumulators, scales by
 //               2^-(t_row + t_k) and folds into float32 registers (round to nearest)
 // The X scales come from bs_nmf_prepare (one pass over X per solver call, fused with
 // the reference's _nmf_check scan); the factor is sliced once per GEMM.
@@ -61,76 +64,70 @@ constexpr int G = 16;               // k-blocks per scale group = accumulation r
 constexpr int GROUP = G * BK;       // 512 K values
 constexpr int THREADS = 480;        // X producer, MMA, 4 epilogue warps, 2 x 4 converter warps, B producer
 constexpr int RAW_BYTES = BM * BK * 4;   // 16 KB fp32 tile
-constexpr int PLANE = BM * BK;           // 4 KB: one digit plane of the A tile
-constexpr int A_BYTES = 3 * PLANE;
 #ifndef I8_RS
-#define I8_RS 7
+#define I8_RS 10
 #endif
 #ifndef I8_BS
-#define I8_BS 6
+#define I8_BS 8
 #endif
-constexpr int RS = I8_RS, BS = I8_BS, CS = 4;
+constexpr int RS = I8_RS, BS = I8_BS, CS = 4;  // raw X stages, B image stages, TMEM A stages
+constexpr float DIGIT_BIAS = 8388608.0f + 32896.0f;  // 2^23 + 0x8080: bytes of M = N + 0x8080
 
 // scale exponent for a block whose largest |value| has float bits `bits`:
-// t = 149 - E puts the maximum in [2^22, 2^23) (N <= 2^23 after rounding).
+// t = 148 - E puts the maximum in [2^21, 2^22) (N <= 2^22 after rounding).
 __host__ __device__ __forceinline__ int exp_code(uint32_t bits) {
   const int e = int(bits >> 23);
-  return min(149 - e, 126);
+  return min(148 - e, 126);
 }
 __device__ __forceinline__ float pow2f(int t) { return __int_as_float((127 + t) << 23); }
 
-// (x0, x1) * m + 2^23 for two values at once (packed f32x2 FMA)
-__device__ __forceinline__ void fma2_shift(uint32_t& a, uint32_t& b, float m) {
+// (x0, x1) * m + DIGIT_BIAS for two values at once (packed f32x2 FMA)
+__device__ __forceinline__ void fma2_digits(uint32_t& a, uint32_t& b, float m) {
   uint64_t v = (uint64_t(b) << 32) | a, r;
   const uint64_t mm = (uint64_t(__float_as_uint(m)) << 32) | __float_as_uint(m);
-  const uint64_t cc = (uint64_t(0x4B000000u) << 32) | 0x4B000000u;
+  const uint64_t cc = (uint64_t(__float_as_uint(DIGIT_BIAS)) << 32) | __float_as_uint(DIGIT_BIAS);
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(v), "l"(mm), "l"(cc));
   a = uint32_t(r);
   b = uint32_t(r >> 32);
 }
 
-// canonical K-major SWIZZLE_NONE operand: core matrix = 8 rows x 16 B, K chunk stride 128 B,
-// 8-row group stride 256 B (probed: scripts/i8_probe.cu)
-__device__ __forceinline__ uint32_t kmaj_off(int row, int kchunk) {
-  return uint32_t(row >> 3) * 256u + uint32_t(kchunk) * 128u + uint32_t(row & 7) * 16u;
-}
-
+// B operand (factor digits, shared memory): canonical K-major SWIZZLE_NONE, core matrix =
+// 8 rows x 16 B, K-chunk stride 128 B, 8-row-group stride 256 B (probed: scripts/i8_probe.cu)
 __device__ __forceinline__ uint64_t i8_desc(uint32_t addr) { return sdesc(addr, 128, 256, 0); }
 
-// kind::i8, u8 x u8 -> s32, both K-major, M = 128
+// kind::i8, s8 x s8 -> s32, both K-major, M = 128
 __host__ __device__ constexpr uint32_t idesc_i8(int N) {
-  return (2u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
 // One k-block of digit products, issued by one elected lane with warp-uniform operands:
-//   first:  acc0..2 = A0[B0|B1|B2];  acc1..2 += A1[B0|B1];  acc3 = A1 B2;  acc2..3 += A2[B0|B1]
-//   else:   acc0..2 += A0[B0|B1|B2]; acc1..3 += A1[B0|B1|B2];              acc2..3 += A2[B0|B1]
-// a: plane 0 descriptor (planes 4 KB apart = +256 in the start field); b: B0 (B2 at +2 NP rows).
+//   acc0..2 (+)= A0 [B0|B1|B2];  acc1..2 += A1 [B0|B1];  acc2 += A2 B0
+// a: TMEM column of plane 0 (planes 8 columns apart); b: B0 descriptor; first: restart acc.
 template <int NP>
-__device__ __forceinline__ void mma_i8_kblock(uint32_t d, uint64_t a, uint64_t b, uint32_t first) {
+__device__ __forceinline__ void mma_i8_kblock(uint32_t d, uint32_t a, uint64_t b, uint32_t first) {
   constexpr uint32_t id3 = idesc_i8(3 * NP), id2 = idesc_i8(2 * NP), id1 = idesc_i8(NP);
-  constexpr uint32_t b2_off = (2 * NP * BK) >> 4;
   asm volatile(
-      "{\n\t.reg .pred p, pf, pn, acc;\n\t.reg .b64 a1, a2, b2;\n\t.reg .b32 d1, d2, d3;\n\t"
+      "{\n\t.reg .pred p, acc;\n\t.reg .b32 a1, a2, d1, d2;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.b32 pf, %3, 0;\n\t"
       "setp.eq.b32 acc, %3, 0;\n\t"
-      "and.pred pn, p, acc;\n\t"
-      "and.pred pf, p, pf;\n\t"
-      "add.s64 a1, %1, 256;\n\tadd.s64 a2, %1, 512;\n\tadd.s64 b2, %2, %4;\n\t"
-      "add.u32 d1, %0, %5;\n\tadd.u32 d2, %0, %6;\n\tadd.u32 d3, %0, %7;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %8, acc;\n\t"
-      "@pf tcgen05.mma.cta_group::1.kind::i8 [d1], a1, %2, %9, 1;\n\t"
-      "@pf tcgen05.mma.cta_group::1.kind::i8 [d3], a1, b2, %10, 0;\n\t"
-      "@pn tcgen05.mma.cta_group::1.kind::i8 [d1], a1, %2, %8, 1;\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [d2], a2, %2, %9, 1;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(first), "n"(b2_off), "n"(NP), "n"(2 * NP), "n"(3 * NP), "n"(id3), "n"(id2), "n"(id1)
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\t"
+      "add.u32 d1, %0, %4;\n\tadd.u32 d2, %0, %5;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %6, acc;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [d1], [a1], %2, %7, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [d2], [a2], %2, %8, 1;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(first), "n"(NP), "n"(2 * NP), "n"(id3), "n"(id2), "n"(id1)
       : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
                : "memory");
 }
 
@@ -302,11 +299,12 @@ __global__ void __launch_bounds__(256) fslice_kernel(const float* __restrict__ F
     const uint32_t inner = uint32_t(kk >> 4) * 128u + uint32_t(kk & 15);
     for (int k = 0; k < NP; ++k) {
       const float x = (in && k < r) ? col[k < r ? k : 0] : 0.f;
-      const uint32_t nb = __float_as_uint(fmaf(x, kmul[k], 8388608.0f));
+      const uint32_t nb = __float_as_uint(fmaf(x, kmul[k], DIGIT_BIAS));
 #pragma unroll
       for (int p = 0; p < 3; ++p) {
         const int row = p * NP + k;
-        kbimg[uint32_t(row >> 3) * 256u + uint32_t(row & 7) * 16u + inner] = uint8_t(nb >> (8 * (2 - p)));
+        const uint32_t d = (nb >> (8 * (2 - p))) & 0xFFu;
+        kbimg[uint32_t(row >> 3) * 256u + uint32_t(row & 7) * 16u + inner] = uint8_t(p == 0 ? d : d ^ 0x80u);
       }
     }
   }
@@ -328,23 +326,26 @@ __global__ void __launch_bounds__(256) fslice_kernel(const float* __restrict__ F
 template <int NP>
 struct I8Cfg {
   static constexpr int B_BYTES = 3 * NP * BK;  // factor digit image per k-block
-  static constexpr int SMEM = RS * RAW_BYTES + BS * B_BYTES + CS * A_BYTES + 1024 + 512;
-  static constexpr int ACC = 4 * NP;           // int32 columns per accumulator buffer
-  static constexpr int TMEM_COLS = 2 * ACC;    // 256 or 512
-  static_assert(TMEM_COLS <= 512 && 3 * NP <= 256, "i8 tile");
+  static constexpr int SMEM = RS * RAW_BYTES + BS * B_BYTES + 1024 + 512;
+  static constexpr int ACC = 3 * NP;           // int32 columns per accumulator buffer
+  static constexpr int A_COL0 = 2 * ACC;       // TMEM A stages: 3 planes x 8 columns each (32 reserved)
+  static constexpr int TMEM_COLS = 2 * ACC + CS * 32 <= 256 ? 256 : 512;
+  static_assert(2 * ACC + CS * 32 <= 512 && 3 * NP <= 256, "i8 tile");
 };
 
 template <bool A_MN, int NP>
 __global__ void __launch_bounds__(THREADS, 1)
 i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restrict__ bimg,
                const int8_t* __restrict__ xexp, int64_t ldx, const float* __restrict__ fmul, int M, int K, int r,
-               int tiles, int kb_per_split, int units, float* __restrict__ out, int64_t slab) {
+               int tiles, int kb_per_split, int units, float* __restrict__ out, int64_t slab, int mode) {
   using C = I8Cfg<NP>;
+#ifndef BS_DEBUG_MODES
+  mode = 0;  // work-skipping modes exist only in debug builds (scripts/i8_modes.py)
+#endif
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* b_base = smem + RS * RAW_BYTES;
-  uint8_t* a_base = b_base + BS * C::B_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(a_base + CS * A_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + BS * C::B_BYTES);
   // raw_full[RS] raw_empty[RS] b_full[BS] b_empty[BS] a_full[CS] a_empty[CS] acc_full[2] acc_empty[2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * BS + 2 * CS + 4);
   auto raw_full = [&](int s) { return smem_u32(bars + s); };
@@ -390,7 +391,13 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         const int kb0 = split * kb_per_split, kb1 = min(kb_total, kb0 + kb_per_split);
         const int m0 = tile * BM;
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (xprod) {
+          if (xprod && (mode & 8)) {
+            mbar_wait_sleep(raw_empty(st), ph ^ 1);
+            mbar_arrive(raw_full(st));
+          } else if (!xprod && (mode & 4)) {
+            mbar_wait_sleep(b_empty(st), ph ^ 1);
+            mbar_arrive(b_full(st));
+          } else if (xprod) {
             mbar_wait_sleep(raw_empty(st), ph ^ 1);
             mbar_expect_tx(raw_full(st), RAW_BYTES);
             const uint32_t dst = smem_u32(smem + st * RAW_BYTES);
@@ -413,7 +420,6 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
     // ---------------- MMA issuer ----------------
     int cs = 0, bs = 0;
     uint32_t cph = 0, bph = 0, gi = 0;
-    const uint32_t id3 = idesc_i8(3 * NP), id2 = idesc_i8(2 * NP), id1 = idesc_i8(NP);
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int split = u / tiles;
       const int kb0 = split * kb_per_split, kb1 = min(kb_total, kb0 + kb_per_split);
@@ -429,9 +435,9 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         tc_fence_after();
         const bool last = (in_group == G - 1) || (kb == kb1 - 1);
         const uint32_t d = __shfl_sync(0xffffffffu, tmem + buf * C::ACC, 0);
-        const uint32_t aa = __shfl_sync(0xffffffffu, smem_u32(a_base + cs * A_BYTES), 0);
+        const uint32_t aa = __shfl_sync(0xffffffffu, tmem + C::A_COL0 + cs * 32, 0);
         const uint32_t bb = __shfl_sync(0xffffffffu, smem_u32(b_base + bs * C::B_BYTES), 0);
-        mma_i8_kblock<NP>(d, i8_desc(aa), i8_desc(bb), in_group == 0 ? 1u : 0u);
+        if (!(mode & 2)) mma_i8_kblock<NP>(d, aa, i8_desc(bb), in_group == 0 ? 1u : 0u);
         __syncwarp();
         mma_commit_elect(a_empty(cs));
         mma_commit_elect(b_empty(bs));
@@ -468,9 +474,9 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         const uint32_t base = tmem + lane_addr + buf * C::ACC;
 #pragma unroll
         for (int c0 = 0; c0 < NP; c0 += 8) {
-          uint32_t v[4][8];
+          uint32_t v[3][8];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < 3; ++w) {
             asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                          : "=r"(v[w][0]), "=r"(v[w][1]), "=r"(v[w][2]), "=r"(v[w][3]), "=r"(v[w][4]),
                            "=r"(v[w][5]), "=r"(v[w][6]), "=r"(v[w][7])
@@ -482,8 +488,7 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
           const float sf[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            float s = fmaf(__int2float_rn(int(v[3][i])), 0.00390625f, __int2float_rn(int(v[2][i])));
-            s = fmaf(s, 0.00390625f, __int2float_rn(int(v[1][i])));
+            float s = fmaf(__int2float_rn(int(v[2][i])), 0.00390625f, __int2float_rn(int(v[1][i])));
             s = fmaf(s, 0.00390625f, __int2float_rn(int(v[0][i])));
             acc[c0 + i] = fmaf(s * sx, sf[i], acc[c0 + i]);
           }
@@ -499,12 +504,11 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
       }
     }
   } else {
-    // ---------------- converters: X row -> three digit planes ----------------
+    // ---------------- converters: X row -> three digit planes in TMEM ----------------
     const int set = (warp - 6) >> 2;
     const int q = warp & 3;
     const int row_in_tile = q * 32 + lane;
-    // this thread's 32 bytes of each plane: chunk 0 at kmaj_off(row, 0), chunk 1 at +128
-    const uint32_t dig_off = kmaj_off(row_in_tile, 0);
+    const uint32_t lane_addr = uint32_t(q * 32) << 16;
     uint32_t j0 = 0;  // CTA-local sequence number of the unit's first k-block
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int split = u / tiles, tile = u - split * tiles;
@@ -527,6 +531,13 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
         const int rst = int(j % RS), cst = int(j % CS);
         mbar_wait(raw_full(rst), (j / RS) & 1);
         mbar_wait(a_empty(cst), ((j / CS) & 1) ^ 1);
+        tc_fence_after();
+        if (mode & 1) {
+          tc_fence_before();
+          mbar_arrive(raw_empty(rst));
+          mbar_arrive(a_full(cst));
+          continue;
+        }
         uint32_t x[32];
         const uint32_t raw = smem_u32(smem + rst * RAW_BYTES);
         if constexpr (A_MN) {
@@ -545,37 +556,31 @@ i8_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const uint8_t* __restric
             x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
           }
         }
-        // N = RN(x 2^t) sits in the low 24 bits of fma(x, 2^t, 2^23); bytes 2, 1, 0 are the digits
+        // M = RN(x 2^t) + 0x8080 sits in the low 24 bits of fma(x, 2^t, 2^23 + 0x8080):
+        // digit 0 = byte 2, digits 1 and 2 = bytes 1 and 0 minus 128 (xor 0x80 as s8)
 #pragma unroll
-#ifndef I8_NOFMA2
-        for (int k = 0; k < 32; k += 2) fma2_shift(x[k], x[k + 1], mul);
-#else
-        for (int k = 0; k < 32; ++k) x[k] = __float_as_uint(fmaf(__uint_as_float(x[k]), mul, 8388608.0f));
-#endif
-        uint32_t p0[8], p1[8], p2[8];
+        for (int k = 0; k < 32; k += 2) fma2_digits(x[k], x[k + 1], mul);
+        uint32_t pl[24];  // plane 0 (8 words), plane 1, plane 2: TMEM columns in this order
 #pragma unroll
         for (int w = 0; w < 8; ++w) {
           const uint32_t a = x[4 * w], b = x[4 * w + 1], c = x[4 * w + 2], d = x[4 * w + 3];
           const uint32_t ab = __byte_perm(a, b, 0x5140);  // a.b0 b.b0 a.b1 b.b1
           const uint32_t cd = __byte_perm(c, d, 0x5140);
-          p2[w] = __byte_perm(ab, cd, 0x5410);            // byte 0 of a b c d
-          p1[w] = __byte_perm(ab, cd, 0x7632);            // byte 1
-          const uint32_t ab2 = __byte_perm(a, b, 0x0062); // a.b2 b.b2
+          pl[16 + w] = __byte_perm(ab, cd, 0x5410) ^ 0x80808080u;  // byte 0 of a b c d
+          pl[8 + w] = __byte_perm(ab, cd, 0x7632) ^ 0x80808080u;   // byte 1
+          const uint32_t ab2 = __byte_perm(a, b, 0x0062);          // a.b2 b.b2
           const uint32_t cd2 = __byte_perm(c, d, 0x0062);
-          p0[w] = __byte_perm(ab2, cd2, 0x5410);          // byte 2
+          pl[w] = __byte_perm(ab2, cd2, 0x5410);                   // byte 2
         }
-        const uint32_t ad = smem_u32(a_base + cst * A_BYTES) + dig_off;
-        st_shared_v4(ad, make_uint4(p0[0], p0[1], p0[2], p0[3]));
-        st_shared_v4(ad + 128, make_uint4(p0[4], p0[5], p0[6], p0[7]));
-        st_shared_v4(ad + PLANE, make_uint4(p1[0], p1[1], p1[2], p1[3]));
-        st_shared_v4(ad + PLANE + 128, make_uint4(p1[4], p1[5], p1[6], p1[7]));
-        st_shared_v4(ad + 2 * PLANE, make_uint4(p2[0], p2[1], p2[2], p2[3]));
-        st_shared_v4(ad + 2 * PLANE + 128, make_uint4(p2[4], p2[5], p2[6], p2[7]));
+        const uint32_t ta = tmem + lane_addr + uint32_t(C::A_COL0 + cst * 32);
+        tmem_st16(ta, pl);
+        tmem_st8(ta + 16, pl + 16);
+        tmem_wait_st();
+        tc_fence_before();
         // The raw stage is released only here, behind stores that depend on every value read
         // from it: an arrive issued right behind the LDS does not wait for them to return
         // (seen on B200: refilled stages read back stale when it did).
         mbar_arrive(raw_empty(rst));
-        fence_proxy_async_smem();
         mbar_arrive(a_full(cst));
       }
       j0 += uint32_t(nk);
@@ -632,8 +637,16 @@ int launch_i8(const CUtensorMap& ta, const uint8_t* img, const int8_t* xexp, int
   const int real = int(ceil_div(kb_total, kb_per));
   const int units = tiles * real;
   const int grid = std::min(units, num_sms());
+  static const int mode = [] {
+#ifdef BS_DEBUG_MODES
+    const char* e = getenv("BS_I8_MODE");
+    return e ? atoi(e) : 0;
+#else
+    return 0;
+#endif
+  }();
   i8_gemm_kernel<A_MN, NP><<<grid, THREADS, C::SMEM, st>>>(ta, img, xexp, ldx, fexp, M, K, r, tiles, kb_per, units,
-                                                            out, slab);
+                                                            out, slab, mode);
   return real;
 }
 
