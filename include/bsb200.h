@@ -151,10 +151,11 @@ int bs_nmf_prepare(const void* X, int dtype, int64_t m, int64_t n_loc,
                    double* stats_dev, void* xscale, void* work,
                    int64_t work_bytes, void* stream);
 
-/* How many scn a / scn b GEMMs ran on each path since the last reset:
- * out4 = {integer digit-slice tcgen05, 3xTF32 tcgen05, float32 CUDA cores,
- *         float64 (DMMA / CUDA cores)}. */
-int bs_gemm_path_counts(int64_t* out4, int reset);
+/* How many hot-path passes ran on each kernel path since the last reset (process-wide):
+ * out8 = {NMF GEMM on integer digit-slice tcgen05, NMF GEMM on 3xTF32 tcgen05,
+ *         NMF GEMM on float32 CUDA cores, NMF GEMM in float64 (DMMA / CUDA cores),
+ *         MDS pass on tcgen05 (mds_tc.cu), MDS pass on CUDA cores, 0, 0}. */
+int bs_gemm_path_counts(int64_t* out8, int reset);
 
 /* scn b local GEMM (distlinalg.py:246-252): P (r x m, column-major, float32
  * or float64 like X) = W_loc X_loc^T summed over the rank's n_loc columns.

@@ -500,12 +500,17 @@ class _TorchCommunicator(Communicator):
                 host, port, rank, size = rendezvous
                 kw.update(init_method=f"tcp://{host}:{port}", rank=rank, world_size=size,
                           timeout=datetime.timedelta(seconds=max(float(timeout), 30.0)))
+            if backend_name == "gloo+cuda":
+                backend_name = "gloo"
+                self._gloo_cuda = True
             if backend_name == "nccl":
                 ndev = max(torch.cuda.device_count(), 1)
                 local = int(os.environ.get("LOCAL_RANK", str(rendezvous[2] % ndev if rendezvous else 0)))
                 torch.cuda.set_device(local)
                 kw["device_id"] = torch.device("cuda", local)
             dist.init_process_group(backend=backend_name, **kw)
+        elif backend_name == "gloo+cuda":
+            self._gloo_cuda = True
         self.rank = dist.get_rank()
         self.size = dist.get_world_size()
         self.backend = dist.get_backend()
@@ -513,8 +518,16 @@ class _TorchCommunicator(Communicator):
             local = int(os.environ.get("LOCAL_RANK", self.rank % max(torch.cuda.device_count(), 1)))
             self.device = torch.device("cuda", local)
             torch.cuda.set_device(self.device)
+            self.coll_device = self.device
+        elif getattr(self, "_gloo_cuda", False):
+            # data on the GPU (rank mod device count: several ranks may share one GPU), collectives
+            # staged through host memory over gloo — the multi-process solver tests on one GPU
+            self.device = torch.device("cuda", self.rank % max(torch.cuda.device_count(), 1))
+            torch.cuda.set_device(self.device)
+            self.coll_device = torch.device("cpu")
         else:
             self.device = torch.device("cpu")
+            self.coll_device = self.device
         self._ops = {ReduceOp.SUM: dist.ReduceOp.SUM, ReduceOp.PROD: dist.ReduceOp.PRODUCT,
                      ReduceOp.MAX: dist.ReduceOp.MAX, ReduceOp.MIN: dist.ReduceOp.MIN}
 
@@ -523,17 +536,17 @@ class _TorchCommunicator(Communicator):
             self._dist.destroy_process_group()
 
     def _to_dev(self, buf):
-        """(device flat tensor, writeback fn)."""
+        """(flat tensor on the collective device, writeback fn)."""
         torch = _torch()
         if _is_tensor(buf):
             flat, wb = fortran_flat(buf)
-            if flat.device != self.device:
-                dflat = flat.to(self.device)
+            if flat.device != self.coll_device:
+                dflat = flat.to(self.coll_device)
                 return dflat, (lambda: (_fortran_writeback(buf, dflat.to(buf.device))
                                         if wb else flat.copy_(dflat.to(flat.device))))
             return flat, ((lambda: _fortran_writeback(buf, flat)) if wb else (lambda: None))
         arr = np.asarray(buf)
-        flat = torch.from_numpy(np.ascontiguousarray(_np_flat(arr))).to(self.device)
+        flat = torch.from_numpy(np.ascontiguousarray(_np_flat(arr))).to(self.coll_device)
         return flat, (lambda: _np_writeback(buf, flat.cpu().numpy()))
 
     def _collective(self, op, buf, send=None, counts=None, root=-1, redop=None):
@@ -552,9 +565,9 @@ class _TorchCommunicator(Communicator):
             sflat, _ = self._to_dev(send)
             mx = max(counts) if counts else 0
             if mx:
-                pad = torch.zeros(mx, dtype=rflat.dtype, device=self.device)
+                pad = torch.zeros(mx, dtype=rflat.dtype, device=self.coll_device)
                 pad[:sflat.numel()].copy_(sflat)
-                out = torch.empty(mx * self.size, dtype=rflat.dtype, device=self.device)
+                out = torch.empty(mx * self.size, dtype=rflat.dtype, device=self.coll_device)
                 dist.all_gather_into_tensor(out, pad)
                 off = 0
                 for r in range(self.size):
@@ -565,19 +578,19 @@ class _TorchCommunicator(Communicator):
             sflat, _ = self._to_dev(send)
             mx = max(counts) if counts else 0
             if mx:
-                padded = torch.zeros(mx * self.size, dtype=rflat.dtype, device=self.device)
+                padded = torch.zeros(mx * self.size, dtype=rflat.dtype, device=self.coll_device)
                 off = 0
                 for r in range(self.size):
                     if counts[r]:
                         padded[r * mx:r * mx + counts[r]].copy_(sflat[off:off + counts[r]])
                     off += counts[r]
-                out = torch.empty(mx, dtype=rflat.dtype, device=self.device)
+                out = torch.empty(mx, dtype=rflat.dtype, device=self.coll_device)
                 dist.reduce_scatter_tensor(out, padded, op=self._ops[redop])
                 rflat.copy_(out[:counts[self.rank]])
         elif op == "scatterv":
             total = sum(counts)
             mx = max(counts) if counts else 0
-            full = torch.empty(total, dtype=rflat.dtype, device=self.device)
+            full = torch.empty(total, dtype=rflat.dtype, device=self.coll_device)
             if self.rank == root:
                 full.copy_(self._to_dev(send)[0])
             dist.broadcast(full, src=root)
@@ -603,7 +616,7 @@ def _parse_descriptor(descriptor):
         if size < 1:
             raise CommInitError("world size must be >= 1")
         return "inproc", size
-    if descriptor in ("nccl", "gloo", "torch"):
+    if descriptor in ("nccl", "gloo", "gloo+cuda", "torch"):
         return "torch", descriptor
     if descriptor.startswith("tcp:"):
         # tcp:host:port,...,rank=<r> (comm.py:501-519): one process per rank; here the

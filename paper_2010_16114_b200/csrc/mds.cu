@@ -529,6 +529,7 @@ static MdsGrid mds_grid(int64_t n, int64_t n_loc, int q, int dtype) {
 
 namespace bs {
 bool mds_tc_eligible(int dtype, int64_t n, int64_t n_loc, int q, int mode, const void* Y, const void* theta);
+void note_gemm_path(int path);
 int64_t mds_tc_workspace(int64_t n, int64_t n_loc, int q);
 int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64_t n_loc, int q, int perturb,
                 double* red, Workspace& ws, cudaStream_t st, double** zp_out, double** tp_out, int* segs_out);
@@ -635,8 +636,10 @@ extern "C" int bs_mds_pass(const void* Y, const void* theta_full, int dtype, int
     const int fg = int(std::min<int64_t>(ceil_div(n_loc * (q + 1), 256), 2048));
     mds_fold_kernel<float><<<fg, 256, 0, st>>>(zp, tp, segs, n_loc, q, static_cast<float*>(zsum),
                                                static_cast<float*>(T));
+    note_gemm_path(4);
     return check_launch("bs_mds_pass", 3);
   }
+  note_gemm_path(5);
   MdsGrid g = mds_grid(n, n_loc, q, dtype);
   unsigned int* ctr = ws.take<unsigned int>(1);
   double* parts = ws.take<double>(2 * int64_t(g.colblocks) * g.segs);

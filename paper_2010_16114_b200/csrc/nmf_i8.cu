@@ -43,13 +43,13 @@
 using namespace bs;
 
 namespace bs {
-static std::atomic<int64_t> g_gemm_path[4];
-void note_gemm_path(int path) { g_gemm_path[path & 3].fetch_add(1, std::memory_order_relaxed); }
+static std::atomic<int64_t> g_gemm_path[8];
+void note_gemm_path(int path) { g_gemm_path[path & 7].fetch_add(1, std::memory_order_relaxed); }
 }  // namespace bs
 
-extern "C" int bs_gemm_path_counts(int64_t* out4, int reset) {
-  for (int i = 0; i < 4; ++i) {
-    out4[i] = reset ? g_gemm_path[i].exchange(0) : g_gemm_path[i].load();
+extern "C" int bs_gemm_path_counts(int64_t* out8, int reset) {
+  for (int i = 0; i < 8; ++i) {
+    out8[i] = reset ? g_gemm_path[i].exchange(0) : g_gemm_path[i].load();
   }
   return BS_OK;
 }

@@ -1,6 +1,11 @@
-"""Multi-GPU parity under torchrun (one process per GPU, NCCL).
+"""Multi-process parity under torchrun (one process per rank).
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/nccl_parity.py
+
+BS_PARITY_BACKEND selects the communicator: ``nccl`` (default; one GPU per rank) or
+``gloo+cuda`` (data on the GPU, collectives staged through the host, so several ranks
+may share one GPU — tests/test_multiproc_gpu.py runs it with 2 ranks on a 1-GPU box).
+The solver-level C ABI sections need NCCL and run only with ``nccl``.
 
 Runs NMF (both algorithms, float32 tcgen05 path and float64), MDS and Cox through
 the 'nccl' Communicator on column-sharded data and checks every rank's result
@@ -29,7 +34,8 @@ def check(name, got, want, tol):
 
 
 def main():
-    comm = bs.init("nccl")
+    backend = os.environ.get("BS_PARITY_BACKEND", "nccl")
+    comm = bs.init(backend)
     ok = True
     for dt, tol, (m, n, r) in ((np.float64, 1e-9, (300, 257, 7)), (np.float32, 2e-5, (2048, 1501, 60))):
         x = orc.rand_fill_common((m, n), 5, dt)
@@ -92,6 +98,12 @@ def main():
         tr.append(np.asarray(st.trace))
         ok &= check("cox packed/int8: nonzero coefficients", [min(np.count_nonzero(bs.gather_full(st.beta)), 1)], [1], 0)
     ok &= check("cox packed genotypes vs int8 trace", tr[0], tr[1], 2e-5)
+    if backend != "nccl":
+        comm.barrier()
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+        sys.exit(0 if ok else 1)
     # the solver-level C ABI (bs_ctx_create over NCCL + bs_cox_run) against cox_fit
     from paper_2010_16114_b200 import runtime
 
