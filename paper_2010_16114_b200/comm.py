@@ -137,54 +137,55 @@ def _np_writeback(buf, flat):
     buf[...] = np.asarray(flat).reshape(buf.shape, order="F")
 
 
-def _check_agree(headers, field, what):
-    ref = headers[0][field]
-    for r, h in enumerate(headers):
-        if h[field] != ref:
-            raise CollectiveContractError(
-                f"{what} mismatch: rank 0 has {ref!r}, rank {r} has {h[field]!r}")
+# Fields every rank must agree on, per collective (the reference's contract, comm.py:102-153).
+_AGREE = {
+    "broadcast": (("dtype", "buffer dtype"), ("root", "broadcast root"), ("recv_len", "broadcast buffer length")),
+    "allreduce": (("dtype", "buffer dtype"), ("redop", "reduction operator"),
+                  ("recv_len", "allreduce buffer length")),
+    "allgatherv": (("dtype", "buffer dtype"), ("counts", "allgatherv counts")),
+    "reduce_scatterv": (("dtype", "buffer dtype"), ("counts", "reduce_scatterv counts"),
+                        ("redop", "reduction operator")),
+    "scatterv": (("dtype", "buffer dtype"), ("counts", "scatterv counts"), ("root", "scatterv root")),
+    "barrier": (),
+}
+
+
+def _lengths_ok(op, headers):
+    """Per-rank buffer lengths against the agreed counts; returns an error message or None."""
+    counts = headers[0]["counts"]
+    if op in ("allgatherv", "reduce_scatterv"):
+        block, whole = ("send_len", "recv_len") if op == "allgatherv" else ("recv_len", "send_len")
+        total = sum(counts)
+        for r, h in enumerate(headers):
+            if h[block] != counts[r]:
+                return f"{op}: rank {r} block holds {h[block]} values, counts say {counts[r]}"
+            if h[whole] != total:
+                return f"{op}: rank {r} full buffer holds {h[whole]}, need {total}"
+    elif op == "scatterv":
+        root = headers[0]["root"]
+        if headers[root]["send_len"] != sum(counts):
+            return f"scatterv: root sends {headers[root]['send_len']} values, counts sum to {sum(counts)}"
+        bad = [r for r, h in enumerate(headers) if h["recv_len"] != counts[r]]
+        if bad:
+            r = bad[0]
+            return f"scatterv: rank {r} receive buffer holds {headers[r]['recv_len']}, counts say {counts[r]}"
+    return None
 
 
 def _validate_headers(headers):
-    """Cross-rank contract checks (comm.py:102-153)."""
-    _check_agree(headers, "op", "collective operation")
-    _check_agree(headers, "seq", "collective sequence number")
-    op = headers[0]["op"]
-    if op == "barrier":
-        return
-    _check_agree(headers, "dtype", "buffer dtype")
-    if op == "broadcast":
-        _check_agree(headers, "root", "broadcast root")
-        _check_agree(headers, "recv_len", "broadcast buffer length")
-    elif op == "allreduce":
-        _check_agree(headers, "redop", "reduction operator")
-        _check_agree(headers, "recv_len", "allreduce buffer length")
-    elif op in ("allgatherv", "reduce_scatterv"):
-        _check_agree(headers, "counts", f"{op} counts")
-        counts = headers[0]["counts"]
-        total = sum(counts)
-        for r, h in enumerate(headers):
-            mine, whole = (h["send_len"], h["recv_len"]) if op == "allgatherv" else (h["recv_len"], h["send_len"])
-            if mine != counts[r]:
-                raise CollectiveContractError(f"{op}: rank {r} block holds {mine} values, counts say {counts[r]}")
-            if whole != total:
-                raise CollectiveContractError(f"{op}: rank {r} full buffer holds {whole}, need {total}")
-        if op == "reduce_scatterv":
-            _check_agree(headers, "redop", "reduction operator")
-    elif op == "scatterv":
-        _check_agree(headers, "counts", "scatterv counts")
-        _check_agree(headers, "root", "scatterv root")
-        counts = headers[0]["counts"]
-        root = headers[0]["root"]
-        if headers[root]["send_len"] != sum(counts):
+    """Cross-rank contract checks; raises CollectiveContractError on the first violation."""
+    first = headers[0]
+    fields = (("op", "collective operation"), ("seq", "collective sequence number"))
+    for field, what in fields + _AGREE.get(first["op"], ()):
+        odd = next((r for r, h in enumerate(headers) if h[field] != first[field]), None)
+        if odd is not None:
             raise CollectiveContractError(
-                f"scatterv: root sends {headers[root]['send_len']} values, counts sum to {sum(counts)}")
-        for r, h in enumerate(headers):
-            if h["recv_len"] != counts[r]:
-                raise CollectiveContractError(
-                    f"scatterv: rank {r} receive buffer holds {h['recv_len']}, counts say {counts[r]}")
-    else:  # pragma: no cover
-        raise CollectiveContractError(f"unknown collective {op!r}")
+                f"{what} mismatch: rank 0 has {first[field]!r}, rank {odd} has {headers[odd][field]!r}")
+    if first["op"] not in _AGREE:  # pragma: no cover
+        raise CollectiveContractError(f"unknown collective {first['op']!r}")
+    msg = _lengths_ok(first["op"], headers)
+    if msg:
+        raise CollectiveContractError(msg)
 
 
 class Communicator:
@@ -257,59 +258,50 @@ class Communicator:
 # ---------------------------------------------------------------------------
 
 
-class _EventBarrier:
-    """Reusable two-generation barrier (comm.py:272-307)."""
-
-    def __init__(self, size, timeout):
-        self._size = size
-        self._timeout = timeout
-        self._lock = threading.Lock()
-        self._count = 0
-        self._gen = 0
-        self._events = [threading.Event(), threading.Event()]
-        self._broken = False
-
-    def wait(self):
-        with self._lock:
-            if self._broken:
-                raise RankAbortedError("world aborted")
-            gen = self._gen
-            self._count += 1
-            if self._count == self._size:
-                self._count = 0
-                self._gen ^= 1
-                self._events[self._gen].clear()
-                self._events[gen].set()
-                return
-        if not self._events[gen].wait(self._timeout):
-            self.abort()
-            raise RankAbortedError("a rank timed out mid-collective")
-        if self._broken:
-            raise RankAbortedError("world aborted")
-
-    def abort(self):
-        with self._lock:
-            self._broken = True
-            for event in self._events:
-                event.set()
-
-
 class _InProcWorld:
-    """Double-parity slot table (comm.py:310-327)."""
+    """Rendezvous board of the in-process world (one rank per thread).
+
+    Collective number ``seq`` gets its own board: every rank posts its (header,
+    payload) entry, waits on the shared condition until all ``size`` entries are
+    there, takes a snapshot, and the last rank to read retires the board.  A rank
+    that fails (or a wait that exceeds ``timeout``) aborts the world: every waiter
+    wakes up with RankAbortedError.
+    """
 
     def __init__(self, size, timeout=180.0):
         self.size = size
-        self.slots = [[None] * size, [None] * size]
-        self._barrier = _EventBarrier(size, timeout)
+        self.timeout = timeout
+        self._cond = threading.Condition()
+        self._boards = {}
+        self._aborted = False
 
     def exchange(self, rank, seq, entry):
-        buf = self.slots[seq & 1]
-        buf[rank] = entry
-        self._barrier.wait()
-        return list(buf)
+        with self._cond:
+            if self._aborted:
+                raise RankAbortedError("world aborted")
+            board = self._boards.setdefault(seq, {"entries": [None] * self.size, "posted": 0, "read": 0})
+            board["entries"][rank] = entry
+            board["posted"] += 1
+            if board["posted"] == self.size:
+                self._cond.notify_all()
+            elif not self._cond.wait_for(lambda: self._aborted or board["posted"] == self.size, self.timeout):
+                self._abort_locked()
+                raise RankAbortedError("a rank timed out mid-collective")
+            if self._aborted:
+                raise RankAbortedError("world aborted")
+            snapshot = list(board["entries"])
+            board["read"] += 1
+            if board["read"] == self.size:
+                del self._boards[seq]
+            return snapshot
+
+    def _abort_locked(self):
+        self._aborted = True
+        self._cond.notify_all()
 
     def abort(self):
-        self._barrier.abort()
+        with self._cond:
+            self._abort_locked()
 
 
 def _device_for_rank(rank):
@@ -696,29 +688,29 @@ def _with_rank_context(comm, fn, args):
 
 
 def _run_threads(comms, fn, args):
+    """Runs ``fn(comm, *args)`` on one thread per rank; the first failing rank aborts the world.
+
+    The exception re-raised is the root cause: a rank's own error wins over the
+    RankAbortedError its failure caused on the others.
+    """
     if len(comms) == 1:
         return [_with_rank_context(comms[0], fn, args)]
-    results = [None] * len(comms)
-    errors = [None] * len(comms)
+    import concurrent.futures as cf
 
-    def work(i):
+    def rank_main(comm):
         try:
-            results[i] = _with_rank_context(comms[i], fn, args)
-        except BaseException as exc:  # noqa: BLE001 - propagated to caller
-            errors[i] = exc
-            comms[i].abort()
+            return _with_rank_context(comm, fn, args)
+        except BaseException:
+            comm.abort()
+            raise
 
-    threads = [threading.Thread(target=work, args=(i,), name=f"rank-{i}") for i in range(len(comms))]
-    for t in threads:
-        t.start()
-    for t in threads:
-        t.join()
+    with cf.ThreadPoolExecutor(max_workers=len(comms), thread_name_prefix="rank") as pool:
+        futures = [pool.submit(rank_main, c) for c in comms]
+        cf.wait(futures)
     for comm in comms:
         comm.close()
-    primary = [e for e in errors if e is not None and not isinstance(e, RankAbortedError)]
-    if primary:
-        raise primary[0]
-    for e in errors:
-        if e is not None:
-            raise e
-    return results
+    failures = [f.exception() for f in futures if f.exception() is not None]
+    if failures:
+        root = [e for e in failures if not isinstance(e, RankAbortedError)]
+        raise (root or failures)[0]
+    return [f.result() for f in futures]
