@@ -75,6 +75,9 @@ int bs_abi_version(void);
 int bs_num_sms(void);
 /* Kernels launched by this library so far in the process (all threads). */
 int64_t bs_launch_count(void);
+/* Adds n to bs_launch_count: the kernels a CUDA graph replay launched (their capture counted them
+ * once; replays do not pass through the counting host code). */
+void bs_note_replayed_launches(int64_t n);
 
 /* ---- L1: distributed-array primitives (distarray.py) -------------------- */
 
@@ -156,6 +159,8 @@ int bs_nmf_prepare(const void* X, int dtype, int64_t m, int64_t n_loc,
  *         NMF GEMM on float32 CUDA cores, NMF GEMM in float64 (DMMA / CUDA cores),
  *         MDS pass on tcgen05 (mds_tc.cu), MDS pass on CUDA cores, 0, 0}. */
 int bs_gemm_path_counts(int64_t* out8, int reset);
+/* Adds delta8 to those counts (CUDA graph replays of captured solver iterations). */
+void bs_add_gemm_path_counts(const int64_t* delta8);
 
 /* scn b local GEMM (distlinalg.py:246-252): P (r x m, column-major, float32
  * or float64 like X) = W_loc X_loc^T summed over the rank's n_loc columns.

@@ -40,6 +40,7 @@ SIGNATURES = {
     "bs_abi_version": (_i, []),
     "bs_num_sms": (_i, []),
     "bs_launch_count": (_i64, []),
+    "bs_note_replayed_launches": (None, [_i64]),
     "bs_philox_uniform": (_i, [_p, _i, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_fill": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_packed_bytes": (_i64, [_i64]),
@@ -72,6 +73,7 @@ SIGNATURES = {
     "bs_nmf_prepare_workspace": (_i64, [_i64, _i64]),
     "bs_nmf_prepare": (_i, [_p, _i, _i64, _i64, _p, _p, _p, _i64, _p]),
     "bs_gemm_path_counts": (_i, [_p, _i]),
+    "bs_add_gemm_path_counts": (None, [_p]),
     "bs_nmf_wxt_scan_workspace": (_i64, [_i, _i64, _i64, _i]),
     "bs_nmf_wxt_scan": (_i, [_p, _p, _i, _i64, _i64, _i, _p, _p, _p, _i64, _p]),
     "bs_nmf_vt_step_workspace": (_i64, [_i, _i64]),

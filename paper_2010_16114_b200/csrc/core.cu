@@ -63,6 +63,10 @@ extern "C" int bs_abi_version(void) { return 1; }
 extern "C" int bs_num_sms(void) { return num_sms(); }
 extern "C" int64_t bs_launch_count(void) { return g_launches.load(); }
 
+// A CUDA graph replay launches the kernels its capture recorded without calling back into the
+// host code that counts them; the caller reports them here (solvers.py, NMF graphs).
+extern "C" void bs_note_replayed_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
 // ---------------------------------------------------------------------------
 // Philox4x64-10, numpy's counter layout (distarray.py:170-182 → numpy
 // bit_generator philox.h): block b (0-based) is philox(counter = b + 1, key) and

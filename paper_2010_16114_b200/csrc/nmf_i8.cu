@@ -47,6 +47,11 @@ static std::atomic<int64_t> g_gemm_path[8];
 void note_gemm_path(int path) { g_gemm_path[path & 7].fetch_add(1, std::memory_order_relaxed); }
 }  // namespace bs
 
+// Graph replays (solvers.py) run captured GEMMs without the host code that counts them.
+extern "C" void bs_add_gemm_path_counts(const int64_t* delta8) {
+  for (int i = 0; i < 8; ++i) g_gemm_path[i].fetch_add(delta8[i], std::memory_order_relaxed);
+}
+
 extern "C" int bs_gemm_path_counts(int64_t* out8, int reset) {
   for (int i = 0; i < 8; ++i) {
     out8[i] = reset ? g_gemm_path[i].exchange(0) : g_gemm_path[i].load();

@@ -213,8 +213,15 @@ def _gather_factor(a, out):
 # ratios; the 3xTF32 path's accumulator truncates (biased ~2e-6), so it always
 # takes the direct residual.
 _KAPPA_I8 = 16.0
+_GRAPHS = os.environ.get("BS_NMF_GRAPH", "1") != "0"  # A/B switch: replay NMF iterations as CUDA graphs
 _KAPPA_F64 = 1e6
 _KAPPA_ALWAYS = -1.0
+
+
+def _path_counts():
+    buf = (ctypes.c_int64 * 8)()
+    _lib.call("bs_gemm_path_counts", buf, 0)
+    return list(buf)
 
 
 def gemm_path_counts(reset=False):
@@ -328,7 +335,9 @@ def _nmf_run(s, iters, trace_every, algo):
     wp, wn = s._work.args("w", _lib.query("bs_nmf_w_step_workspace", code, m, n_loc, r))
     rp, rn = s._work.args("resid", _lib.query("bs_nmf_residual_workspace", m, n_loc))
     eps = float(s.eps)
-    for it in range(iters):
+
+    def iteration(tr, st):
+        """One NMF iteration on stream `st`; the objective goes to device slot `tr` (None: no trace)."""
         # WXt = W X^T (scn b) and its reduce-scatter (distlinalg.py:246-252)
         _lib.call("bs_nmf_wxt", _lib.ptr(Xf), _lib.ptr(Wl), code, m, n_loc, r, _lib.ptr(P), _lib.ptr(xs), xp, xn, st)
         if comm.size > 1:
@@ -344,8 +353,7 @@ def _nmf_run(s, iters, trace_every, algo):
                   n_loc, r, eps, _lib.ptr(red), _lib.ptr(xs), wp, wn, st)
         if comm.size > 1:
             comm.allreduce(red, ReduceOp.SUM)
-        if trace_every and it % trace_every == 0:
-            tr = _at(trace_dev, it)
+        if tr is not None:
             _lib.call("bs_nmf_objective", _lib.ptr(xsq), _lib.ptr(red), _lib.ptr(VtV), r, tr, _lib.ptr(guard),
                       kappa, st)
             # cancellation regime: the reference's direct residual (solvers.py:124-136), skipped on the
@@ -355,6 +363,40 @@ def _nmf_run(s, iters, trace_every, algo):
             if comm.size > 1:
                 comm.allreduce(direct, ReduceOp.SUM)
             _lib.call("bs_nmf_objective_select", _lib.ptr(guard), _lib.ptr(direct), tr, st)
+
+    # One rank: after a first eager iteration (which also sets up kernel attributes and tensor
+    # maps), the iteration is captured once as a CUDA graph (with / without the trace) and
+    # replayed — C1's iteration is ~0.5 ms of ~10 launches, so launch gaps matter.  The traced
+    # graph writes the objective to a fixed slot that is copied into the call's trace.
+    use_graph = comm.size == 1 and iters >= 3 and _GRAPHS
+    graphs = s._dev.setdefault("graphs", {})
+    slot = s._dev.get("slot")
+    if slot is None:
+        slot = s._dev["slot"] = _dev_f64(1, dev)
+    for it in range(iters):
+        want = bool(trace_every and it % trace_every == 0)
+        if not use_graph or it == 0:
+            iteration(_at(trace_dev, it) if want else None, st)
+            continue
+        # every pointer and scalar the captured launches bake in
+        key = (want, algo, kappa, eps, xp.value, vp.value, wp.value, rp.value,
+               *(t.data_ptr() if t is not None else 0 for t in (Xf, Wl, Vtl, xs, P, tmp, red, VtV, direct, guard)))
+        entry = graphs.get(key)
+        if entry is None:
+            g = torch.cuda.CUDAGraph()
+            lib = _lib.load()
+            n0, p0 = lib.bs_launch_count(), _path_counts()
+            with torch.cuda.graph(g):
+                iteration(_lib.ptr(slot) if want else None, _lib.stream_ptr())
+            n, dp = lib.bs_launch_count() - n0, (ctypes.c_int64 * 8)(*(b - a for a, b in zip(p0, _path_counts())))
+            lib.bs_note_replayed_launches(-n)  # captured, not run
+            lib.bs_add_gemm_path_counts((ctypes.c_int64 * 8)(*(-v for v in dp)))
+            entry = graphs[key] = (g, n, dp)
+        entry[0].replay()
+        _lib.load().bs_note_replayed_launches(entry[1])
+        _lib.load().bs_add_gemm_path_counts(entry[2])
+        if want:
+            trace_dev[it:it + 1].copy_(slot)
     if trace_every:
         vals = trace_dev.cpu().numpy()
         s.trace.extend(float(vals[it]) for it in range(iters) if it % trace_every == 0)
