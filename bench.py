@@ -64,6 +64,13 @@ def _peaks():
     return 6650.0, "fallback"
 
 
+def _fp64_peak():
+    p = ROOT / "profiles" / "r02_fp_peaks.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["fp64"]["burst_tflops"])
+    return 37.0
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -315,12 +322,22 @@ def _measure(comm, wl, steps, warmup):
     bytes_launch = _bytes_per_launch(dom, wl, comm, data)
     peak, peak_kind = _peaks()
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
+            "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
+            "avg_launch_ms": avg_ms, "share_of_step": tot[dom] / ms}
+    if wl["kind"] == "nmf" and wl["dtype"] == "float64":
+        # float64 NMF GEMMs run on the FP64 tensor pipe (DMMA) at 5 flop/B, past the ridge:
+        # the bound is FP64 throughput (cuBLAS DGEMM measured on a B200, profiles/r02_fp_peaks.json)
+        flops = 2.0 * wl["m"] * data.local.shape[1] * wl["r"]
+        fp64 = _fp64_peak()
+        roof = dict(roof, bound="tensor", unit="TFLOP/s", achieved=flops / (avg_ms * 1e-3) / 1e12,
+                    peak=fp64, peak_source="cuBLAS DGEMM 8192^3 on B200, profiles/r02_fp_peaks.json (measured)",
+                    frac=flops / (avg_ms * 1e-3) / 1e12 / fp64, flops_per_launch=flops,
+                    hbm_frac=achieved / peak)
     res = {
         "value": steps / (ms * 1e-3), "ms_per_step": ms / steps,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
-                     "avg_launch_ms": avg_ms, "share_of_step": tot[dom] / ms},
+        "roofline": roof,
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     return res, st, step, data
