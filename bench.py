@@ -245,10 +245,9 @@ def _setup(comm, wl):
             bs.genotype_fill(x, seed=2016, maf_range=(0.05, 0.5))
             sdt = np.float32
         else:
-            x = bs.empty((m, n), comm, np.dtype(wl["dtype"]))
-            gen = torch.Generator(device=comm.device)
-            gen.manual_seed(2012 + comm.rank)
-            x.local.normal_(generator=gen)
+            # X ~ N(0, 1) (--dist standard_normal) from the counter-based device
+            # generator: the same matrix for any rank count
+            x = bs.normal_fill(bs.empty((m, n), comm, np.dtype(wl["dtype"])), 2012)
             sdt = None
         if wl["dtype"] == "int8":
             # C5: tied survival times handled by Breslow,
@@ -406,7 +405,7 @@ def _run_b200(args, wl):
 
 def _data_desc(wl):
     if wl["kind"] == "cox" and wl["dtype"] != "int8":
-        return "synthetic (device normal draws)"
+        return "synthetic (counter-based Philox Box-Muller normals on device, rank-count independent)"
     if wl["kind"] == "cox":
         return "synthetic (counter-based Philox genotypes, rank-count independent)"
     return "synthetic (numpy-exact Philox rand_fill on device)"

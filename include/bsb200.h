@@ -88,6 +88,13 @@ void bs_note_replayed_launches(int64_t n);
 int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t first,
                       uint64_t key0, uint64_t key1, void* stream);
 
+/* Counter-based standard normals for synthetic inputs (a documented GPU normal;
+ * numpy's ziggurat stream has data-dependent consumption): element e of the global stream is
+ * Box-Muller on Philox4x64-10 block (e/2 + 1, 1, 0, 0) under (key0, key1), so the matrix does not
+ * depend on the rank count.  Writes elements [first, first + count) to out (float32 / float64). */
+int bs_philox_normal(void* out, int dtype, int64_t count, int64_t first,
+                     uint64_t key0, uint64_t key1, void* stream);
+
 /* Counter-based genotype matrix (the C5 input; no reference
  * equivalent -- the reference's rand_fill is float-only, distarray.py:176-177):
  * X[i, j] = [u1 < maf[j - lo]] + [u2 < maf[j - lo]] for the local columns j in

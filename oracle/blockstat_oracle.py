@@ -59,8 +59,8 @@ def philox_key(seed):
     return int(st[0]), int(st[1])
 
 
-def philox_block(b, key):
-    c = [(b + 1) & _MASK, 0, 0, 0]
+def philox_block(b, key, c1=0):
+    c = [(b + 1) & _MASK, c1, 0, 0]
     k0, k1 = key
     for r in range(10):
         if r:
@@ -72,6 +72,21 @@ def philox_block(b, key):
         hi1, lo1 = p1 >> 64, p1 & _MASK
         c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
     return c
+
+
+def philox_normal(seed, first, count):
+    """Elements [first, first+count) of the counter-based normal stream of bs_philox_normal
+    (no reference equivalent: numpy's ziggurat consumes a data-dependent number of words;
+    SURVEY.md §8(f)1).  Element e: Box-Muller on Philox block (e // 2 + 1, 1, 0, 0)."""
+    key = philox_key(seed)
+    out = np.empty(count)
+    for i, e in enumerate(range(first, first + count)):
+        w = philox_block(e // 2, key, c1=1)
+        u1 = ((w[0] >> 11) + 0.5) / 2.0 ** 53
+        u2 = (w[1] >> 11) / 2.0 ** 53
+        r = np.sqrt(-2.0 * np.log(u1))
+        out[i] = r * (np.cos(2.0 * np.pi * u2) if e % 2 == 0 else np.sin(2.0 * np.pi * u2))
+    return out
 
 
 def philox_raw(seed, count):

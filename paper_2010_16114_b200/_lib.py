@@ -42,6 +42,7 @@ SIGNATURES = {
     "bs_launch_count": (_i64, []),
     "bs_note_replayed_launches": (None, [_i64]),
     "bs_philox_uniform": (_i, [_p, _i, _i64, _i64, _u64, _u64, _p]),
+    "bs_philox_normal": (_i, [_p, _i, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_fill": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),
     "bs_genotype_packed_bytes": (_i64, [_i64]),
     "bs_nccl_unique_id": (_i, [_p]),

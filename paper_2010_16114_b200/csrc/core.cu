@@ -147,6 +147,54 @@ extern "C" int bs_philox_uniform(void* out, int dtype, int64_t count, int64_t fi
   return check_launch("bs_philox_uniform");
 }
 
+// Counter-based standard normals (SURVEY §8(f)1 allows a documented GPU normal in place of
+// numpy's ziggurat, whose data-dependent consumption defeats a counter-based restatement).
+// Element e of the global stream takes Philox4x64-10 block (e / 2 + 1, 1, 0, 0) under the seed's
+// key — counter word 1 set, so the words are disjoint from the uniform stream — and Box-Muller:
+// u1 = ((w0 >> 11) + 0.5) 2^-53 in (0, 1), u2 = (w1 >> 11) 2^-53, r = sqrt(-2 ln u1),
+// z = r cos(2 pi u2) for even e, r sin(2 pi u2) for odd e (float64 arithmetic, then rounded).
+// Depends only on (key, e): a column split over any number of ranks draws the same matrix.
+template <typename T>
+__global__ void philox_normal_kernel(T* __restrict__ out, int64_t count, int64_t first, uint64_t k0, uint64_t k1) {
+  const int64_t p_first = first / 2, p_last = (first + count - 1) / 2;
+  for (int64_t p = p_first + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p <= p_last;
+       p += int64_t(gridDim.x) * blockDim.x) {
+    uint64_t c[4] = {uint64_t(p) + 1ULL, 1ULL, 0ULL, 0ULL};
+    philox4x64_10(c, k0, k1);
+    const double u1 = (double(c[0] >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+    const double u2 = double(c[1] >> 11) * (1.0 / 9007199254740992.0);
+    const double r = sqrt(-2.0 * log(u1));
+    double sn, cs;
+    sincospi(2.0 * u2, &sn, &cs);
+    const int64_t e0 = 2 * p;
+    if (e0 >= first && e0 < first + count) out[e0 - first] = T(r * cs);
+    if (e0 + 1 >= first && e0 + 1 < first + count) out[e0 + 1 - first] = T(r * sn);
+  }
+}
+
+extern "C" int bs_philox_normal(void* out, int dtype, int64_t count, int64_t first, uint64_t key0, uint64_t key1,
+                                void* stream) {
+  clear_error();
+  if (count < 0 || first < 0) {
+    set_error("bs_philox_normal: negative count/first");
+    return BS_EINVAL;
+  }
+  if (count == 0) return BS_OK;
+  const int threads = 256;
+  const int grid = int(std::min<int64_t>(ceil_div(count / 2 + 2, threads), int64_t(num_sms()) * 16));
+  if (dtype == BS_F64)
+    philox_normal_kernel<double><<<grid, threads, 0, as_stream(stream)>>>(static_cast<double*>(out), count, first,
+                                                                         key0, key1);
+  else if (dtype == BS_F32)
+    philox_normal_kernel<float><<<grid, threads, 0, as_stream(stream)>>>(static_cast<float*>(out), count, first,
+                                                                        key0, key1);
+  else {
+    set_error("bs_philox_normal: requires a float dtype");
+    return BS_EINVAL;
+  }
+  return check_launch("bs_philox_normal");
+}
+
 // Counter-based genotypes: X[i, j] = [u1 < p_j] + [u2 < p_j] with u1, u2
 // elements 2e, 2e+1 (e = j*m + i, j global) of Generator(Philox(key)).random(., float64) and
 // p_j = maf[j_local].  Each element depends only on (key, i, j): any rank count / partition

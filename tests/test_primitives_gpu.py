@@ -181,3 +181,25 @@ def test_genotype_fill_frequencies():
     x = bs.run_inproc(1, fn)[0].astype(np.float64)
     p = 0.1 + 0.3 * np.random.Generator(np.random.Philox(6)).random(n)
     np.testing.assert_allclose(x.mean(axis=0), 2 * p, atol=0.03)   # Bin(2, p) means
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_normal_fill_is_rank_count_independent_and_normal(dt):
+    """normal_fill (bs_philox_normal): Box-Muller on Philox words keyed by the global index."""
+
+    def fn(comm):
+        a = bs.empty((333, 201), comm, dt)
+        bs.normal_fill(a, 77)
+        return bs.gather_full(a)
+
+    ref = bs.run_inproc(1, fn)[0]
+    for p in (2, 3):
+        np.testing.assert_array_equal(bs.run_inproc(p, fn)[0], ref)
+    # host restatement (oracle.philox_normal): Box-Muller on Philox block (e // 2 + 1, 1, 0, 0)
+    from oracle import blockstat_oracle as orc
+
+    flat = ref.ravel(order="F")
+    for e in (0, 1, 2, 12345, flat.size - 1):
+        z = orc.philox_normal(77, e, 1)[0]
+        assert abs(float(flat[e]) - z) <= (1e-6 if dt == np.float32 else 1e-12) * max(1.0, abs(z))
+    assert abs(flat.mean()) < 0.02 and abs(flat.std() - 1.0) < 0.02
