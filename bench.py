@@ -41,6 +41,9 @@ sys.path.insert(0, str(ROOT))
 WORKLOADS = {
     "nmf_apg_c2": dict(kind="nmf", algo="apg", m=200_000, n=100_000, r=60, dtype="float32",
                        desc="NMF-APG 200000x100000 rank 60 (BASELINE configs[1])"),
+    "nmf_apg_c2_f64": dict(kind="nmf", algo="apg", m=200_000, n=100_000, r=60, dtype="float64",
+                           desc="NMF-APG 200000x100000 rank 60, float64 (the reference's default precision; "
+                                "160 GB: >= 2 GPUs) (BASELINE configs[1])"),
     "nmf_mu_c1": dict(kind="nmf", algo="mu", m=10_000, n=10_000, r=20, dtype="float64",
                       desc="NMF-MU 10000x10000 rank 20 (BASELINE configs[0])"),
     "mds_c3": dict(kind="mds", n=100_000, d=1000, q=20, dtype="float32",
