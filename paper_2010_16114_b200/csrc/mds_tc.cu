@@ -51,7 +51,7 @@ constexpr int KP = 32;           // augmented q padded (one 128-byte row of fp32
 constexpr int Y_BOX = 32 * 4 * BJ;   // 16 KB
 constexpr int Y_STAGE = 2 * Y_BOX;
 constexpr int B_STAGE = 16384;       // hi at 0, lo at 8192
-constexpr int NY = 3, NB1 = 2, NB2 = 4;
+constexpr int NY = 4, NB1 = 2, NB2 = 3;  // Y is held until its pairs are done
 constexpr int OFF_B1 = NY * Y_STAGE;
 constexpr int OFF_B2 = OFF_B1 + NB1 * B_STAGE;
 constexpr int RINGS = OFF_B2 + NB2 * B_STAGE;
@@ -71,6 +71,24 @@ __device__ __forceinline__ void mma3_kstep(uint32_t d, uint32_t a_hi, uint32_t a
       "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, 1;\n\t}" ::"r"(d),
       "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(id), "r"(acc0)
       : "memory");
+}
+
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)), "l"(*reinterpret_cast<uint64_t*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
 }
 
 __device__ __forceinline__ float rsqrt_approx(float x) {
@@ -127,6 +145,9 @@ __device__ __noinline__ float careful_block(float* buf, int64_t ib, int64_t i_en
 
 constexpr int TR_CHUNKS = 4096;  // trace: first chunks of CTA 0
 __device__ __forceinline__ void tr_mark(unsigned long long* tr, int ev, uint32_t chunk) {
+#ifndef BS_DEBUG_MODES
+  return;  // the event trace (BS_MDS_TC_TRACE) exists only in debug builds
+#endif
   if (tr && blockIdx.x == 0 && chunk < TR_CHUNKS) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -288,7 +309,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       unit_range(u, j0, i0, nch, seg);
       mbar_wait_sleep(a1_full, ut & 1);
       tc_fence_after();
-      int t1 = 0, t2 = 0;
+      int t1 = 0, t2 = 0, g2 = 0;  // g2 = t2 mod G (no division in the loop)
       while (t2 < nch) {
         bool issued = false;
         if (t1 < nch) {  // bounded by d1_empty: at most two chunks ahead of the epilogue's D1 reads
@@ -322,8 +343,8 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const uint32_t c = cbase + uint32_t(t2);
           const uint32_t b = c & 1;
           const int s = int(c % NB2);
-          const bool first = (t2 % a.G) == 0;
-          const bool last = ((t2 % a.G) == a.G - 1) || (t2 == nch - 1);
+          const bool first = g2 == 0;
+          const bool last = (g2 == a.G - 1) || (t2 == nch - 1);
           int probe = 0;
           if (lane == 0)
             probe = mbar_test(a2_full(b), (c >> 1) & 1) && (!first || mbar_test(d2_empty, (gi & 1) ^ 1)) &&
@@ -348,6 +369,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
             }
             __syncwarp();
             ++t2;
+            g2 = g2 == a.G - 1 ? 0 : g2 + 1;
             issued = true;
           }
         }
@@ -397,6 +419,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
 #pragma unroll
       for (int k = 0; k < 8; ++k) Tacc[k] = 0.f;
       bool fold_pending = false;
+      int gpos = 0;  // t mod G
       auto fold = [&]() {
         mbar_wait(d2_full, gi & 1);
         tc_fence_after();
@@ -424,7 +447,9 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const uint32_t c0 = uint32_t(sub & 1) * 4u;
 #pragma unroll
           for (int c = 0; c < 4; ++c) yv[c] = ld_shared_v4(ybase + (((c0 + uint32_t(c)) ^ uint32_t(jrow & 7)) << 4));
-          mbar_arrive(y_empty(s));  // in registers: the TMA may refill the stage
+          // y_empty is signalled only after the pair math has used every loaded value: an arrive
+          // right behind the LDS does not wait for them to return (the TMA then refilled the stage
+          // under the load — seen as run-to-run differences once the math was rescheduled)
         }
         float y[16];
 #pragma unroll
@@ -445,20 +470,28 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
 #pragma unroll
           for (int e = 0; e < 16; ++e) wz[e] = wl[e] = g[e] ^ __float_as_uint(y[e]);
         } else {
+        // two pairs per packed f32x2 instruction (same per-element roundings as the scalar chain;
+        // the slice's stress is summed in two interleaved chains)
+        float2 st2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const float d2 = __uint_as_float(g[e]);  // |ti|^2 + |tj|^2 - 2 ti.tj  (solvers.py:246)
-          dmin = fminf(dmin, d2);
-          const float r = rsqrt_approx(d2);
-          const float d = d2 * r;
-          const float z = y[e] * r;               // solvers.py:297
-          const float er = y[e] - d;
-          st_blk = fmaf(er, er, st_blk);
-          const float w = 1.f - z;                // solvers.py:299
-          const uint32_t hw = tf32_hi(__float_as_uint(w));
-          wz[e] = hw;
-          wl[e] = __float_as_uint(w - __uint_as_float(hw));
+        for (int e = 0; e < 16; e += 2) {
+          const float2 d2 = make_float2(__uint_as_float(g[e]), __uint_as_float(g[e + 1]));  // solvers.py:246
+          dmin = fminf(dmin, fminf(d2.x, d2.y));
+          const float2 r = make_float2(rsqrt_approx(d2.x), rsqrt_approx(d2.y));
+          const float2 yy = make_float2(y[e], y[e + 1]);
+          const float2 d = mul2(d2, r);
+          const float2 z = mul2(yy, r);        // solvers.py:297
+          const float2 er = sub2(yy, d);
+          st2 = fma2(er, er, st2);
+          const float2 w = sub2(make_float2(1.f, 1.f), z);  // solvers.py:299
+          const uint32_t h0 = tf32_hi(__float_as_uint(w.x)), h1 = tf32_hi(__float_as_uint(w.y));
+          const float2 lo = sub2(w, make_float2(__uint_as_float(h0), __uint_as_float(h1)));
+          wz[e] = h0;
+          wz[e + 1] = h1;
+          wl[e] = __float_as_uint(lo.x);
+          wl[e + 1] = __float_as_uint(lo.y);
         }
+        st_blk = st2.x + st2.y;
         }
         const bool bad = !(a.mode & 1) && (!(dmin > thr) || !live || (ib + 16 > i_end) || (jg >= ib && jg < ib + 16));
         if (bad) {
@@ -479,6 +512,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
             wl[e] = __float_as_uint(w - __uint_as_float(hw));
           }
         }
+        mbar_arrive(y_empty(s));  // behind the math that consumed every y value
         stress += double(st_blk);
         // A2 <- hi | lo of W for this chunk
         mbar_wait(a2_empty(b), ((cc >> 1) & 1) ^ 1);
@@ -493,7 +527,8 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         mbar_arrive(a2_full(b));
         if (warp == 2 && lane == 0) tr_mark(a.trace, 4, cc);  // A2 written (warp 2)
         if (fold_pending) fold();
-        if ((t % a.G) == a.G - 1 || t == nch - 1) fold_pending = true;
+        if (gpos == a.G - 1 || t == nch - 1) fold_pending = true;
+        gpos = gpos == a.G - 1 ? 0 : gpos + 1;
       }
       if (fold_pending) fold();
       // ---- unit outputs: T (each slice owns 8 of the augmented k) and zsum = #i - sum_i w ----
