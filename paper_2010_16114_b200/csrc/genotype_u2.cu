@@ -412,8 +412,6 @@ grad_u2_ring_kernel(const uint32_t* __restrict__ P, const double* __restrict__ v
           const uint32_t addr = my + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF);
           asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[u].x), "=r"(w[u].y) : "r"(addr));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + 8 * s);
         ++k;
 #pragma unroll
         for (int u = 0; u < CF; ++u) {
@@ -426,6 +424,10 @@ grad_u2_ring_kernel(const uint32_t* __restrict__ P, const double* __restrict__ v
             cs[CF * b + u] = s0 + s1;
           }
         }
+        // the stage is released only behind the math that consumed every word read from it
+        // (an arrive right behind the loads does not wait for them to return)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
       } else {
 #pragma unroll
         for (int u = 0; u < CF; ++u) cs[CF * b + u] = 0.f;
@@ -520,8 +522,6 @@ xbeta_u2_ring_kernel(const uint32_t* __restrict__ P, const float* __restrict__ b
 #pragma unroll
         for (int u = 0; u < CF; ++u)
           w[u] = ld_shared_u32(ring + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF) + 4 * t);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + 8 * s);
         ++k;
         const int nc = int(j_end - j < CF ? j_end - j : CF);
 #pragma unroll
@@ -546,6 +546,10 @@ xbeta_u2_ring_kernel(const uint32_t* __restrict__ P, const float* __restrict__ b
             }
           }
         }
+        // the stage is released only behind the math that consumed every word read from it
+        // (an arrive right behind the loads does not wait for them to return)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
       }
     }
 #pragma unroll
@@ -627,8 +631,6 @@ grad_i8_ring_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, 
         for (int u = 0; u < CF; ++u)
 #pragma unroll
           for (int h = 0; h < 2; ++h) w[u][h] = ld_shared_v4(my + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF) + 512 * h);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + 8 * s);
         ++k;
 #pragma unroll
         for (int u = 0; u < CF; ++u) {
@@ -647,6 +649,10 @@ grad_i8_ring_kernel(const int8_t* __restrict__ X, const double* __restrict__ v, 
           u2_unpack(acc, s0, s1);
           cs[CF * b + u] = s0 + s1;
         }
+        // the stage is released only behind the math that consumed every word read from it
+        // (an arrive right behind the loads does not wait for them to return)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
       } else {
 #pragma unroll
         for (int u = 0; u < CF; ++u) cs[CF * b + u] = 0.f;
@@ -711,8 +717,6 @@ xbeta_i8_ring_kernel(const int8_t* __restrict__ X, const float* __restrict__ bet
         uint4 w[CF];
 #pragma unroll
         for (int u = 0; u < CF; ++u) w[u] = ld_shared_v4(ring + s * UR_STAGE_BYTES + u * (UR_STAGE_BYTES / CF) + 16 * t);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + 8 * s);
         ++k;
         const int nc = int(j_end - j < CF ? j_end - j : CF);
 #pragma unroll
@@ -727,6 +731,10 @@ xbeta_i8_ring_kernel(const int8_t* __restrict__ X, const float* __restrict__ bet
             acc[2 * a + 1] = u2_fma2(i8r_pair(q4[a], 2), bb, acc[2 * a + 1]);
           }
         }
+        // the stage is released only behind the math that consumed every word read from it
+        // (an arrive right behind the loads does not wait for them to return)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + 8 * s);
       }
     }
 #pragma unroll
