@@ -132,11 +132,24 @@ __global__ void sum_slabs_f64(const double* __restrict__ parts, int S, int64_t l
   }
 }
 
+// packed genotypes, float32 arithmetic: the integer tensor-core gradient pass (genotype_tc.cu);
+// BS_U2_TC=0 restores the CUDA-core ring kernel (A/B only)
+static bool u2_tc() {
+  static const bool on = [] {
+    const char* e = getenv("BS_U2_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 static int xsize(int xdtype) { return xdtype == BS_F64 ? 8 : xdtype == BS_F32 ? 4 : 1; }  // BS_U2: 16 rows / word
 
 namespace bs {
 int launch_xbeta_u2(const void* P, const void* beta, bool f64, int64_t m, int64_t n_loc, int64_t splits,
                     int64_t cps, double* parts, int* splits_used, cudaStream_t st);
+int64_t u2_grad_tc_workspace(int64_t m);
+bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
+                       Workspace& ws, cudaStream_t st, int* rc);
 int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t n_loc, int groups, int segs,
                    int64_t cpg, double* parts, const int* flags, cudaStream_t st);
 bool launch_xbeta_i8_ring(const int8_t* X, const float* beta, int64_t m, int64_t n_loc, int64_t splits,
@@ -865,10 +878,9 @@ static int prox_grid(int64_t n_loc) {
 }
 
 extern "C" int64_t bs_cox_grad_workspace(int xdtype, int64_t m, int64_t n_loc) {
-  (void)xdtype;
   GrGrid g = gr_grid(m, n_loc);
   return ws_bytes<double>(int64_t(g.segs) * std::max<int64_t>(n_loc, 1)) + ws_bytes<unsigned int>(1) +
-         ws_bytes<double>(prox_grid(n_loc));
+         ws_bytes<double>(prox_grid(n_loc)) + (xdtype == BS_U2 ? u2_grad_tc_workspace(m) : 0);
 }
 
 // scn p for int8 X with float32 arithmetic.  Warp w of a CTA owns rows
@@ -990,11 +1002,18 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
   const int pg = prox_grid(n_loc);
   double* bparts = ws.take<double>(pg);
   if (!parts || !counter || !bparts) { set_error("bs_cox_grad_step: workspace too small"); return BS_EWORK; }
+  int segs_used = g.segs;
   if (m == 0) {
     if (cudaMemsetAsync(parts, 0, sizeof(double) * n_loc, st) != cudaSuccess) return BS_ECUDA;
   } else {
     const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-    if (xdtype == BS_U2) {
+    int tc_rc = BS_OK;
+    if (xdtype == BS_U2 && dtype == BS_F32 && u2_tc() &&
+        launch_grad_u2_tc(X, dmpd, m, n_loc, parts, flags, ws, st, &tc_rc)) {
+      // integer tensor-core pass (genotype_tc.cu): one slab
+      if (tc_rc != BS_OK) return tc_rc;
+      segs_used = 1;
+    } else if (xdtype == BS_U2) {
       launch_grad_u2(X, dtype == BS_F64, dmpd, m, n_loc, g.groups, g.segs, g.cpg, parts, flags, st);
     } else if (xdtype == BS_F64) launch_grad<double>(static_cast<const double*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else if (xdtype == BS_F32) launch_grad<float>(static_cast<const float*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
@@ -1006,7 +1025,7 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
     } else if (xdtype == BS_I8) launch_grad<int8_t>(static_cast<const int8_t*>(X), dmpd, m, n_loc, g, vec_ok, parts, flags, st);
     else { set_error("bs_cox_grad_step: unsupported X dtype %d", xdtype); return BS_EINVAL; }
   }
-  const int segs = m == 0 ? 1 : g.segs;
+  const int segs = m == 0 ? 1 : segs_used;
   if (dtype == BS_F64)
     prox_kernel<double><<<pg, 256, 0, st>>>(parts, segs, n_loc, static_cast<double*>(grad), static_cast<double*>(beta),
                                             sigma, lam, do_step, bparts, counter, l1_dev, flags);

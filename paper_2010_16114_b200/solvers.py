@@ -229,14 +229,15 @@ def gemm_path_counts(reset=False):
 
     Keys: ``integer`` (tcgen05 kind::i8 digit slices), ``tf32`` (tcgen05 3xTF32),
     ``cuda_core`` (float32 CUDA cores), ``float64`` (DMMA / CUDA cores); ``tensor`` = the
-    first two together; ``mds_tensor`` / ``mds_cuda_core``: MDS passes (bs_mds_pass).
+    first two together; ``mds_tensor`` / ``mds_cuda_core``: MDS passes (bs_mds_pass);
+    ``cox_packed_tensor``: packed-genotype Cox gradient passes on the integer tensor cores.
     """
     import ctypes as C
 
     buf = (C.c_int64 * 8)()
     _lib.call("bs_gemm_path_counts", buf, 1 if reset else 0)
     d = {"integer": buf[0], "tf32": buf[1], "cuda_core": buf[2], "float64": buf[3], "mds_tensor": buf[4],
-         "mds_cuda_core": buf[5]}
+         "mds_cuda_core": buf[5], "cox_packed_tensor": buf[6]}
     d["tensor"] = d["integer"] + d["tf32"]
     return d
 
