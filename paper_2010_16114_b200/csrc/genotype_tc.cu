@@ -288,10 +288,14 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         mbar_wait(raw_full(rst), (jj / RS) & 1);
         mbar_wait(a_empty(cst), ((jj / CS) & 1) ^ 1);
         tc_fence_after();
+        // the tile row (128 B) sits in SWIZZLE_128B: 16-byte chunk c of row r at chunk c ^ (r % 8),
+        // so the 32 lanes' reads of one chunk spread over the banks
         const uint32_t src = smem_u32(smem + rst * X_BYTES) + uint32_t(col) * BKB;
+        const uint32_t sw = uint32_t(col & 7);
 #pragma unroll
         for (int h = 0; h < BKB / 32; ++h) {  // 32 packed bytes -> 32 words -> one TMEM store
-          const uint4 p0 = ld_shared_v4(src + 32 * h), p1 = ld_shared_v4(src + 32 * h + 16);
+          const uint4 p0 = ld_shared_v4(src + ((uint32_t(2 * h) ^ sw) << 4));
+          const uint4 p1 = ld_shared_v4(src + ((uint32_t(2 * h + 1) ^ sw) << 4));
           const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
           uint32_t u[32];
 #pragma unroll
@@ -323,7 +327,7 @@ bool make_map_u8(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, u
   cuuint32_t box[2] = {b0, b1};
   cuuint32_t es[2] = {1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
