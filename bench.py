@@ -327,7 +327,10 @@ def _measure(comm, wl, steps, warmup):
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
             "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
-            "avg_launch_ms": avg_ms, "share_of_step": tot[dom] / ms}
+            "avg_launch_ms": avg_ms, "launches_timed": len(per[dom]),
+            # one launch of the dominant entry point per iteration (replayed CUDA-graph iterations
+            # are not individually timed, so the share is per-launch time over per-step time)
+            "share_of_step": avg_ms / (ms / steps)}
     if wl["kind"] == "nmf" and wl["dtype"] == "float64":
         # float64 NMF GEMMs run on the FP64 tensor pipe (DMMA) at 5 flop/B, past the ridge:
         # the bound is FP64 throughput (cuBLAS DGEMM measured on a B200, profiles/r02_fp_peaks.json)

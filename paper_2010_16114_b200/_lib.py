@@ -185,6 +185,8 @@ def call(name, *args):
     if prof:
         import torch
 
+        prof = not torch.cuda.is_current_stream_capturing()  # graph captures are timed by their replays
+    if prof:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()

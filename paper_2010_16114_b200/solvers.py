@@ -365,11 +365,12 @@ def _nmf_run(s, iters, trace_every, algo):
                 comm.allreduce(direct, ReduceOp.SUM)
             _lib.call("bs_nmf_objective_select", _lib.ptr(guard), _lib.ptr(direct), tr, st)
 
-    # One rank: after a first eager iteration (which also sets up kernel attributes and tensor
-    # maps), the iteration is captured once as a CUDA graph (with / without the trace) and
-    # replayed — C1's iteration is ~0.5 ms of ~10 launches, so launch gaps matter.  The traced
+    # One rank, X under 4 GiB: after a first eager iteration (which also sets up kernel attributes
+    # and tensor maps), the iteration is captured once as a CUDA graph (with / without the trace)
+    # and replayed — C1's iteration is ~0.5 ms of ~10 launches, so launch gaps matter.  The traced
     # graph writes the objective to a fixed slot that is copied into the call's trace.
-    use_graph = comm.size == 1 and iters >= 3 and _GRAPHS
+    # Only where launches matter: a C2-sized iteration (80 GB of X, ~30 ms) gains nothing.
+    use_graph = comm.size == 1 and iters >= 3 and _GRAPHS and Xf.numel() * Xf.element_size() < (4 << 30)
     graphs = s._dev.setdefault("graphs", {})
     slot = s._dev.get("slot")
     if slot is None:
