@@ -48,6 +48,7 @@ extern "C" {
 #define BS_I64 2
 #define BS_I8 3
 #define BS_U2 4  /* 2-bit packed genotypes (X only; see bs_genotype_pack) */
+#define BS_U2T 5 /* the packed transpose of a BS_U2 block (bs_cox_xbeta only; see bs_genotype_transpose_packed) */
 
 /* ReduceOp codes (comm.py:54-58) */
 #define BS_SUM 0
@@ -113,6 +114,12 @@ int bs_genotype_pack(const int8_t* X, int64_t m, int64_t n_loc, void* P, void* s
 int bs_genotype_unpack(const void* P, int64_t m, int64_t n_loc, int8_t* X, void* stream);
 int bs_genotype_fill_packed(void* P, const double* maf, int64_t m, int64_t lo, int64_t n_loc,
                             uint64_t key0, uint64_t key1, void* stream);
+/* Q = the packed (n_loc x m) transpose of the packed (m x n_loc) block P: row i of X takes
+ * bs_genotype_packed_bytes(n_loc) bytes at offset i * that, genotype j in bits 2(j%4)..+1 of
+ * byte j/4.  Passed as X with xdtype BS_U2T, bs_cox_xbeta (dtype BS_F32) computes X beta on
+ * the integer tensor cores from Q with the same pass as the packed gradient (an addition:
+ * the layout trades the memory of a second copy for a K-major operand). */
+int bs_genotype_transpose_packed(const void* P, int64_t m, int64_t n_loc, void* Q, void* stream);
 
 /* reduce_all local fold (distarray.py:335-348): out_dev[0] = op over
  * transform(x[0..count)) in float64.  Empty input gives the neutral element. */

@@ -21,7 +21,7 @@ HEADER = PKG.parent / "include" / "bsb200.h"
 # status codes (bsb200.h)
 BS_OK, BS_EINVAL, BS_ECUDA, BS_EWORK, BS_ENUMERIC, BS_ENCCL, BS_EDEGEN = 0, 1, 2, 3, 4, 5, 6
 # dtype codes (comm.py:68-72 + int8)
-BS_F32, BS_F64, BS_I64, BS_I8, BS_U2 = 0, 1, 2, 3, 4
+BS_F32, BS_F64, BS_I64, BS_I8, BS_U2, BS_U2T = 0, 1, 2, 3, 4, 5
 # ReduceOp codes (comm.py:54-58 order)
 BS_SUM, BS_PROD, BS_MAX, BS_MIN = 0, 1, 2, 3
 BS_T_NONE, BS_T_ABS, BS_T_SQUARE = 0, 1, 2
@@ -60,6 +60,7 @@ SIGNATURES = {
     "bs_genotype_pack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_unpack": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_genotype_fill_packed": (_i, [_p, _p, _i64, _i64, _i64, _u64, _u64, _p]),
+    "bs_genotype_transpose_packed": (_i, [_p, _i64, _i64, _p, _p]),
     "bs_reduce_workspace": (_i64, [_i64]),
     "bs_reduce": (_i, [_p, _i, _i64, _i, _i, _p, _p, _i64, _p]),
     "bs_fold": (_i, [_p, _p, _i, _i64, _i, _i, _p]),

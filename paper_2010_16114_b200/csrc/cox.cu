@@ -150,6 +150,8 @@ int launch_xbeta_u2(const void* P, const void* beta, bool f64, int64_t m, int64_
 int64_t u2_grad_tc_workspace(int64_t m);
 bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
                        Workspace& ws, cudaStream_t st, int* rc);
+bool launch_xbeta_u2t_tc(const void* Q, const float* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
+                         cudaStream_t st, int* rc);
 int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t n_loc, int groups, int segs,
                    int64_t cpg, double* parts, const int* flags, cudaStream_t st);
 bool launch_xbeta_i8_ring(const int8_t* X, const float* beta, int64_t m, int64_t n_loc, int64_t splits,
@@ -179,6 +181,7 @@ static XbGrid xb_grid(int xdtype, int64_t m, int64_t n_loc, bool vec_ok) {
 }
 
 extern "C" int64_t bs_cox_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) {
+  if (xdtype == BS_U2T) return u2_grad_tc_workspace(n_loc);
   XbGrid g = xb_grid(xdtype, m, n_loc, false);  // vec=1 gives the most tiles, splits <= that case
   XbGrid h = xb_grid(xdtype, m, n_loc, true);
   return ws_bytes<double>(int64_t(std::max(g.splits, h.splits)) * m);
@@ -281,6 +284,16 @@ extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dty
   if (m < 0 || n_loc < 0) { set_error("bs_cox_xbeta: negative shape"); return BS_EINVAL; }
   if (m == 0) return BS_OK;
   if (n_loc == 0) return cudaMemsetAsync(out, 0, sizeof(double) * m, st) == cudaSuccess ? BS_OK : BS_ECUDA;
+  if (xdtype == BS_U2T) {  // packed transpose, float32: one integer tensor-core pass (genotype_tc.cu)
+    if (dtype != BS_F32) { set_error("bs_cox_xbeta: BS_U2T takes float32 beta"); return BS_EINVAL; }
+    Workspace ws(work, work_bytes);
+    int rc = BS_OK;
+    if (!launch_xbeta_u2t_tc(X, static_cast<const float*>(beta), m, n_loc, out, ws, st, &rc)) {
+      set_error("bs_cox_xbeta: BS_U2T needs the tcgen05 path (sm_100a, 16-byte aligned X)");
+      return BS_EINVAL;
+    }
+    return rc;
+  }
   const bool vec_ok = xdtype == BS_U2 ||
                       ((m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0));
   XbGrid g = xb_grid(xdtype, m, n_loc, vec_ok);

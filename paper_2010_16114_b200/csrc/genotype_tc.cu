@@ -70,7 +70,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // image row n, k-block kb: canonical K-major SWIZZLE_NONE, 8 rows x 16 B core matrices,
 // K-chunk stride 128 B, 8-row-group stride B_SBO.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) vdigits_kernel(const double* __restrict__ v, int64_t m,
+template <typename T>
+__global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, int64_t m,
                                                       uint8_t* __restrict__ img, double* __restrict__ gscale,
                                                       const int* flags) {
   __shared__ double smax[4];
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(128) vdigits_kernel(const double* __restrict__
   double mx = 0.0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    vv[e] = (i0 + e < m) ? v[i0 + e] : 0.0;
+    vv[e] = (i0 + e < m) ? double(v[i0 + e]) : 0.0;
     mx = fmax(mx, fabs(vv[e]));
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -319,6 +320,62 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// packed transpose: Q = the packed (n x m) transpose of the packed (m x n) block P, so that
+// X beta = Q^T beta runs through the same pass (K = the n columns, M = the m rows).
+// CTA tile: 128 rows (32 bytes of each column) x 128 columns (32 bytes of each output row).
+// Thread (a4 = word, jb = column byte) takes the 4 x 4 genotypes of one byte in each of four
+// columns, gathers them into one word (byte c = column c) and transposes the 2-bit fields in
+// place with two delta swaps (byte r = row r).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) u2_transpose_kernel(const uint8_t* __restrict__ P, int64_t m, int64_t n,
+                                                           int64_t ld, uint8_t* __restrict__ Q, int64_t ldT) {
+  __shared__ uint32_t s_in[128][9];                // column c: 8 words (128 rows), one word of padding
+  __shared__ __align__(16) uint8_t s_out[128][32];  // output row r: 32 bytes (128 columns)
+  const int t = threadIdx.x;
+  const int64_t i0 = int64_t(blockIdx.x) * 128;
+  const int64_t ntj = (n + 127) / 128;
+  for (int64_t tj = blockIdx.y; tj < ntj; tj += gridDim.y) {
+    const int64_t j0 = tj * 128;
+    {
+      const int c = t >> 1, h = t & 1;
+      const int64_t b = i0 / 4 + 16 * h;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (j0 + c < n && b < ld) v = *reinterpret_cast<const uint4*>(P + (j0 + c) * ld + b);
+      s_in[c][4 * h] = v.x;
+      s_in[c][4 * h + 1] = v.y;
+      s_in[c][4 * h + 2] = v.z;
+      s_in[c][4 * h + 3] = v.w;
+    }
+    __syncthreads();
+    {
+      const int jb = t & 31, a4 = t >> 5;
+      const uint32_t w0 = s_in[4 * jb][a4], w1 = s_in[4 * jb + 1][a4];
+      const uint32_t w2 = s_in[4 * jb + 2][a4], w3 = s_in[4 * jb + 3][a4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t sel = uint32_t(e) | (uint32_t(e + 4) << 4);
+        uint32_t w = __byte_perm(__byte_perm(w0, w1, sel), __byte_perm(w2, w3, sel), 0x5410u);
+        uint32_t x = ((w >> 6) ^ w) & 0x00CC00CCu;
+        w ^= x ^ (x << 6);
+        x = ((w >> 12) ^ w) & 0x0000F0F0u;
+        w ^= x ^ (x << 12);
+        const int row = 4 * (4 * a4 + e);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s_out[row + r][jb] = uint8_t(w >> (8 * r));
+      }
+    }
+    __syncthreads();
+    {
+      const int r = t >> 1, h = t & 1;
+      const int64_t b = j0 / 4 + 16 * h;
+      if (i0 + r < m && b < ldT)
+        *reinterpret_cast<uint4*>(Q + (i0 + r) * ldT + b) = *reinterpret_cast<const uint4*>(&s_out[r][16 * h]);
+    }
+    __syncthreads();
+  }
+}
+
 bool make_map_u8(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint32_t b0, uint32_t b1) {
   auto fn = encode_fn();
   if (!fn) return false;
@@ -340,31 +397,55 @@ int64_t u2_grad_tc_workspace(int64_t m) {
   return ws_bytes<uint8_t>(ng * G * B_BYTES) + ws_bytes<double>(ng);
 }
 
-// grad partials (one slab: out[j], j < n_loc) of packed X against v on the tensor cores.
-// Returns false when the path does not apply (no tcgen05, or the tensor map is refused).
-bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
-                       Workspace& ws, cudaStream_t st, int* rc) {
+// One tensor-core pass: out[j] = sum_k P[k, j] v[k] for the packed (K x M) block P (ld =
+// ceil(K / 64) * 16 bytes per column), one slab.  Returns false when the path does not apply
+// (no tcgen05, misaligned P, or the tensor map is refused).
+template <typename T>
+static bool u2_tc_pass(const void* P, const T* v, int64_t K, int64_t M, double* out, const int* flags, Workspace& ws,
+                       cudaStream_t st, int* rc, const char* what) {
   *rc = BS_OK;
-  if (!tc_enabled() || m <= 0 || n_loc <= 0 || (reinterpret_cast<uintptr_t>(P) & 15)) return false;
-  const int64_t ld = ((m + 63) / 64) * 16;
-  const int64_t nkb = (m + BKR - 1) / BKR, ng = (nkb + G - 1) / G;
+  if (!tc_enabled() || K <= 0 || M <= 0 || (reinterpret_cast<uintptr_t>(P) & 15)) return false;
+  const int64_t ld = ((K + 63) / 64) * 16;
+  const int64_t nkb = (K + BKR - 1) / BKR, ng = (nkb + G - 1) / G;
   uint8_t* img = ws.take<uint8_t>(ng * G * B_BYTES);
   double* gscale = ws.take<double>(ng);
   if (!img || !gscale) {
-    set_error("u2 tensor-core grad: workspace too small");
+    set_error("%s: workspace too small", what);
     *rc = BS_EWORK;
     return true;
   }
   CUtensorMap tm;
-  if (!make_map_u8(&tm, P, uint64_t(ld), uint64_t(n_loc), BKB, BM)) return false;
-  vdigits_kernel<<<int(ng), 128, 0, st>>>(v, m, img, gscale, flags);
-  const int tiles = int((n_loc + BM - 1) / BM);
+  if (!make_map_u8(&tm, P, uint64_t(ld), uint64_t(M), BKB, BM)) return false;
+  vdigits_kernel<T><<<int(ng), 128, 0, st>>>(v, K, img, gscale, flags);
+  const int tiles = int((M + BM - 1) / BM);
   const int grid = std::min(tiles, num_sms());
   smem_attr(gradtc_kernel, SMEM);
-  gradtc_kernel<<<grid, THREADS, SMEM, st>>>(tm, img, gscale, m, n_loc, tiles, out, flags);
-  *rc = check_launch("u2 tensor-core grad", 2);
+  gradtc_kernel<<<grid, THREADS, SMEM, st>>>(tm, img, gscale, K, M, tiles, out, flags);
+  *rc = check_launch(what, 2);
   note_gemm_path(6);
   return true;
+}
+
+// grad partials (one slab: out[j], j < n_loc) of packed X against v on the tensor cores.
+bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
+                       Workspace& ws, cudaStream_t st, int* rc) {
+  return u2_tc_pass<double>(P, v, m, n_loc, out, flags, ws, st, rc, "u2 tensor-core grad");
+}
+
+// X beta (out[i], i < m) from the packed transpose Q of the local block (bs_genotype_transpose_packed):
+// the same pass with K = n_loc and M = m.
+bool launch_xbeta_u2t_tc(const void* Q, const float* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
+                         cudaStream_t st, int* rc) {
+  return u2_tc_pass<float>(Q, beta, n_loc, m, out, nullptr, ws, st, rc, "u2 tensor-core xbeta");
+}
+
+int launch_u2_transpose(const void* P, int64_t m, int64_t n, void* Q, cudaStream_t st) {
+  const int64_t ld = ((m + 63) / 64) * 16, ldT = ((n + 63) / 64) * 16;
+  const int64_t nti = (m + 127) / 128, ntj = (n + 127) / 128;
+  if (nti > 0x7fffffffLL) return BS_EINVAL;
+  dim3 grid(unsigned(nti), unsigned(std::min<int64_t>(ntj, 65535)));
+  u2_transpose_kernel<<<grid, 256, 0, st>>>(static_cast<const uint8_t*>(P), m, n, ld, static_cast<uint8_t*>(Q), ldT);
+  return check_launch("bs_genotype_transpose_packed", 1);
 }
 
 }  // namespace bs

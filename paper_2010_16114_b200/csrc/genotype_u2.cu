@@ -949,6 +949,21 @@ extern "C" int bs_genotype_pack(const int8_t* X, int64_t m, int64_t n_loc, void*
   return check_launch("bs_genotype_pack");
 }
 
+namespace bs {
+int launch_u2_transpose(const void* P, int64_t m, int64_t n, void* Q, cudaStream_t st);
+}
+
+extern "C" int bs_genotype_transpose_packed(const void* P, int64_t m, int64_t n_loc, void* Q, void* stream) {
+  clear_error();
+  if (m < 0 || n_loc < 0) { set_error("bs_genotype_transpose_packed: negative shape"); return BS_EINVAL; }
+  if (m == 0 || n_loc == 0) return BS_OK;
+  if ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Q)) & 15) {
+    set_error("bs_genotype_transpose_packed: P and Q must be 16-byte aligned");
+    return BS_EINVAL;
+  }
+  return bs::launch_u2_transpose(P, m, n_loc, Q, as_stream(stream));
+}
+
 extern "C" int bs_genotype_unpack(const void* P, int64_t m, int64_t n_loc, int8_t* X, void* stream) {
   clear_error();
   if (m < 0 || n_loc < 0) { set_error("bs_genotype_unpack: negative shape"); return BS_EINVAL; }

@@ -683,7 +683,36 @@ def cox_init(x, y, delta, lam, sigma=None, ties="none", dtype=None):
                   "flags": torch.zeros(1, dtype=torch.int32, device=dev),
                   "no_ties": ties == "none"}
     state._work = _Work(dev)
+    xt = _packed_transpose(x, sdt)
+    if xt is not None:
+        state._dev["xt"] = xt
     return state
+
+
+_U2_XT = os.environ.get("BS_U2_XT", "1") != "0"  # A/B switch: X beta from a packed transpose
+
+
+def _packed_transpose(x, sdt):
+    """The packed transpose of a PackedGenotypes block for float32 arithmetic, or None.
+
+    X beta then runs on the integer tensor cores as the same K-major pass as the gradient
+    (bs_genotype_transpose_packed).  It costs a second copy of the packed block, taken here
+    (later in-place changes to X are not seen), so it is made only when the device keeps
+    4 GiB free beside it; otherwise X beta stays on the CUDA-core ring kernel.
+    """
+    if not (_U2_XT and getattr(x, "packed", False) and sdt == np.dtype(np.float32)):
+        return None
+    torch = _torch()
+    m, n_loc = x.shape[0], x.local.shape[1]
+    if m == 0 or n_loc == 0 or x.comm.device.type != "cuda":
+        return None
+    ldt = _lib.query("bs_genotype_packed_bytes", n_loc)
+    free, _ = torch.cuda.mem_get_info(x.comm.device)
+    if ldt * m + (4 << 30) > free:
+        return None
+    xt = torch.empty(ldt * m, dtype=torch.uint8, device=x.comm.device)
+    _lib.call("bs_genotype_transpose_packed", _lib.ptr(_flat_local(x)), m, n_loc, _lib.ptr(xt), _lib.stream_ptr())
+    return xt
 
 
 _EXP_CLAMP = {np.dtype(np.float64): 700.0, np.dtype(np.float32): 85.0}
@@ -703,9 +732,11 @@ def _xbeta(s, beta_local):
     st = _lib.stream_ptr()
     s._dev.pop("xb_beta", None)  # xb no longer holds a fused pass's partial
     local_reduce(beta_local, ReduceOp.SUM, _lib.BS_T_ABS, out=xb[m:m + 1])
-    wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", _lib.xcode(x), m, n_loc))
-    _lib.call("bs_cox_xbeta", _lib.ptr(_flat_local(x)), _lib.xcode(x), _lib.ptr(beta_local),
-              _lib.dtype_code(beta_local.dtype), m, n_loc, _lib.ptr(xb), wp, wn, st)
+    xt = s._dev.get("xt")
+    xptr, xcode = (_lib.ptr(xt), _lib.BS_U2T) if xt is not None else (_lib.ptr(_flat_local(x)), _lib.xcode(x))
+    wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", xcode, m, n_loc))
+    _lib.call("bs_cox_xbeta", xptr, xcode, _lib.ptr(beta_local), _lib.dtype_code(beta_local.dtype), m, n_loc,
+              _lib.ptr(xb), wp, wn, st)
     if comm.size > 1:
         comm.allreduce(xb, ReduceOp.SUM)
 

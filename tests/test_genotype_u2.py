@@ -227,3 +227,93 @@ def test_packed_genotypes_write_as_int8_dsta(tmp_path):
 
     for got in bs.run_inproc(3, fn):
         np.testing.assert_array_equal(got, orc.genotype_fill(m, n, 9))
+
+
+def _transpose_dev(XP, m, n):
+    ldt = bs.packed_bytes_per_column(n)
+    Q = torch.full((ldt * m,), 0xAA, dtype=torch.uint8, device=XP.device)  # pad bytes must come out zero
+    _lib.call("bs_genotype_transpose_packed", _lib.ptr(XP), m, n, _lib.ptr(Q), _lib.stream_ptr())
+    return Q
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(1, 3), (15, 4), (65, 9), (130, 129), (1000, 33), (8193, 5), (300, 1000)])
+def test_transpose_packed_matches_oracle(m, n):
+    """bs_genotype_transpose_packed: the packed block of X^T, byte for byte (pad bits zero)."""
+    x = np.random.Generator(np.random.Philox(5 * m + n)).integers(0, 3, size=(m, n)).astype(np.int8)
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to("cuda:0")
+    got = _transpose_dev(XP, m, n).cpu().numpy()
+    np.testing.assert_array_equal(got, orc.pack_genotypes_u2(np.ascontiguousarray(x.T)).ravel(order="F"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(100, 7), (4096, 65), (20000, 300), (9000, 1), (700, 5000)])
+def test_packed_transpose_xbeta_tensor_cores(m, n):
+    """X beta from the packed transpose (BS_U2T) on the integer tensor cores: float32 accuracy
+    against a float64 X beta, and the same result as the packed ring kernel within that."""
+    gen = np.random.Generator(np.random.Philox(7 * m + n))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    beta = gen.standard_normal(n).astype(np.float32)
+    beta[::3] *= np.float32(1e-4)
+    dev = torch.device("cuda:0")
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    Q = _transpose_dev(XP, m, n)
+    b = torch.from_numpy(beta).to(dev)
+    v = torch.zeros(m, dtype=torch.float64, device=dev)
+    bs.gemm_path_counts(reset=True)
+    ws = torch.zeros(max(_lib.query("bs_cox_xbeta_workspace", _lib.BS_U2T, m, n), 256), dtype=torch.uint8, device=dev)
+    xb = torch.zeros(m + 1, dtype=torch.float64, device=dev)
+    _lib.call("bs_cox_xbeta", _lib.ptr(Q), _lib.BS_U2T, _lib.ptr(b), _lib.BS_F32, m, n, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    assert bs.gemm_path_counts()["cox_packed_tensor"] == 1
+    xbt = xb[:m].cpu().numpy()
+    xbp, _ = _xbeta_grad(XP, _lib.BS_U2, b, v, torch.float32)
+    bh = beta.astype(np.float64)
+    want = x.astype(np.float64) @ bh
+    sc = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
+    assert np.max(np.abs(xbt - want) / sc) < 2e-6  # beta rounded to 27 bits of its 2048-column group max
+    assert np.max(np.abs(xbp - xbt) / sc) < 2e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e25])
+def test_packed_transpose_xbeta_any_beta_scale(scale):
+    """The tensor-core X beta scales each 2048-column group of beta by a power of two in float64."""
+    m, n = 9000, 300
+    gen = np.random.Generator(np.random.Philox(19))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    beta = (gen.standard_normal(n) * scale).astype(np.float32)
+    beta[::5] *= np.float32(1e-5)
+    beta[3::11] = 0.0
+    dev = torch.device("cuda:0")
+    Q = _transpose_dev(torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev), m, n)
+    b = torch.from_numpy(beta).to(dev)
+    ws = torch.zeros(max(_lib.query("bs_cox_xbeta_workspace", _lib.BS_U2T, m, n), 256), dtype=torch.uint8, device=dev)
+    xb = torch.zeros(m, dtype=torch.float64, device=dev)
+    _lib.call("bs_cox_xbeta", _lib.ptr(Q), _lib.BS_U2T, _lib.ptr(b), _lib.BS_F32, m, n, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    got = xb.cpu().numpy()
+    bh = beta.astype(np.float64)
+    want = x.astype(np.float64) @ bh
+    sc = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want) / sc) < 2e-6
+
+
+@pytest.mark.gpu
+def test_cox_fit_packed_uses_transposed_xbeta():
+    """cox_init keeps a packed transpose for float32 packed X, and cox_fit's X beta then takes
+    the tensor-core pass (two packed tensor-core passes per iteration)."""
+    m, n, seed, iters = 3000, 257, 11, 6
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(2)).random(m) < 0.6).astype(np.float64)
+
+    def fn(comm):
+        a = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        st = bs.cox_init(a, y, delta, 1e-6, ties="breslow", dtype=np.float32)
+        assert st._dev.get("xt") is not None
+        bs.gemm_path_counts(reset=True)
+        bs.cox_fit(st, iters)
+        return bs.gemm_path_counts()["cox_packed_tensor"]
+
+    assert bs.run_inproc(1, fn)[0] >= 2 * iters
