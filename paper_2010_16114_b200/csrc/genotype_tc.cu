@@ -58,6 +58,51 @@ __host__ __device__ constexpr uint32_t idesc_u8s8(int N) {
   return (2u << 4) | (0u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
+// One k-block (16 k steps of 32 rows) from the whole warp: one elected lane issues
+// D (+)= A(TMEM) x B(smem), u8 x s8 -> s32, M = 128, N = NB, K = 32 per step.  A advances 8
+// TMEM columns per step (immediate offsets), B two 128-byte K chunks (+16 in the low word
+// of the descriptor; the 14-bit address field never carries into the high word here).
+__device__ __forceinline__ void mma_kblock16(uint32_t d, uint32_t blo, uint32_t bhi, uint32_t a, uint32_t first) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 lo;\n\t.reg .b64 b;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %4, 0;\n\t"
+      "mov.b64 b, {%1, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], b, %5, q;\n\t"
+      "add.u32 lo, %1, 16;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+8], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 32;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+16], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 48;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+24], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 64;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+32], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 80;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+40], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 96;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+48], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 112;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+56], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 128;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+64], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 144;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+72], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 160;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+80], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 176;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+88], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 192;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+96], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 208;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+104], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 224;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+112], b, %5, 1;\n\t"
+      "add.u32 lo, %1, 240;\n\tmov.b64 b, {lo, %2};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+120], b, %5, 1;\n\t"
+      "}" ::"r"(d), "r"(blo), "r"(bhi), "r"(a), "r"(first), "n"(idesc_u8s8(NB))
+      : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
@@ -199,51 +244,47 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    int cs = 0, bs = 0;
-    uint32_t cph = 0, bph = 0, gi = 0;
-    constexpr uint32_t id = idesc_u8s8(NB);
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      for (int kb = 0; kb < nkb; ++kb) {
+    // The k-blocks of this CTA run as one sequence g = 0, 1, ... (tile-major); g's A stage is
+    // g % CS and its B stage g % BS.  Unrolling six k-blocks at a time makes both stages
+    // compile-time constants: every MMA operand is then a loop-invariant base plus an
+    // immediate, so the single issuing warp spends a few instructions per MMA.
+    static_assert(BS == 6 && CS == 3, "the unrolled issue loop assumes 6 B stages and 3 A stages");
+    static_assert(TMEM_COLS == 512, "a whole-TMEM allocation starts at address 0");
+    if (tmem != 0u) __trap();
+    const uint32_t my_tiles = uint32_t((tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x));
+    const uint32_t total = my_tiles * uint32_t(nkb);
+    const uint64_t b_desc0 = sdesc(smem_u32(b_base), 128, B_SBO, 0);
+    const uint32_t blo0 = uint32_t(b_desc0), bhi = uint32_t(b_desc0 >> 32);
+    int kb = 0;
+    uint32_t gi = 0;
+    for (uint32_t g0 = 0; g0 < total; g0 += 6) {
+      const uint32_t bph = (g0 / 6) & 1u;
+#pragma unroll
+      for (int u = 0; u < 6; ++u) {
+        if (g0 + uint32_t(u) >= total) break;
+        const int cs = u % 3;
+        const uint32_t cph = uint32_t(u / 3);  // (g / CS) & 1 with g0 a multiple of 6
         const int in_group = kb % G;
-        const uint32_t buf = gi & 1;
+        const uint32_t buf = gi & 1u;
         if (in_group == 0) {
-          mbar_wait(acc_empty(buf), ((gi >> 1) & 1) ^ 1);
+          mbar_wait(acc_empty(buf), ((gi >> 1) & 1u) ^ 1u);
           tc_fence_after();
         }
         mbar_wait(a_full(cs), cph);
-        mbar_wait(b_full(bs), bph);
+        mbar_wait(b_full(u), bph);
         tc_fence_after();
         const bool last = (in_group == G - 1) || (kb == nkb - 1);
-        const uint32_t d = __shfl_sync(0xffffffffu, tmem + buf * ACC, 0);
-        const uint32_t a = __shfl_sync(0xffffffffu, tmem + A_COL0 + cs * A_COLS, 0);
-        const uint32_t bb = __shfl_sync(0xffffffffu, smem_u32(b_base + bs * B_BYTES), 0);
-        const uint64_t bdesc = sdesc(bb, 128, B_SBO, 0);
-        const uint32_t first = in_group == 0 ? 1u : 0u;
-        // k step s of 32 rows: A advances 8 TMEM columns, B two 128-byte K chunks (+16 in the descriptor)
-#pragma unroll
-        for (int s4 = 0; s4 < KSTEPS; s4 += 4) {
-          asm volatile(
-              "{\n\t.reg .pred p, acc;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
-              "elect.sync _|p, 0xffffffff;\n\t"
-              "setp.eq.b32 acc, %3, 0;\n\t"
-              "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
-              "add.s64 b1, %2, 16;\n\tadd.s64 b2, %2, 32;\n\tadd.s64 b3, %2, 48;\n\t"
-              "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %4, acc;\n\t"
-              "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %4, 1;\n\t"
-              "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %4, 1;\n\t"
-              "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %4, 1;\n\t}" ::"r"(d),
-              "r"(a + uint32_t(8 * s4)), "l"(bdesc + uint64_t(16 * s4)), "r"(s4 == 0 ? first : 0u), "n"(id)
-              : "memory");
-        }
-        __syncwarp();
+        // the CTA owns all 512 TMEM columns, so its TMEM base is address 0 (checked above):
+        // constant operand addresses keep the issue loop free of register-to-uniform moves
+        mma_kblock16(buf * ACC, blo0 + uint32_t((u * B_BYTES) >> 4), bhi, uint32_t(A_COL0 + cs * A_COLS),
+                     in_group == 0 ? 0u : 1u);
         mma_commit_elect(a_empty(cs));
-        mma_commit_elect(b_empty(bs));
+        mma_commit_elect(b_empty(u));
         if (last) {
           mma_commit_elect(acc_full(buf));
           ++gi;
         }
-        if (++cs == CS) { cs = 0; cph ^= 1; }
-        if (++bs == BS) { bs = 0; bph ^= 1; }
+        if (++kb == nkb) kb = 0;
       }
     }
   } else if (warp < 6) {
