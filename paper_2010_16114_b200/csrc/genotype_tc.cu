@@ -1,28 +1,41 @@
-// Tensor-core scn p for 2-bit packed genotypes (C5): grad_j = sum_i X_ij v_i
-// (distlinalg.py:355-358, solvers.py:446-447) as tcgen05 kind::i8 MMAs with exact int32 sums.
+// Tensor-core passes over 2-bit packed genotypes (C5), float32 arithmetic:
+//   scn p   grad_j = sum_i X_ij v_i   (distlinalg.py:355-358, solvers.py:446-447), and
+//   scn m   (X beta)_i = sum_j X_ij beta_j from the packed transpose (same pass, K = columns)
+// as tcgen05 kind::mxf4 MMAs (e2m1 x e2m1 -> f32, K = 64 per instruction, block scales 1).
 //
-// A = X^T (M = 128 columns j of the local block, K = rows i): a packed column is already
-// K-major, four genotypes per byte.  One PRMT replicates a packed byte b into all four lanes
-// of a word and one AND with 0xC0300C03 keeps field q in byte q, i.e. byte q = g_{4t+q} 4^q
-// (0..128, u8) — no shifts; the 4^q is undone on the B side.  Each converter thread unpacks
-// its column's 32 bytes of a 128-row k-block into 32 words and tcgen05.st's them into TMEM
-// (A operand, K-major, lane = column).
+// Why mxf4: below N = 128 every tcgen05 MMA costs a fixed ~64 cycles (scripts/ts_rate.cu,
+// profiles/r02_tcgen05_i8_rate.txt), so the genotypes one instruction consumes set the speed:
+// kind::i8 (K = 32 bytes) capped the previous version at 16 packed bytes per cycle per SM
+// (4.8 TB/s); e2m1 takes 64 per instruction, twice that, above the HBM rate.
 //
-// B = the v digits (K = i, N = 16): v is scaled per group of 2048 rows by 2^t so |v| < 2^27,
-// rounded to an integer, and split into four balanced signed 7-bit digits
-// (V = d0 2^21 + d1 2^14 + d2 2^7 + d3, d in [-64, 64]); row n = 4 d + q of the image holds
-// digit d of v_i when i % 4 == q and 0 otherwise, so
-//   D[j][4d + q] = 4^q sum_{i % 4 = q} X_ij d_d(v_i)
-// and the epilogue forms sum_d 2^(7(3 - d)) sum_q 4^-q D[j][4d + q] 2^-t in float64.
-// Products and sums are exact integers; the only rounding is v to 27 bits of its group
-// maximum (symmetric) — tighter than the float32 arithmetic of the CUDA-core kernels.
+// A = X^T (M = 128 columns j, K = rows i, K-major in shared memory): genotype g in {0, 1, 2}
+// is exactly the e2m1 code g (0, 0.5, 1.0).  A packed word w holds 16 genotypes at bits 2r;
+// w & 0x33333333 leaves the 8 even-row genotypes as nibbles, (w >> 2) & 0x33333333 the 8
+// odd-row ones, so each converter thread turns 16 genotypes into 8 bytes of A with three
+// integer instructions.  K order inside every 16-row group is therefore
+//   position s < 8: row 2s,   position s >= 8: row 2(s - 8) + 1,
+// and the B image uses the same order.
 //
-// CTA (one per SM, persistent over 128-column tiles; each tile runs the whole m):
-//   warp 0      TMA: packed tile (32 B x 128 columns = 128 rows x 128 columns) per k-block
-//   warp 14     bulk copy of the v-digit image (16 x 128 B) per k-block
-//   warps 6-13  two converter sets (alternate k-blocks): unpack -> TMEM
-//   warp 1      MMA issuer: 4 MMAs (M = 128, N = 16, K = 32) per k-block
-//   warps 2-5   epilogue: every group drains D (16 int32 per column) into a float64 sum
+// B = the v digits (N = 16): v is scaled per group of 2048 rows by 2^t so |v| < 2^46,
+// rounded to an integer V, and split into 16 balanced base-8 digits in [-4, 3] (exact e2m1
+// values), digit n in row n of the image.  D[j][n] = sum_i (g_ij / 2) d_n(v_i) is a sum of
+// multiples of 1/2 below 2^14 per 2048-row group, exact in the f32 accumulator; the epilogue
+// forms 2 sum_n 8^n D[j][n] 2^-t in float64.  The only rounding is v to 46 bits of its group
+// maximum.
+//
+// Shared memory carries, per k-block: the packed tile (TMA write, converter read, 16 KB
+// each way), the e2m1 A operand (converter write, tensor-core read, 32 KB each way) and the
+// digit image (4 KB): ~100 KB, which at 128 B per cycle is the pass's bound (~0.75 of HBM;
+// loading X straight into converter registers instead was slower, 17.8 ms at C5, for lack
+// of loads in flight).  The precision gain over kind::i8 (v to 46 bits instead of 27) is the
+// main reason for this form.
+//
+// CTA (one per SM, persistent over 128-column tiles; each tile runs the whole K):
+//   warp 0      TMA: packed tile (128 B x 128 columns = 512 rows x 128 columns) per k-block
+//   warp 14     bulk copy of the v-digit image (16 rows x 256 B) per k-block
+//   warps 6-13  two converter sets (alternate k-blocks): packed -> e2m1, into shared memory
+//   warp 1      MMA issuer: 8 MMAs (M = 128, N = 16, K = 64) per k-block
+//   warps 2-5   epilogue: every group drains D (16 f32 per column) into a float64 sum
 #include "tc_common.cuh"
 
 #include <algorithm>
@@ -37,69 +50,47 @@ void note_gemm_path(int path);
 namespace {
 
 constexpr int BM = 128;            // columns j per tile (MMA M)
-constexpr int BKR = 512;           // rows i per k-block (MMA K, 16 x 32)
+constexpr int BKR = 512;           // rows i per k-block
 constexpr int BKB = BKR / 4;       // packed bytes per column per k-block (128)
-constexpr int KSTEPS = BKR / 32;
+constexpr int KSTEPS = BKR / 64;   // MMAs per k-block (K = 64)
+static_assert(KSTEPS == 8, "mma_kblock8 issues eight K = 64 steps");
 constexpr int G = 4;               // k-blocks per scale group (2048 rows)
 constexpr int GROWS = G * BKR;
-constexpr int NB = 16;             // B rows: 4 digits x 4 phases
-constexpr int B_BYTES = NB * BKR;  // 8 KB per k-block
-constexpr int B_SBO = 8 * BKR;     // 8-row-group stride of the B image: BKR/16 chunks x 128 B
-constexpr int X_BYTES = BM * BKB;  // 16 KB per k-block
+constexpr int NB = 16;             // B rows: 16 base-8 digits
+constexpr int ROWB = BKR / 2;      // e2m1 bytes per operand row per k-block (256)
+constexpr int SBO = (ROWB / 16) * 128;  // 8-row-group stride: 16 K chunks x (8 rows x 16 B)
+constexpr int A_BYTES = BM * ROWB;  // 32 KB per k-block
+constexpr int B_BYTES = NB * ROWB;  // 4 KB per k-block
+constexpr int X_BYTES = BM * BKB;   // 16 KB per k-block
 constexpr int THREADS = 480;
-constexpr int RS = 8, BS = 6, CS = 3;
-constexpr int ACC = NB;            // TMEM columns per accumulator buffer
-constexpr int A_COLS = BKR / 4;    // TMEM columns per A stage: BKR unpacked bytes (128)
-constexpr int A_COL0 = 2 * ACC;
+constexpr int RS = 6, BS = 6, CS = 2;
+constexpr int ACC = NB;             // TMEM columns per accumulator buffer
+constexpr uint32_t T_SFA = 64, T_SFB = 96;  // scale-factor columns (all 2^0)
 constexpr int TMEM_COLS = 512;
-constexpr int SMEM = RS * X_BYTES + BS * B_BYTES + 1024 + 512;
+constexpr int OFF_A = RS * X_BYTES, OFF_B = OFF_A + CS * A_BYTES;
+constexpr int SMEM = OFF_B + BS * B_BYTES + 1024 + 512;
+// kind::mxf4 block-scaled descriptor: A, B e2m1 (1), scales ue8m0, N = 16, M = 128
+constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
 
-__host__ __device__ constexpr uint32_t idesc_u8s8(int N) {
-  return (2u << 4) | (0u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(BM >> 4) << 24);
-}
-
-// One k-block (16 k steps of 32 rows) from the whole warp: one elected lane issues
-// D (+)= A(TMEM) x B(smem), u8 x s8 -> s32, M = 128, N = NB, K = 32 per step.  A advances 8
-// TMEM columns per step (immediate offsets), B two 128-byte K chunks (+16 in the low word
-// of the descriptor; the 14-bit address field never carries into the high word here).
-__device__ __forceinline__ void mma_kblock16(uint32_t d, uint32_t blo, uint32_t bhi, uint32_t a, uint32_t first) {
+// One k-block (8 k steps of 64 rows) from the whole warp: one elected lane issues
+// D (+)= A(smem) x B(smem) with unit block scales.  Both operands advance two 128-byte K
+// chunks per step (+16 in the low word of each descriptor; no carry into the high word).
+__device__ __forceinline__ void mma_kblock8(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                            uint32_t first) {
   asm volatile(
-      "{\n\t.reg .pred p, q;\n\t.reg .b32 lo;\n\t.reg .b64 b;\n\t"
+      "{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t.reg .b64 a, b;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
       "setp.ne.b32 q, %4, 0;\n\t"
-      "mov.b64 b, {%1, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3], b, %5, q;\n\t"
-      "add.u32 lo, %1, 16;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+8], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 32;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+16], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 48;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+24], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 64;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+32], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 80;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+40], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 96;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+48], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 112;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+56], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 128;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+64], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 144;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+72], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 160;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+80], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 176;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+88], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 192;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+96], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 208;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+104], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 224;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+112], b, %5, 1;\n\t"
-      "add.u32 lo, %1, 240;\n\tmov.b64 b, {lo, %2};\n\t"
-      "@p tcgen05.mma.cta_group::1.kind::i8 [%0], [%3+120], b, %5, 1;\n\t"
-      "}" ::"r"(d), "r"(blo), "r"(bhi), "r"(a), "r"(first), "n"(idesc_u8s8(NB))
+      "mov.b64 a, {%1, %5};\n\tmov.b64 b, {%2, %6};\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%7], [%8], q;\n\t"
+#define BS_F4_STEP(OFF)                                                                  \
+      "add.u32 t, %1, " #OFF ";\n\tmov.b64 a, {t, %5};\n\t"                            \
+      "add.u32 t, %2, " #OFF ";\n\tmov.b64 b, {t, %6};\n\t"                            \
+      "@p tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a, b, %3, [%7], [%8], 1;\n\t"
+      BS_F4_STEP(16) BS_F4_STEP(32) BS_F4_STEP(48) BS_F4_STEP(64) BS_F4_STEP(80) BS_F4_STEP(96) BS_F4_STEP(112)
+#undef BS_F4_STEP
+      "}" ::"r"(d),
+      "r"(alo), "r"(blo), "r"(IDESC), "r"(first), "r"(ahi), "r"(bhi), "r"(T_SFA), "r"(T_SFB)
       : "memory");
 }
 
@@ -110,10 +101,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// v digits: one CTA per 2048-row group, thread t owns rows [16 t, 16 t + 16) of the group
-// (one 16-byte K chunk of one k-block) and writes that chunk for all 16 image rows.
-// image row n, k-block kb: canonical K-major SWIZZLE_NONE, 8 rows x 16 B core matrices,
-// K-chunk stride 128 B, 8-row-group stride B_SBO.
+// v digits: one CTA per 2048-row group, thread t owns rows [16 t, 16 t + 16) of the group,
+// i.e. one 16-position K group of one k-block, and writes its 8 bytes of every image row.
+// Image of a k-block: canonical K-major SWIZZLE_NONE, 8 rows x 16 B core matrices, K-chunk
+// stride 128 B, 8-row-group stride SBO.
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, int64_t m,
@@ -134,46 +125,32 @@ __global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, i
   if (lane == 0) smax[warp] = mx;
   __syncthreads();
   mx = fmax(fmax(smax[0], smax[1]), fmax(smax[2], smax[3]));
-  // scale 2^s with mx 2^s in [2^26, 2^27); an all-zero group keeps s = 0
+  // scale 2^s with mx 2^s in [2^45, 2^46); an all-zero group keeps s = 0
   int ex = 0;
   frexp(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
-  const int s = mx > 0.0 ? 27 - ex : 0;
+  const int s = mx > 0.0 ? 46 - ex : 0;
   if (t == 0) gscale[blockIdx.x] = ldexp(1.0, -s);
-  uint8_t dg[4][16];
+  unsigned long long word[NB];
+#pragma unroll
+  for (int n = 0; n < NB; ++n) word[n] = 0ull;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    double y = ldexp(vv[e], s);              // exact
-    double r = y;
-    const double w[4] = {2097152.0, 16384.0, 128.0, 1.0};  // 2^21, 2^14, 2^7, 1
+    long long V = llrint(ldexp(vv[e], s));  // exact scaling, one rounding
+    const int pos = (e & 1) ? 8 + (e >> 1) : (e >> 1);  // K position of row e in its 16-group
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
-      const double q = d < 3 ? floor(r / w[d] + 0.5) : rint(r);  // last digit: round to nearest
-      r -= q * w[d];                          // exact
-      dg[d][e] = uint8_t(int8_t(q));
+    for (int n = 0; n < NB; ++n) {  // balanced base-8 digits in [-4, 3], least significant first
+      const int q = int(((V + 4) & 7)) - 4;
+      V = (V - q) >> 3;
+      const unsigned long long code = (0x5420ACDEu >> (4 * (q + 4))) & 0xFu;  // e2m1 of -4..3
+      word[n] |= code << (4 * pos);
     }
   }
-  // write: k-block kb = t / (BKR / 16), chunk c = t % (BKR / 16)
+  // write: k-block kb = t / (BKR / 16), 8-byte half h of 16-byte K chunk c
   const int64_t kb = (int64_t(blockIdx.x) * GROWS) / BKR + t / (BKR / 16);
-  const int c = t % (BKR / 16);
-  uint8_t* kimg = img + kb * B_BYTES;
+  const int tt = t % (BKR / 16);
+  uint8_t* kimg = img + kb * B_BYTES + (tt >> 1) * 128 + (tt & 1) * 8;
 #pragma unroll
-  for (int n = 0; n < NB; ++n) {
-    const int d = n >> 2, q = n & 3;
-    uint32_t wd[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      uint32_t x = 0;
-#pragma unroll
-      for (int e4 = 0; e4 < 4; ++e4) {
-        const int e = 4 * b + e4;  // row 16 t + e: phase e % 4
-        const uint32_t byte = (e % 4 == q) ? uint32_t(dg[d][e]) : 0u;
-        x |= byte << (8 * e4);
-      }
-      wd[b] = x;
-    }
-    *reinterpret_cast<uint4*>(kimg + (n >> 3) * B_SBO + c * 128 + (n & 7) * 16) =
-        make_uint4(wd[0], wd[1], wd[2], wd[3]);
-  }
+  for (int n = 0; n < NB; ++n) *reinterpret_cast<unsigned long long*>(kimg + (n >> 3) * SBO + (n & 7) * 16) = word[n];
 }
 
 // ---------------------------------------------------------------------------
@@ -186,7 +163,8 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* b_base = smem + RS * X_BYTES;
+  uint8_t* a_base = smem + OFF_A;
+  uint8_t* b_base = smem + OFF_B;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + BS * B_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * BS + 2 * CS + 4);
   auto raw_full = [&](int s) { return smem_u32(bars + s); };
@@ -219,6 +197,18 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp >= 2 && warp < 6) {  // unit block scales (ue8m0 127 = 2^0) in every lane of the SF columns
+    uint32_t ones[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) ones[c] = 0x7F7F7F7Fu;
+    const uint32_t la = uint32_t((warp & 3) * 32) << 16;
+    tmem_st16(tmem + la + T_SFA, ones);
+    tmem_st16(tmem + la + T_SFB, ones);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0 || warp == 14) {
     // ---------------- producers: packed X tiles (warp 0), v-digit images (warp 14) ----------------
@@ -248,12 +238,14 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
     // g % CS and its B stage g % BS.  Unrolling six k-blocks at a time makes both stages
     // compile-time constants: every MMA operand is then a loop-invariant base plus an
     // immediate, so the single issuing warp spends a few instructions per MMA.
-    static_assert(BS == 6 && CS == 3, "the unrolled issue loop assumes 6 B stages and 3 A stages");
+    static_assert(BS == 6 && (CS == 2 || CS == 3), "the unrolled issue loop assumes 6 B stages, 2 or 3 A stages");
     static_assert(TMEM_COLS == 512, "a whole-TMEM allocation starts at address 0");
     if (tmem != 0u) __trap();
     const uint32_t my_tiles = uint32_t((tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x));
     const uint32_t total = my_tiles * uint32_t(nkb);
-    const uint64_t b_desc0 = sdesc(smem_u32(b_base), 128, B_SBO, 0);
+    const uint64_t a_desc0 = sdesc(smem_u32(a_base), 128, SBO, 0);
+    const uint64_t b_desc0 = sdesc(smem_u32(b_base), 128, SBO, 0);
+    const uint32_t alo0 = uint32_t(a_desc0), ahi = uint32_t(a_desc0 >> 32);
     const uint32_t blo0 = uint32_t(b_desc0), bhi = uint32_t(b_desc0 >> 32);
     int kb = 0;
     uint32_t gi = 0;
@@ -262,8 +254,8 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
 #pragma unroll
       for (int u = 0; u < 6; ++u) {
         if (g0 + uint32_t(u) >= total) break;
-        const int cs = u % 3;
-        const uint32_t cph = uint32_t(u / 3);  // (g / CS) & 1 with g0 a multiple of 6
+        const int cs = u % CS;
+        const uint32_t cph = (g0 / CS + uint32_t(u / CS)) & 1u;
         const int in_group = kb % G;
         const uint32_t buf = gi & 1u;
         if (in_group == 0) {
@@ -274,10 +266,8 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         mbar_wait(b_full(u), bph);
         tc_fence_after();
         const bool last = (in_group == G - 1) || (kb == nkb - 1);
-        // the CTA owns all 512 TMEM columns, so its TMEM base is address 0 (checked above):
-        // constant operand addresses keep the issue loop free of register-to-uniform moves
-        mma_kblock16(buf * ACC, blo0 + uint32_t((u * B_BYTES) >> 4), bhi, uint32_t(A_COL0 + cs * A_COLS),
-                     in_group == 0 ? 0u : 1u);
+        mma_kblock8(buf * ACC, alo0 + uint32_t((cs * A_BYTES) >> 4), ahi, blo0 + uint32_t((u * B_BYTES) >> 4), bhi,
+                    in_group == 0 ? 0u : 1u);
         mma_commit_elect(a_empty(cs));
         mma_commit_elect(b_empty(u));
         if (last) {
@@ -304,24 +294,19 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         tmem_ld16_u(tmem + lane_addr + buf * ACC, r);
         tc_fence_before();
         mbar_arrive(acc_empty(buf));
-        double s = 0.0;
+        double sd = 0.0;
 #pragma unroll
-        for (int dd = 0; dd < 4; ++dd) {
-          double sd = 0.0;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) sd = fma(double(int(r[4 * dd + qq])), ldexp(1.0, -2 * qq), sd);
-          s = fma(sd, ldexp(1.0, 7 * (3 - dd)), s);
-        }
-        acc = fma(s, __ldg(gscale + g), acc);
+        for (int n = NB - 1; n >= 0; --n) sd = fma(sd, 8.0, double(__uint_as_float(r[n])));  // sum_n 8^n D[n]
+        acc = fma(sd, 2.0 * __ldg(gscale + g), acc);  // genotype codes are g / 2
       }
       if (j < n_loc) out[j] = acc;
     }
   } else {
-    // ---------------- converters: packed bytes -> u8 genotypes (x 4^q) in TMEM ----------------
+    // ---------------- converters: packed bytes -> e2m1 nibbles in shared memory ----------------
     const int set = (warp - 6) >> 2;
     const int q = warp & 3;
     const int col = q * 32 + lane;  // row of A = column of the tile
-    const uint32_t lane_addr = uint32_t(q * 32) << 16;
+    const uint32_t dst0 = uint32_t((col >> 3) * SBO + (col & 7) * 16);
     uint32_t j0 = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       for (int t = int((uint32_t(set) - j0) & 1u); t < nkb; t += 2) {
@@ -329,26 +314,26 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         const int rst = int(jj % RS), cst = int(jj % CS);
         mbar_wait(raw_full(rst), (jj / RS) & 1);
         mbar_wait(a_empty(cst), ((jj / CS) & 1) ^ 1);
-        tc_fence_after();
         // the tile row (128 B) sits in SWIZZLE_128B: 16-byte chunk c of row r at chunk c ^ (r % 8),
         // so the 32 lanes' reads of one chunk spread over the banks
         const uint32_t src = smem_u32(smem + rst * X_BYTES) + uint32_t(col) * BKB;
         const uint32_t sw = uint32_t(col & 7);
+        const uint32_t dst = smem_u32(a_base + cst * A_BYTES) + dst0;
 #pragma unroll
-        for (int h = 0; h < BKB / 32; ++h) {  // 32 packed bytes -> 32 words -> one TMEM store
-          const uint4 p0 = ld_shared_v4(src + ((uint32_t(2 * h) ^ sw) << 4));
-          const uint4 p1 = ld_shared_v4(src + ((uint32_t(2 * h + 1) ^ sw) << 4));
-          const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-          uint32_t u[32];
+        for (int c = 0; c < BKB / 16; ++c) {  // 64 genotypes -> two 16-byte K chunks of e2m1
+          const uint4 p = ld_shared_v4(src + ((uint32_t(c) ^ sw) << 4));
+          const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+          uint32_t e[4], o[4];
 #pragma unroll
-          for (int w = 0; w < 8; ++w)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) u[4 * w + b] = __byte_perm(pw[w], 0u, 0x1111u * uint32_t(b)) & 0xC0300C03u;
-          tmem_st32(tmem + lane_addr + uint32_t(A_COL0 + cst * A_COLS + 32 * h), u);
+          for (int k = 0; k < 4; ++k) {
+            e[k] = w[k] & 0x33333333u;         // even rows 2s -> nibble s
+            o[k] = (w[k] >> 2) & 0x33333333u;  // odd rows 2s + 1 -> nibble s
+          }
+          st_shared_v4(dst + uint32_t(2 * c) * 128u, make_uint4(e[0], o[0], e[1], o[1]));
+          st_shared_v4(dst + uint32_t(2 * c + 1) * 128u, make_uint4(e[2], o[2], e[3], o[3]));
         }
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(raw_empty(rst));  // behind the TMEM store, which depends on every loaded word
+        fence_proxy_async_smem();  // the generic-proxy stores become visible to the tensor core
+        mbar_arrive(raw_empty(rst));  // behind the stores, which depend on every loaded word
         mbar_arrive(a_full(cst));
       }
       j0 += uint32_t(nkb);

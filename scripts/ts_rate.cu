@@ -50,7 +50,12 @@ __global__ void __launch_bounds__(128, 1) rate(int iters, long long* out) {
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        if (TS == 2)
+        if (TS == 4)
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], p;\n\t}" ::"r"(tmem),
+                       "l"(a), "l"(b), "n"((1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) | (8u << 24)),
+                       "r"(tmem + 384), "r"(tmem + 448));
+        else if (TS == 2)
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
                        "l"(a), "l"(b), "n"(id));
@@ -108,12 +113,10 @@ void run(const char* name) {
 }
 
 int main() {
-  run<1, 16, 1>("TS");
   run<2, 16, 1>("SSc");
-  run<3, 16, 1>("TSc");
-  run<2, 64, 1>("SSc");
-  run<2, 128, 1>("SSc");
-  run<2, 256, 1>("SSc");
-  run<3, 256, 1>("TSc");
+  run<4, 16, 1>("MXF4");
+  run<4, 64, 1>("MXF4");
+  run<4, 128, 1>("MXF4");
+  run<4, 256, 1>("MXF4");
   return 0;
 }

@@ -249,8 +249,9 @@ def test_transpose_packed_matches_oracle(m, n):
 @pytest.mark.gpu
 @pytest.mark.parametrize("m,n", [(100, 7), (4096, 65), (20000, 300), (9000, 1), (700, 5000)])
 def test_packed_transpose_xbeta_tensor_cores(m, n):
-    """X beta from the packed transpose (BS_U2T) on the integer tensor cores: float32 accuracy
-    against a float64 X beta, and the same result as the packed ring kernel within that."""
+    """X beta from the packed transpose (BS_U2T) on the tensor cores (kind::mxf4, exact sums of
+    46-bit beta digits): 1e-9 of sum |x beta| against a float64 X beta, and the packed
+    float32 ring kernel within its 2e-5."""
     gen = np.random.Generator(np.random.Philox(7 * m + n))
     x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
     beta = gen.standard_normal(n).astype(np.float32)
@@ -271,14 +272,15 @@ def test_packed_transpose_xbeta_tensor_cores(m, n):
     bh = beta.astype(np.float64)
     want = x.astype(np.float64) @ bh
     sc = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
-    assert np.max(np.abs(xbt - want) / sc) < 2e-6  # beta rounded to 27 bits of its 2048-column group max
+    assert np.max(np.abs(xbt - want) / sc) < 1e-9  # beta rounded to 46 bits of its 2048-column group max
     assert np.max(np.abs(xbp - xbt) / sc) < 2e-5
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("scale", [1e-38, 1e-20, 1.0, 1e25])
 def test_packed_transpose_xbeta_any_beta_scale(scale):
-    """The tensor-core X beta scales each 2048-column group of beta by a power of two in float64."""
+    """The tensor-core X beta scales each 2048-column group of beta by a power of two in float64,
+    so tiny and huge beta keep the 46-bit digits."""
     m, n = 9000, 300
     gen = np.random.Generator(np.random.Philox(19))
     x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
@@ -297,7 +299,7 @@ def test_packed_transpose_xbeta_any_beta_scale(scale):
     want = x.astype(np.float64) @ bh
     sc = np.abs(x).astype(np.float64) @ np.abs(bh) + 1e-300
     assert np.all(np.isfinite(got))
-    assert np.max(np.abs(got - want) / sc) < 2e-6
+    assert np.max(np.abs(got - want) / sc) < 1e-9
 
 
 @pytest.mark.gpu
@@ -317,3 +319,24 @@ def test_cox_fit_packed_uses_transposed_xbeta():
         return bs.gemm_path_counts()["cox_packed_tensor"]
 
     assert bs.run_inproc(1, fn)[0] >= 2 * iters
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [5000, 20000])
+def test_packed_tensor_core_grad_46_bits(m):
+    """The packed gradient on the tensor cores (kind::mxf4) rounds v only to 46 bits of its
+    2048-row group maximum: mixed magnitudes inside a group stay far below float32 error."""
+    n = 300
+    gen = np.random.Generator(np.random.Philox(23 + m))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    v = gen.standard_normal(m)
+    v[::3] *= 1e-6
+    dev = torch.device("cuda:0")
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    b = torch.zeros(n, dtype=torch.float32, device=dev)
+    bs.gemm_path_counts(reset=True)
+    _, gp = _xbeta_grad(XP, _lib.BS_U2, b, torch.from_numpy(v).to(dev), torch.float32)
+    assert bs.gemm_path_counts()["cox_packed_tensor"] == 1
+    want = x.astype(np.float64).T @ v
+    sc = np.abs(x).astype(np.float64).T @ np.abs(v)
+    assert np.max(np.abs(gp.astype(np.float64) - want) / sc) < 1e-7  # float32 output rounding dominates
