@@ -117,7 +117,7 @@ int bs_genotype_fill_packed(void* P, const double* maf, int64_t m, int64_t lo, i
 /* Q = the packed (n_loc x m) transpose of the packed (m x n_loc) block P: row i of X takes
  * bs_genotype_packed_bytes(n_loc) bytes at offset i * that, genotype j in bits 2(j%4)..+1 of
  * byte j/4.  Passed as X with xdtype BS_U2T, bs_cox_xbeta (dtype BS_F32) computes X beta on
- * the integer tensor cores from Q with the same pass as the packed gradient (an addition:
+ * the tensor cores (kind::mxf4) from Q with the same pass as the packed gradient (an addition:
  * the layout trades the memory of a second copy for a K-major operand). */
 int bs_genotype_transpose_packed(const void* P, int64_t m, int64_t n_loc, void* Q, void* stream);
 

@@ -230,7 +230,7 @@ def gemm_path_counts(reset=False):
     Keys: ``integer`` (tcgen05 kind::i8 digit slices), ``tf32`` (tcgen05 3xTF32),
     ``cuda_core`` (float32 CUDA cores), ``float64`` (DMMA / CUDA cores); ``tensor`` = the
     first two together; ``mds_tensor`` / ``mds_cuda_core``: MDS passes (bs_mds_pass);
-    ``cox_packed_tensor``: packed-genotype Cox gradient passes on the integer tensor cores.
+    ``cox_packed_tensor``: packed-genotype Cox passes (gradient, X beta) on the tensor cores (kind::mxf4).
     """
     import ctypes as C
 
@@ -695,7 +695,7 @@ _U2_XT = os.environ.get("BS_U2_XT", "1") != "0"  # A/B switch: X beta from a pac
 def _packed_transpose(x, sdt):
     """The packed transpose of a PackedGenotypes block for float32 arithmetic, or None.
 
-    X beta then runs on the integer tensor cores as the same K-major pass as the gradient
+    X beta then runs on the tensor cores (kind::mxf4) as the same K-major pass as the gradient
     (bs_genotype_transpose_packed).  It costs a second copy of the packed block, taken here
     (later in-place changes to X are not seen), so it is made only when the device keeps
     4 GiB free beside it; otherwise X beta stays on the CUDA-core ring kernel.
