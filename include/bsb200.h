@@ -172,7 +172,7 @@ int bs_nmf_prepare(const void* X, int dtype, int64_t m, int64_t n_loc,
  * out8 = {NMF GEMM on integer digit-slice tcgen05, NMF GEMM on 3xTF32 tcgen05,
  *         NMF GEMM on float32 CUDA cores, NMF GEMM in float64 (DMMA / CUDA cores),
  *         MDS pass on tcgen05 (mds_tc.cu), MDS pass on CUDA cores,
- *         packed-genotype Cox gradient on tcgen05 (genotype_tc.cu), 0}. */
+ *         packed-genotype Cox pass (gradient or X.beta) on tcgen05 kind::mxf4 (genotype_tc.cu), 0}. */
 int bs_gemm_path_counts(int64_t* out8, int reset);
 /* Adds delta8 to those counts (CUDA graph replays of captured solver iterations). */
 void bs_add_gemm_path_counts(const int64_t* delta8);
