@@ -732,7 +732,7 @@ def _xbeta(s, beta_local):
     st = _lib.stream_ptr()
     s._dev.pop("xb_beta", None)  # xb no longer holds a fused pass's partial
     local_reduce(beta_local, ReduceOp.SUM, _lib.BS_T_ABS, out=xb[m:m + 1])
-    xt = s._dev.get("xt")
+    xt = s._dev.get("xt") if beta_local.dtype == _torch().float32 else None  # BS_U2T takes float32 beta
     xptr, xcode = (_lib.ptr(xt), _lib.BS_U2T) if xt is not None else (_lib.ptr(_flat_local(x)), _lib.xcode(x))
     wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", xcode, m, n_loc))
     _lib.call("bs_cox_xbeta", xptr, xcode, _lib.ptr(beta_local), _lib.dtype_code(beta_local.dtype), m, n_loc,

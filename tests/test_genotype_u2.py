@@ -340,3 +340,24 @@ def test_packed_tensor_core_grad_46_bits(m):
     want = x.astype(np.float64).T @ v
     sc = np.abs(x).astype(np.float64).T @ np.abs(v)
     assert np.max(np.abs(gp.astype(np.float64) - want) / sc) < 1e-7  # float32 output rounding dominates
+
+
+@pytest.mark.gpu
+def test_partial_loglik_float64_beta_on_packed_float32_state():
+    """A float64 beta on a float32 packed state takes the packed ring kernel (the transpose
+    pass takes float32 beta only) and agrees with the float32 beta."""
+    m, n, seed = 2000, 65, 4
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(6)).random(m) < 0.5).astype(np.float64)
+
+    def fn(comm):
+        a = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        st = bs.cox_init(a, y, delta, 1e-6, sigma=1e-5, ties="breslow", dtype=np.float32)
+        bs.cox_fit(st, 3)
+        b64 = bs.empty((n,), comm, np.float64)
+        b64.local.copy_(st.beta.local.double())
+        return bs.cox_partial_loglik(st), bs.cox_partial_loglik(st, b64)
+
+    l32, l64 = bs.run_inproc(1, fn)[0]
+    assert np.isfinite(l64)
+    np.testing.assert_allclose(l64, l32, rtol=1e-5)
