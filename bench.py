@@ -19,8 +19,8 @@ Usage:
 Other workloads (--workload): nmf_mu_c1 (10k x 10k, r=20, float64), mds_c3
 (n=100,000 from 1000-dim points, q=20, float32), cox_c4 (100,000 x 200,000,
 float32, lambda=1e-8), cox_c5 (counter-based genotypes 400,000 x 500,000 packed
-2 bits per entry, Breslow ties, 4.5% events; fits one GPU), cox_c5_int8 (the same
-matrix stored int8; needs >= 2 GPUs).  Only the default is the driver's headline line.
+2 bits per entry, Breslow ties, 4.5% events; fits one GPU), cox_c5_f64 (the same, in
+the reference's float64 arithmetic), cox_c5_int8 (the same matrix stored int8; needs >= 2 GPUs).  Only the default is the driver's headline line.
 """
 
 from __future__ import annotations
@@ -53,6 +53,9 @@ WORKLOADS = {
     "cox_c5": dict(kind="cox", m=400_000, n=500_000, dtype="int8", storage="u2", lam=1e-8,
                    desc="l1-Cox genotypes 400000x500000, 2-bit packed (50 GB), float32 arithmetic "
                         "(BASELINE configs[4])"),
+    "cox_c5_f64": dict(kind="cox", m=400_000, n=500_000, dtype="int8", storage="u2", arith="float64", lam=1e-8,
+                       desc="l1-Cox genotypes 400000x500000, 2-bit packed (50 GB), float64 arithmetic "
+                            "(the reference's precision) (BASELINE configs[4])"),
     "cox_c5_int8": dict(kind="cox", m=400_000, n=500_000, dtype="int8", storage="int8", lam=1e-8,
                         desc="l1-Cox genotypes 400000x500000 stored int8 (200 GB: >= 2 GPUs), float32 "
                              "arithmetic (BASELINE configs[4])"),
@@ -246,7 +249,7 @@ def _setup(comm, wl):
             # X_ij ~ Bin(2, MAF_j), MAF_j ~ U(0.05, 0.5), counter-based
             x = bs.PackedGenotypes(comm, (m, n)) if wl.get("storage") == "u2" else bs.empty((m, n), comm, np.int8)
             bs.genotype_fill(x, seed=2016, maf_range=(0.05, 0.5))
-            sdt = np.float32
+            sdt = np.dtype(wl.get("arith", "float32"))
         else:
             # X ~ N(0, 1) (--dist standard_normal) from the counter-based device
             # generator: the same matrix for any rank count
@@ -419,7 +422,7 @@ def _data_desc(wl):
 
 def _arith_dtype(wl):
     if wl.get("storage") == "u2":
-        return "u2->f32"
+        return "u2->f64" if wl.get("arith") == "float64" else "u2->f32"
     return {"float32": "f32", "float64": "f64", "int8": "int8->f32"}[wl["dtype"]]
 
 
