@@ -361,7 +361,7 @@ def _free(*objs):
     torch.cuda.empty_cache()
 
 
-EXTRAS = ("nmf_mu_c1", "mds_c3", "cox_c4", "cox_c5")
+EXTRAS = ("nmf_mu_c1", "mds_c3", "cox_c4", "cox_c5", "cox_c5_f64")
 
 
 def _run_b200(args, wl):

@@ -132,7 +132,7 @@ __global__ void sum_slabs_f64(const double* __restrict__ parts, int S, int64_t l
   }
 }
 
-// packed genotypes, float32 arithmetic: the integer tensor-core gradient pass (genotype_tc.cu);
+// packed genotypes (float32 or float64 arithmetic): the tensor-core gradient pass (genotype_tc.cu);
 // BS_U2_TC=0 restores the CUDA-core ring kernel (A/B only)
 static bool u2_tc() {
   static const bool on = [] {
@@ -149,8 +149,10 @@ int launch_xbeta_u2(const void* P, const void* beta, bool f64, int64_t m, int64_
                     int64_t cps, double* parts, int* splits_used, cudaStream_t st);
 int64_t u2_grad_tc_workspace(int64_t m);
 bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
-                       Workspace& ws, cudaStream_t st, int* rc);
+                       Workspace& ws, cudaStream_t st, int* rc, bool f64);
 bool launch_xbeta_u2t_tc(const void* Q, const float* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
+                         cudaStream_t st, int* rc);
+bool launch_xbeta_u2t_tc(const void* Q, const double* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
                          cudaStream_t st, int* rc);
 int launch_grad_u2(const void* P, bool f64, const double* v, int64_t m, int64_t n_loc, int groups, int segs,
                    int64_t cpg, double* parts, const int* flags, cudaStream_t st);
@@ -284,11 +286,14 @@ extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dty
   if (m < 0 || n_loc < 0) { set_error("bs_cox_xbeta: negative shape"); return BS_EINVAL; }
   if (m == 0) return BS_OK;
   if (n_loc == 0) return cudaMemsetAsync(out, 0, sizeof(double) * m, st) == cudaSuccess ? BS_OK : BS_ECUDA;
-  if (xdtype == BS_U2T) {  // packed transpose, float32: one integer tensor-core pass (genotype_tc.cu)
-    if (dtype != BS_F32) { set_error("bs_cox_xbeta: BS_U2T takes float32 beta"); return BS_EINVAL; }
+  if (xdtype == BS_U2T) {  // packed transpose: one tensor-core pass (genotype_tc.cu)
+    if (dtype != BS_F32 && dtype != BS_F64) { set_error("bs_cox_xbeta: BS_U2T takes float32 or float64 beta"); return BS_EINVAL; }
     Workspace ws(work, work_bytes);
     int rc = BS_OK;
-    if (!launch_xbeta_u2t_tc(X, static_cast<const float*>(beta), m, n_loc, out, ws, st, &rc)) {
+    const bool ok = dtype == BS_F32
+                        ? launch_xbeta_u2t_tc(X, static_cast<const float*>(beta), m, n_loc, out, ws, st, &rc)
+                        : launch_xbeta_u2t_tc(X, static_cast<const double*>(beta), m, n_loc, out, ws, st, &rc);
+    if (!ok) {
       set_error("bs_cox_xbeta: BS_U2T needs the tcgen05 path (sm_100a, 16-byte aligned X)");
       return BS_EINVAL;
     }
@@ -1021,8 +1026,8 @@ extern "C" int bs_cox_grad_step(const void* X, int xdtype, const double* dmpd, i
   } else {
     const bool vec_ok = (m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
     int tc_rc = BS_OK;
-    if (xdtype == BS_U2 && dtype == BS_F32 && u2_tc() &&
-        launch_grad_u2_tc(X, dmpd, m, n_loc, parts, flags, ws, st, &tc_rc)) {
+    if (xdtype == BS_U2 && (dtype == BS_F32 || dtype == BS_F64) && u2_tc() &&
+        launch_grad_u2_tc(X, dmpd, m, n_loc, parts, flags, ws, st, &tc_rc, dtype == BS_F64)) {
       // integer tensor-core pass (genotype_tc.cu): one slab
       if (tc_rc != BS_OK) return tc_rc;
       segs_used = 1;

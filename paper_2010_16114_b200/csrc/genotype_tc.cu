@@ -16,12 +16,14 @@
 //   position s < 8: row 2s,   position s >= 8: row 2(s - 8) + 1,
 // and the B image uses the same order.
 //
-// B = the v digits (N = 16): v is scaled per group of 2048 rows by 2^t so |v| < 2^46,
-// rounded to an integer V, and split into 16 balanced base-8 digits in [-4, 3] (exact e2m1
+// B = the v digits (N = NB): v is scaled per group of 2048 rows by 2^t so |v| < 2^(3 NB - 2),
+// rounded to an integer V, and split into NB balanced base-8 digits in [-4, 4] (exact e2m1
 // values), digit n in row n of the image.  D[j][n] = sum_i (g_ij / 2) d_n(v_i) is a sum of
 // multiples of 1/2 below 2^14 per 2048-row group, exact in the f32 accumulator; the epilogue
-// forms 2 sum_n 8^n D[j][n] 2^-t in float64.  The only rounding is v to 46 bits of its group
-// maximum.
+// forms 2 sum_n 8^n D[j][n] 2^-t in float64.  The only rounding is v to 3 NB - 2 bits of its
+// group maximum: NB = 16 (46 bits) for float32 arithmetic, NB = 32 (94 bits: float64 values
+// 2^41 below their group's largest still keep all 53 bits) for float64 arithmetic — the MMA
+// costs the same for any N <= 128.
 //
 // Shared memory carries, per k-block: the packed tile (TMA write, converter read, 16 KB
 // each way), the e2m1 A operand (converter write, tensor-core read, 32 KB each way) and the
@@ -56,27 +58,32 @@ constexpr int KSTEPS = BKR / 64;   // MMAs per k-block (K = 64)
 static_assert(KSTEPS == 8, "mma_kblock8 issues eight K = 64 steps");
 constexpr int G = 4;               // k-blocks per scale group (2048 rows)
 constexpr int GROWS = G * BKR;
-constexpr int NB = 16;             // B rows: 16 base-8 digits
 constexpr int ROWB = BKR / 2;      // e2m1 bytes per operand row per k-block (256)
 constexpr int SBO = (ROWB / 16) * 128;  // 8-row-group stride: 16 K chunks x (8 rows x 16 B)
 constexpr int A_BYTES = BM * ROWB;  // 32 KB per k-block
-constexpr int B_BYTES = NB * ROWB;  // 4 KB per k-block
+constexpr int NB_MAX = 32;          // B rows (base-8 digits): 16 (float32) or 32 (float64)
+template <int NB>
+constexpr int b_bytes() { return NB * ROWB; }  // 4 / 8 KB per k-block
 constexpr int X_BYTES = BM * BKB;   // 16 KB per k-block
 constexpr int THREADS = 480;
 constexpr int RS = 6, BS = 6, CS = 2;
-constexpr int ACC = NB;             // TMEM columns per accumulator buffer
+constexpr int ACC = 32;             // TMEM columns per accumulator buffer (>= NB)
 constexpr uint32_t T_SFA = 64, T_SFB = 96;  // scale-factor columns (all 2^0)
 constexpr int TMEM_COLS = 512;
 constexpr int OFF_A = RS * X_BYTES, OFF_B = OFF_A + CS * A_BYTES;
-constexpr int SMEM = OFF_B + BS * B_BYTES + 1024 + 512;
-// kind::mxf4 block-scaled descriptor: A, B e2m1 (1), scales ue8m0, N = 16, M = 128
-constexpr uint32_t IDESC = (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
+template <int NB>
+constexpr int smem_bytes() { return OFF_B + BS * b_bytes<NB>() + 1024 + 512; }
+// kind::mxf4 block-scaled descriptor: A, B e2m1 (1), scales ue8m0, N = NB, M = 128
+template <int NB>
+constexpr uint32_t idesc_f4() {
+  return (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (1u << 23) | (uint32_t(BM >> 4) << 24);
+}
 
 // One k-block (8 k steps of 64 rows) from the whole warp: one elected lane issues
 // D (+)= A(smem) x B(smem) with unit block scales.  Both operands advance two 128-byte K
 // chunks per step (+16 in the low word of each descriptor; no carry into the high word).
 __device__ __forceinline__ void mma_kblock8(uint32_t d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
-                                            uint32_t first) {
+                                            uint32_t idesc, uint32_t first) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t.reg .b64 a, b;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
@@ -90,7 +97,7 @@ __device__ __forceinline__ void mma_kblock8(uint32_t d, uint32_t alo, uint32_t a
       BS_F4_STEP(16) BS_F4_STEP(32) BS_F4_STEP(48) BS_F4_STEP(64) BS_F4_STEP(80) BS_F4_STEP(96) BS_F4_STEP(112)
 #undef BS_F4_STEP
       "}" ::"r"(d),
-      "r"(alo), "r"(blo), "r"(IDESC), "r"(first), "r"(ahi), "r"(bhi), "r"(T_SFA), "r"(T_SFB)
+      "r"(alo), "r"(blo), "r"(idesc), "r"(first), "r"(ahi), "r"(bhi), "r"(T_SFA), "r"(T_SFB)
       : "memory");
 }
 
@@ -106,7 +113,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // Image of a k-block: canonical K-major SWIZZLE_NONE, 8 rows x 16 B core matrices, K-chunk
 // stride 128 B, 8-row-group stride SBO.
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, int NB>
 __global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, int64_t m,
                                                       uint8_t* __restrict__ img, double* __restrict__ gscale,
                                                       const int* flags) {
@@ -116,39 +123,46 @@ __global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, i
   const int64_t i0 = int64_t(blockIdx.x) * GROWS + 16 * t;
   double vv[16];
   double mx = 0.0;
+  int nonfinite = 0;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     vv[e] = (i0 + e < m) ? double(v[i0 + e]) : 0.0;
+    nonfinite |= !isfinite(vv[e]);
     mx = fmax(mx, fabs(vv[e]));
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (lane == 0) smax[warp] = mx;
-  __syncthreads();
+  // a NaN / inf in the group makes its scale NaN, so the sums come out NaN as float
+  // arithmetic would give them (the digits are then zeros, not digits of a non-finite)
+  nonfinite = __syncthreads_or(nonfinite);
   mx = fmax(fmax(smax[0], smax[1]), fmax(smax[2], smax[3]));
-  // scale 2^s with mx 2^s in [2^45, 2^46); an all-zero group keeps s = 0
+  // scale 2^s with mx 2^s in [2^(3 NB - 3), 2^(3 NB - 2)); an all-zero group keeps s = 0
   int ex = 0;
   frexp(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
-  const int s = mx > 0.0 ? 46 - ex : 0;
-  if (t == 0) gscale[blockIdx.x] = ldexp(1.0, -s);
+  const int s = (mx > 0.0 && !nonfinite) ? 3 * NB - 2 - ex : 0;
+  if (t == 0) gscale[blockIdx.x] = nonfinite ? __longlong_as_double(0x7ff8000000000000ll) : ldexp(1.0, -s);
   unsigned long long word[NB];
 #pragma unroll
   for (int n = 0; n < NB; ++n) word[n] = 0ull;
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    long long V = llrint(ldexp(vv[e], s));  // exact scaling, one rounding
+    // r = rint(v 2^s) is an integer below 2^(3 NB - 2) in magnitude (exact in float64: above
+    // 2^53 the scaled value is already integral); balanced base-8 digits from the top, each
+    // step exact: q = floor(r / 8^k + 1/2) in [-4, 4], r -= q 8^k
+    double r = nonfinite ? 0.0 : rint(ldexp(vv[e], s));
     const int pos = (e & 1) ? 8 + (e >> 1) : (e >> 1);  // K position of row e in its 16-group
 #pragma unroll
-    for (int n = 0; n < NB; ++n) {  // balanced base-8 digits in [-4, 3], least significant first
-      const int q = int(((V + 4) & 7)) - 4;
-      V = (V - q) >> 3;
-      const unsigned long long code = (0x5420ACDEu >> (4 * (q + 4))) & 0xFu;  // e2m1 of -4..3
+    for (int n = NB - 1; n >= 0; --n) {
+      const double q = floor(fma(r, ldexp(1.0, -3 * n), 0.5));
+      r = fma(-q, ldexp(1.0, 3 * n), r);
+      const unsigned long long code = (0x65420ACDEull >> (4 * (int(q) + 4))) & 0xFull;  // e2m1 of -4..4
       word[n] |= code << (4 * pos);
     }
   }
   // write: k-block kb = t / (BKR / 16), 8-byte half h of 16-byte K chunk c
   const int64_t kb = (int64_t(blockIdx.x) * GROWS) / BKR + t / (BKR / 16);
   const int tt = t % (BKR / 16);
-  uint8_t* kimg = img + kb * B_BYTES + (tt >> 1) * 128 + (tt & 1) * 8;
+  uint8_t* kimg = img + kb * b_bytes<NB>() + (tt >> 1) * 128 + (tt & 1) * 8;
 #pragma unroll
   for (int n = 0; n < NB; ++n) *reinterpret_cast<unsigned long long*>(kimg + (n >> 3) * SBO + (n & 7) * 16) = word[n];
 }
@@ -156,6 +170,7 @@ __global__ void __launch_bounds__(128) vdigits_kernel(const T* __restrict__ v, i
 // ---------------------------------------------------------------------------
 // the pass
 // ---------------------------------------------------------------------------
+template <int NB>
 __global__ void __launch_bounds__(THREADS, 1)
 gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ bimg,
               const double* __restrict__ gscale, int64_t m, int64_t n_loc, int tiles, double* __restrict__ out,
@@ -165,6 +180,7 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* a_base = smem + OFF_A;
   uint8_t* b_base = smem + OFF_B;
+  constexpr int B_BYTES = b_bytes<NB>();
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + BS * B_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * BS + 2 * CS + 4);
   auto raw_full = [&](int s) { return smem_u32(bars + s); };
@@ -267,7 +283,7 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         tc_fence_after();
         const bool last = (in_group == G - 1) || (kb == nkb - 1);
         mma_kblock8(buf * ACC, alo0 + uint32_t((cs * A_BYTES) >> 4), ahi, blo0 + uint32_t((u * B_BYTES) >> 4), bhi,
-                    in_group == 0 ? 0u : 1u);
+                    idesc_f4<NB>(), in_group == 0 ? 0u : 1u);
         mma_commit_elect(a_empty(cs));
         mma_commit_elect(b_empty(u));
         if (last) {
@@ -290,8 +306,14 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
         const uint32_t buf = gi & 1;
         mbar_wait(acc_full(buf), (gi >> 1) & 1);
         tc_fence_after();
-        uint32_t r[16];
-        tmem_ld16_u(tmem + lane_addr + buf * ACC, r);
+        uint32_t r[NB];
+#pragma unroll
+        for (int c = 0; c < NB; c += 8)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(r[c]), "=r"(r[c + 1]), "=r"(r[c + 2]), "=r"(r[c + 3]), "=r"(r[c + 4]), "=r"(r[c + 5]),
+                         "=r"(r[c + 6]), "=r"(r[c + 7])
+                       : "r"(tmem + lane_addr + buf * ACC + uint32_t(c)));
+        tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(acc_empty(buf));
         double sd = 0.0;
@@ -420,20 +442,20 @@ namespace bs {
 
 int64_t u2_grad_tc_workspace(int64_t m) {
   const int64_t nkb = (m + BKR - 1) / BKR, ng = (nkb + G - 1) / G;
-  return ws_bytes<uint8_t>(ng * G * B_BYTES) + ws_bytes<double>(ng);
+  return ws_bytes<uint8_t>(ng * G * b_bytes<NB_MAX>()) + ws_bytes<double>(ng);
 }
 
 // One tensor-core pass: out[j] = sum_k P[k, j] v[k] for the packed (K x M) block P (ld =
-// ceil(K / 64) * 16 bytes per column), one slab.  Returns false when the path does not apply
-// (no tcgen05, misaligned P, or the tensor map is refused).
-template <typename T>
+// ceil(K / 64) * 16 bytes per column), one slab, with NB digits of v.  Returns false when the
+// path does not apply (no tcgen05, misaligned P, or the tensor map is refused).
+template <typename T, int NB>
 static bool u2_tc_pass(const void* P, const T* v, int64_t K, int64_t M, double* out, const int* flags, Workspace& ws,
                        cudaStream_t st, int* rc, const char* what) {
   *rc = BS_OK;
   if (!tc_enabled() || K <= 0 || M <= 0 || (reinterpret_cast<uintptr_t>(P) & 15)) return false;
   const int64_t ld = ((K + 63) / 64) * 16;
   const int64_t nkb = (K + BKR - 1) / BKR, ng = (nkb + G - 1) / G;
-  uint8_t* img = ws.take<uint8_t>(ng * G * B_BYTES);
+  uint8_t* img = ws.take<uint8_t>(ng * G * b_bytes<NB>());
   double* gscale = ws.take<double>(ng);
   if (!img || !gscale) {
     set_error("%s: workspace too small", what);
@@ -442,27 +464,33 @@ static bool u2_tc_pass(const void* P, const T* v, int64_t K, int64_t M, double* 
   }
   CUtensorMap tm;
   if (!make_map_u8(&tm, P, uint64_t(ld), uint64_t(M), BKB, BM)) return false;
-  vdigits_kernel<T><<<int(ng), 128, 0, st>>>(v, K, img, gscale, flags);
+  vdigits_kernel<T, NB><<<int(ng), 128, 0, st>>>(v, K, img, gscale, flags);
   const int tiles = int((M + BM - 1) / BM);
   const int grid = std::min(tiles, num_sms());
-  smem_attr(gradtc_kernel, SMEM);
-  gradtc_kernel<<<grid, THREADS, SMEM, st>>>(tm, img, gscale, K, M, tiles, out, flags);
+  smem_attr(gradtc_kernel<NB>, smem_bytes<NB>());
+  gradtc_kernel<NB><<<grid, THREADS, smem_bytes<NB>(), st>>>(tm, img, gscale, K, M, tiles, out, flags);
   *rc = check_launch(what, 2);
   note_gemm_path(6);
   return true;
 }
 
-// grad partials (one slab: out[j], j < n_loc) of packed X against v on the tensor cores.
+// grad partials (one slab: out[j], j < n_loc) of packed X against v on the tensor cores, with
+// 16 digits of v for float32 arithmetic and 32 for float64.
 bool launch_grad_u2_tc(const void* P, const double* v, int64_t m, int64_t n_loc, double* out, const int* flags,
-                       Workspace& ws, cudaStream_t st, int* rc) {
-  return u2_tc_pass<double>(P, v, m, n_loc, out, flags, ws, st, rc, "u2 tensor-core grad");
+                       Workspace& ws, cudaStream_t st, int* rc, bool f64) {
+  return f64 ? u2_tc_pass<double, 32>(P, v, m, n_loc, out, flags, ws, st, rc, "u2 tensor-core grad")
+             : u2_tc_pass<double, 16>(P, v, m, n_loc, out, flags, ws, st, rc, "u2 tensor-core grad");
 }
 
 // X beta (out[i], i < m) from the packed transpose Q of the local block (bs_genotype_transpose_packed):
 // the same pass with K = n_loc and M = m.
 bool launch_xbeta_u2t_tc(const void* Q, const float* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
                          cudaStream_t st, int* rc) {
-  return u2_tc_pass<float>(Q, beta, n_loc, m, out, nullptr, ws, st, rc, "u2 tensor-core xbeta");
+  return u2_tc_pass<float, 16>(Q, beta, n_loc, m, out, nullptr, ws, st, rc, "u2 tensor-core xbeta");
+}
+bool launch_xbeta_u2t_tc(const void* Q, const double* beta, int64_t m, int64_t n_loc, double* out, Workspace& ws,
+                         cudaStream_t st, int* rc) {
+  return u2_tc_pass<double, 32>(Q, beta, n_loc, m, out, nullptr, ws, st, rc, "u2 tensor-core xbeta");
 }
 
 int launch_u2_transpose(const void* P, int64_t m, int64_t n, void* Q, cudaStream_t st) {

@@ -693,14 +693,14 @@ _U2_XT = os.environ.get("BS_U2_XT", "1") != "0"  # A/B switch: X beta from a pac
 
 
 def _packed_transpose(x, sdt):
-    """The packed transpose of a PackedGenotypes block for float32 arithmetic, or None.
+    """The packed transpose of a PackedGenotypes block (float32 / float64 arithmetic), or None.
 
     X beta then runs on the tensor cores (kind::mxf4) as the same K-major pass as the gradient
     (bs_genotype_transpose_packed).  It costs a second copy of the packed block, taken here
     (later in-place changes to X are not seen), so it is made only when the device keeps
     4 GiB free beside it; otherwise X beta stays on the CUDA-core ring kernel.
     """
-    if not (_U2_XT and getattr(x, "packed", False) and sdt == np.dtype(np.float32)):
+    if not (_U2_XT and getattr(x, "packed", False) and sdt in (np.dtype(np.float32), np.dtype(np.float64))):
         return None
     torch = _torch()
     m, n_loc = x.shape[0], x.local.shape[1]
@@ -732,7 +732,7 @@ def _xbeta(s, beta_local):
     st = _lib.stream_ptr()
     s._dev.pop("xb_beta", None)  # xb no longer holds a fused pass's partial
     local_reduce(beta_local, ReduceOp.SUM, _lib.BS_T_ABS, out=xb[m:m + 1])
-    xt = s._dev.get("xt") if beta_local.dtype == _torch().float32 else None  # BS_U2T takes float32 beta
+    xt = s._dev.get("xt") if beta_local.dtype == s.beta.local.dtype else None  # the state's arithmetic
     xptr, xcode = (_lib.ptr(xt), _lib.BS_U2T) if xt is not None else (_lib.ptr(_flat_local(x)), _lib.xcode(x))
     wp, wn = s._work.args("xbeta", _lib.query("bs_cox_xbeta_workspace", xcode, m, n_loc))
     _lib.call("bs_cox_xbeta", xptr, xcode, _lib.ptr(beta_local), _lib.dtype_code(beta_local.dtype), m, n_loc,

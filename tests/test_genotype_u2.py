@@ -134,7 +134,7 @@ def test_cox_fit_packed_matches_int8_and_oracle(p):
         bs.cox_fit(st, iters)
         return np.asarray(st.trace, dtype=np.float64), bs.gather_full(st.beta), st.sigma
 
-    int8_runs = bs.run_inproc(p, lambda c: fn(c, False))
+    int8_runs = bs.run_inproc(p, lambda c: fn(c, False))  # packed: both passes on the tensor cores
     packed_runs = bs.run_inproc(p, lambda c: fn(c, True))
     (t8, b8, s8), (tp, bp, sp) = int8_runs[0], packed_runs[0]
     np.testing.assert_allclose(sp, s8, rtol=1e-10)  # opnorm through the packed kernels
@@ -244,6 +244,28 @@ def test_transpose_packed_matches_oracle(m, n):
     XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to("cuda:0")
     got = _transpose_dev(XP, m, n).cpu().numpy()
     np.testing.assert_array_equal(got, orc.pack_genotypes_u2(np.ascontiguousarray(x.T)).ravel(order="F"))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(100, 7), (4096, 65), (20000, 300), (9000, 1), (700, 5000)])
+def test_packed_transpose_xbeta_float64(m, n):
+    """X beta from the packed transpose with float64 beta: 32 base-8 digits (94 bits of each
+    2048-column group's maximum), i.e. float64 accuracy even with a 1e9 spread inside a group."""
+    gen = np.random.Generator(np.random.Philox(13 * m + n))
+    x = gen.integers(0, 3, size=(m, n)).astype(np.int8)
+    beta = gen.standard_normal(n)
+    beta[::3] *= 1e-9
+    dev = torch.device("cuda:0")
+    Q = _transpose_dev(torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev), m, n)
+    b = torch.from_numpy(beta).to(dev)
+    ws = torch.zeros(max(_lib.query("bs_cox_xbeta_workspace", _lib.BS_U2T, m, n), 256), dtype=torch.uint8, device=dev)
+    xb = torch.zeros(m, dtype=torch.float64, device=dev)
+    _lib.call("bs_cox_xbeta", _lib.ptr(Q), _lib.BS_U2T, _lib.ptr(b), _lib.BS_F64, m, n, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    got = xb.cpu().numpy()
+    want = x.astype(np.float64) @ beta
+    sc = np.abs(x).astype(np.float64) @ np.abs(beta) + 1e-300
+    assert np.max(np.abs(got - want) / sc) < 1e-14
 
 
 @pytest.mark.gpu
@@ -361,3 +383,46 @@ def test_partial_loglik_float64_beta_on_packed_float32_state():
     l32, l64 = bs.run_inproc(1, fn)[0]
     assert np.isfinite(l64)
     np.testing.assert_allclose(l64, l32, rtol=1e-5)
+
+
+@pytest.mark.gpu
+def test_packed_tensor_core_passes_propagate_nan():
+    """A NaN in beta (X beta from the transpose) or in v (the gradient) gives NaN outputs, as
+    float arithmetic would, not finite digits of a non-finite value."""
+    m, n = 3000, 40
+    gen = np.random.Generator(np.random.Philox(31))
+    x = gen.integers(1, 3, size=(m, n)).astype(np.int8)  # no zero genotypes: every sum sees the NaN
+    dev = torch.device("cuda:0")
+    XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+    Q = _transpose_dev(XP, m, n)
+    beta = torch.ones(n, dtype=torch.float32, device=dev)
+    beta[7] = float("nan")
+    ws = torch.zeros(max(_lib.query("bs_cox_xbeta_workspace", _lib.BS_U2T, m, n), 256), dtype=torch.uint8, device=dev)
+    xb = torch.zeros(m, dtype=torch.float64, device=dev)
+    _lib.call("bs_cox_xbeta", _lib.ptr(Q), _lib.BS_U2T, _lib.ptr(beta), _lib.BS_F32, m, n, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    assert torch.isnan(xb).all()
+
+
+@pytest.mark.gpu
+def test_cox_fit_packed_float64_matches_int8():
+    """Packed genotypes in float64 arithmetic (both passes on the tensor cores with 32 digits)
+    against int8 storage (exact CUDA-core float64 kernels): float64-level agreement."""
+    m, n, seed, iters = 3000, 257, 11, 12
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(2)).random(m) < 0.6).astype(np.float64)
+
+    def fn(comm, packed):
+        a = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)) if packed else bs.empty((m, n), comm, np.int8), seed)
+        st = bs.cox_init(a, y, delta, 1e-6, sigma=1e-5, ties="breslow", dtype=np.float64)
+        if packed:
+            assert st._dev.get("xt") is not None
+        bs.gemm_path_counts(reset=True)
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.beta), bs.gemm_path_counts()["cox_packed_tensor"]
+
+    t8, b8, _ = bs.run_inproc(1, lambda c: fn(c, False))[0]
+    tp, bp, passes = bs.run_inproc(1, lambda c: fn(c, True))[0]
+    assert passes >= 2 * iters
+    np.testing.assert_allclose(tp, t8, rtol=1e-12)
+    np.testing.assert_allclose(bp, b8, rtol=1e-9, atol=1e-12 * np.abs(b8).max())
