@@ -663,7 +663,11 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
 }
 
-template <int RP, bool A_MN, int NS>
+// K16: the tile's products as mma.sync m16n8k16 (2048 FMAs per instruction, a warp's 32 rows
+// as two 16-row fragments) instead of m8n8k4 (256): 8x fewer DMMA instructions and fragment
+// loads per FMA.  The summation order inside an instruction differs, so K16 and the m8n8k4
+// kernels agree to rounding, not bitwise.
+template <int RP, bool A_MN, int NS, bool K16 = false>
 __global__ void __launch_bounds__(128)
 dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, int64_t M, int64_t ldx, int r,
                   int64_t K, int64_t k_per_split, double* __restrict__ out) {
@@ -711,7 +715,8 @@ dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, in
       }
     }
   };
-  double acc[4][NF][2];
+  static_assert(!K16 || BK % 16 == 0, "m16n8k16 steps need BK % 16 == 0");
+  double acc[4][NF][2];  // m8n8k4: fragment f = rows 8f.., m16n8k16: [2 mf + h] = rows 16 mf + 8 h ..
 #pragma unroll
   for (int f = 0; f < 4; ++f)
 #pragma unroll
@@ -731,6 +736,32 @@ dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, in
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* at = dm_smem + int(t % NS) * CA::STAGE;
     const double* bt = at + C::A_ELEMS;
+    if constexpr (K16) {
+      auto A_at = [&](int row, int k) { return A_MN ? at[k * SA + row] : at[row * SA + k]; };
+#pragma unroll
+      for (int ks = 0; ks < BK; ks += 16) {
+        double b[NF][4];
+#pragma unroll
+        for (int g = 0; g < NF; ++g)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) b[g][i] = bt[(ks + fk + 4 * i) * (RP + PB) + 8 * g + fr];
+#pragma unroll
+        for (int mf = 0; mf < 2; ++mf) {
+          const int row = 32 * warp + 16 * mf + fr;
+          double a[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[i] = A_at(row + 8 * (i & 1), ks + fk + 4 * (i >> 1));
+#pragma unroll
+          for (int g = 0; g < NF; ++g)
+            asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+                "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
+                : "+d"(acc[2 * mf][g][0]), "+d"(acc[2 * mf][g][1]), "+d"(acc[2 * mf + 1][g][0]),
+                  "+d"(acc[2 * mf + 1][g][1])
+                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                  "d"(b[g][0]), "d"(b[g][1]), "d"(b[g][2]), "d"(b[g][3]));
+        }
+      }
+    } else {
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
       double a[4], b[NF];
@@ -749,6 +780,7 @@ dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, in
               : "+d"(acc[f][g][0]), "+d"(acc[f][g][1])
               : "d"(a[f]), "d"(b[g]));
     }
+    }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   double* dst = out + int64_t(blockIdx.y) * M * r;
@@ -763,6 +795,14 @@ dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, in
       if (c + 1 < r) dst[row * r + c + 1] = acc[f][g][1];
     }
   }
+}
+
+static bool dmma_k16() {  // BS_DMMA_K16=0 keeps the m8n8k4 instruction (A/B switch)
+  static const bool on = [] {
+    const char* e = getenv("BS_DMMA_K16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 static int dmma_stages() {
@@ -787,6 +827,12 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
     const int rpa = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : 32;
 #define BS_DMMA_A(RPV, NSV)                                                                                    \
   {                                                                                                            \
+    if (dmma_k16()) {                                                                                          \
+      smem_attr(dmma_async_kernel<RPV, A_MN, NSV, true>, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM);                \
+      dmma_async_kernel<RPV, A_MN, NSV, true>                                                                  \
+          <<<grid, 128, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);             \
+      return true;                                                                                             \
+    }                                                                                                          \
     smem_attr(dmma_async_kernel<RPV, A_MN, NSV>, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM);                        \
     dmma_async_kernel<RPV, A_MN, NSV>                                                                          \
         <<<grid, 128, DmmaAsyncCfg<RPV, A_MN, NSV>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);               \
