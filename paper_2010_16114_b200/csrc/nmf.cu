@@ -500,11 +500,12 @@ cc_gemm_kernel(const T* __restrict__ X, const T* __restrict__ B, int64_t M, int6
 // IEEE float64 FMA, like the CUDA-core kernel (only the summation order differs).
 // ---------------------------------------------------------------------------
 
-template <int RP, bool A_MN>
+template <int RP, bool A_MN, int BKO = 0>
 struct DmmaCfg {
   // B row stride RP + PB must be 8 doubles mod 16 (64 B mod 128), or the 4 k rows a
-  // fragment load touches share banks: RP = 8 / 24 pad by 0, the others by 8.
-  static constexpr int BM = 128, BK = RP >= 64 ? 8 : 16, PB = RP % 16 == 8 ? 0 : 8;
+  // fragment load touches share banks: RP = 8 / 24 pad by 0, the others by 8.  BK: 8 for
+  // RP = 64 in the register-staged kernel (staging registers), else 16 (BKO overrides).
+  static constexpr int BM = 128, BK = BKO ? BKO : (RP >= 64 ? 8 : 16), PB = RP % 16 == 8 ? 0 : 8;
   // A tile: [k][m] (m contiguous) for scn b; [m][k] (k contiguous, +4 pad) for scn a
   static constexpr int A_ELEMS = A_MN ? BK * (BM + 8) : BM * (BK + 4);
   static constexpr int B_ELEMS = BK * (RP + PB);
@@ -649,7 +650,7 @@ dmma_gemm_kernel(const double* __restrict__ X, const double* __restrict__ B, int
 // cp.async src-size operand.
 template <int RP, bool A_MN, int NS>
 struct DmmaAsyncCfg {
-  using B = DmmaCfg<RP, A_MN>;
+  using B = DmmaCfg<RP, A_MN, 16>;  // no staging registers: BK = 16 for every RP
   static constexpr int STAGE = B::A_ELEMS + B::B_ELEMS;  // doubles per stage
   static constexpr int SMEM = NS * STAGE * 8;
 };
@@ -665,13 +666,14 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
 
 // K16: the tile's products as mma.sync m16n8k16 (2048 FMAs per instruction, a warp's 32 rows
 // as two 16-row fragments) instead of m8n8k4 (256): 8x fewer DMMA instructions and fragment
-// loads per FMA.  The summation order inside an instruction differs, so K16 and the m8n8k4
-// kernels agree to rounding, not bitwise.
+// loads per FMA.  The FP64 tensor core accumulates k in order either way: K16 results are
+// bitwise equal to the m8n8k4 kernels' (tests/test_nmf_gpu.py, register vs cp.async pipeline).
+// K16 also serves RP = 48 / 64 (one B fragment live at a time; 234 registers, 2 CTAs per SM).
 template <int RP, bool A_MN, int NS, bool K16 = false>
 __global__ void __launch_bounds__(128)
 dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, int64_t M, int64_t ldx, int r,
                   int64_t K, int64_t k_per_split, double* __restrict__ out) {
-  using C = DmmaCfg<RP, A_MN>;
+  using C = DmmaCfg<RP, A_MN, 16>;
   using CA = DmmaAsyncCfg<RP, A_MN, NS>;
   constexpr int BM = C::BM, BK = C::BK, V = 2, NF = RP / 8, PB = C::PB;
   constexpr int SA = A_MN ? BM + 8 : BK + 4;
@@ -740,25 +742,26 @@ dmma_async_kernel(const double* __restrict__ X, const double* __restrict__ B, in
       auto A_at = [&](int row, int k) { return A_MN ? at[k * SA + row] : at[row * SA + k]; };
 #pragma unroll
       for (int ks = 0; ks < BK; ks += 16) {
-        double b[NF][4];
-#pragma unroll
-        for (int g = 0; g < NF; ++g)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) b[g][i] = bt[(ks + fk + 4 * i) * (RP + PB) + 8 * g + fr];
+        double a[2][8];  // the warp's two 16-row fragments, loaded once per k step
 #pragma unroll
         for (int mf = 0; mf < 2; ++mf) {
           const int row = 32 * warp + 16 * mf + fr;
-          double a[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = A_at(row + 8 * (i & 1), ks + fk + 4 * (i >> 1));
+          for (int i = 0; i < 8; ++i) a[mf][i] = A_at(row + 8 * (i & 1), ks + fk + 4 * (i >> 1));
+        }
 #pragma unroll
-          for (int g = 0; g < NF; ++g)
+        for (int g = 0; g < NF; ++g) {  // one n fragment of B at a time (RP = 64: 8 of them)
+          double b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) b[i] = bt[(ks + fk + 4 * i) * (RP + PB) + 8 * g + fr];
+#pragma unroll
+          for (int mf = 0; mf < 2; ++mf)
             asm("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
                 "{%12,%13,%14,%15}, {%0,%1,%2,%3};"
                 : "+d"(acc[2 * mf][g][0]), "+d"(acc[2 * mf][g][1]), "+d"(acc[2 * mf + 1][g][0]),
                   "+d"(acc[2 * mf + 1][g][1])
-                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
-                  "d"(b[g][0]), "d"(b[g][1]), "d"(b[g][2]), "d"(b[g][3]));
+                : "d"(a[mf][0]), "d"(a[mf][1]), "d"(a[mf][2]), "d"(a[mf][3]), "d"(a[mf][4]), "d"(a[mf][5]),
+                  "d"(a[mf][6]), "d"(a[mf][7]), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
         }
       }
     } else {
@@ -823,6 +826,17 @@ static bool launch_dmma(const double* X, const double* B, int64_t M, int64_t ldx
   const int ns = dmma_stages();
   const bool async_ok = ns != 0 && (ldx % 2) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
                         (reinterpret_cast<uintptr_t>(B) & 7) == 0 && (A_MN || kps % 2 == 0);
+  if (async_ok && dmma_k16() && r > 32 && r <= 64) {  // RP 48 / 64: the m16n8k16 form only
+    const int rpw = r <= 48 ? 48 : 64;
+    if (rpw == 48) {
+      smem_attr(dmma_async_kernel<48, A_MN, 2, true>, DmmaAsyncCfg<48, A_MN, 2>::SMEM);
+      dmma_async_kernel<48, A_MN, 2, true><<<grid, 128, DmmaAsyncCfg<48, A_MN, 2>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
+    } else {
+      smem_attr(dmma_async_kernel<64, A_MN, 2, true>, DmmaAsyncCfg<64, A_MN, 2>::SMEM);
+      dmma_async_kernel<64, A_MN, 2, true><<<grid, 128, DmmaAsyncCfg<64, A_MN, 2>::SMEM, st>>>(X, B, M, ldx, r, K, kps, out);
+    }
+    return true;
+  }
   if (async_ok && r <= 32) {
     const int rpa = r <= 8 ? 8 : r <= 16 ? 16 : r <= 24 ? 24 : 32;
 #define BS_DMMA_A(RPV, NSV)                                                                                    \
