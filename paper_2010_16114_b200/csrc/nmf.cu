@@ -664,10 +664,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_by
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
 }
 
-// K16: the tile's products as mma.sync m16n8k16 (2048 FMAs per instruction, a warp's 32 rows
-// as two 16-row fragments) instead of m8n8k4 (256): 8x fewer DMMA instructions and fragment
-// loads per FMA.  The FP64 tensor core accumulates k in order either way: K16 results are
-// bitwise equal to the m8n8k4 kernels' (tests/test_nmf_gpu.py, register vs cp.async pipeline).
+// K16: the tile's products as mma.sync m16n8k16 (a warp's 32 rows as two 16-row fragments)
+// instead of m8n8k4.  ptxas lowers it to 16 DMMA.8x8x4 (profiles/r02_sass_tensor_excerpt.txt),
+// so the tensor work and the bits are those of the m8n8k4 kernels (tests/test_nmf_gpu.py,
+// register vs cp.async pipeline); what it saves is fragment loads and PTX-level overhead.
 // K16 also serves RP = 48 / 64 (one B fragment live at a time; 234 registers, 2 CTAs per SM).
 template <int RP, bool A_MN, int NS, bool K16 = false>
 __global__ void __launch_bounds__(128)
