@@ -162,6 +162,18 @@ bool launch_grad_i8_ring(const int8_t* X, const double* v, int64_t m, int64_t n_
                          const int* flags, cudaStream_t st);
 }  // namespace bs
 
+struct GrGrid {
+  int groups, segs;
+  int64_t cpg;
+};
+static GrGrid gr_grid(int64_t m, int64_t n_loc);
+
+template <typename T>
+__global__ void widen_f64_kernel(const T* __restrict__ x, int64_t n, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    y[i] = double(x[i]);
+}
+
 struct XbGrid {
   int64_t tiles;
   int splits;
@@ -183,7 +195,11 @@ static XbGrid xb_grid(int xdtype, int64_t m, int64_t n_loc, bool vec_ok) {
 }
 
 extern "C" int64_t bs_cox_xbeta_workspace(int xdtype, int64_t m, int64_t n_loc) {
-  if (xdtype == BS_U2T) return u2_grad_tc_workspace(n_loc);
+  if (xdtype == BS_U2T) {  // the tensor-core pass, or the CUDA-core fallback (beta widened + slabs)
+    const GrGrid g = gr_grid(n_loc, m);
+    return std::max<int64_t>(u2_grad_tc_workspace(n_loc),
+                             ws_bytes<double>(n_loc) + ws_bytes<double>(int64_t(g.segs) * std::max<int64_t>(m, 1)));
+  }
   XbGrid g = xb_grid(xdtype, m, n_loc, false);  // vec=1 gives the most tiles, splits <= that case
   XbGrid h = xb_grid(xdtype, m, n_loc, true);
   return ws_bytes<double>(int64_t(std::max(g.splits, h.splits)) * m);
@@ -293,11 +309,23 @@ extern "C" int bs_cox_xbeta(const void* X, int xdtype, const void* beta, int dty
     const bool ok = dtype == BS_F32
                         ? launch_xbeta_u2t_tc(X, static_cast<const float*>(beta), m, n_loc, out, ws, st, &rc)
                         : launch_xbeta_u2t_tc(X, static_cast<const double*>(beta), m, n_loc, out, ws, st, &rc);
-    if (!ok) {
-      set_error("bs_cox_xbeta: BS_U2T needs the tcgen05 path (sm_100a, 16-byte aligned X)");
-      return BS_EINVAL;
-    }
-    return rc;
+    if (ok) return rc;
+    // no tcgen05 (BS_DISABLE_TCGEN05, another part) or a misaligned block: the CUDA-core packed
+    // gradient kernel on the transpose computes the same sums, (X beta)_i = sum_j Q[j][i] beta_j
+    Workspace wf(work, work_bytes);
+    const GrGrid g = gr_grid(n_loc, m);
+    double* bd = wf.take<double>(n_loc);
+    double* slabs = wf.take<double>(int64_t(g.segs) * m);
+    if (!bd || !slabs) { set_error("bs_cox_xbeta: workspace too small"); return BS_EWORK; }
+    const int wg = int(std::min<int64_t>(ceil_div(n_loc, 256), 1024));
+    if (dtype == BS_F32) widen_f64_kernel<float><<<wg, 256, 0, st>>>(static_cast<const float*>(beta), n_loc, bd);
+    else widen_f64_kernel<double><<<wg, 256, 0, st>>>(static_cast<const double*>(beta), n_loc, bd);
+    launch_grad_u2(X, dtype == BS_F64, bd, n_loc, m, g.groups, g.segs, g.cpg, slabs, nullptr, st);
+    if (g.segs > 1)
+      sum_slabs_f64<<<int(std::min<int64_t>(ceil_div(m, 256), 2048)), 256, 0, st>>>(slabs, g.segs, m, out);
+    else
+      cudaMemcpyAsync(out, slabs, sizeof(double) * m, cudaMemcpyDeviceToDevice, st);
+    return check_launch("bs_cox_xbeta", 3);
   }
   const bool vec_ok = xdtype == BS_U2 ||
                       ((m % (16 / xsize(xdtype)) == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0));
@@ -874,11 +902,6 @@ prox_kernel(const double* __restrict__ parts, int segs, int64_t n_loc, T* __rest
     l1[0] = s;
   }
 }
-
-struct GrGrid {
-  int groups, segs;
-  int64_t cpg;
-};
 
 static GrGrid gr_grid(int64_t m, int64_t n_loc) {
   GrGrid g;

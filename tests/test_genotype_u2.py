@@ -426,3 +426,51 @@ def test_cox_fit_packed_float64_matches_int8():
     assert passes >= 2 * iters
     np.testing.assert_allclose(tp, t8, rtol=1e-12)
     np.testing.assert_allclose(bp, b8, rtol=1e-9, atol=1e-12 * np.abs(b8).max())
+
+
+_NO_TC_SCRIPT = r"""
+import sys, numpy as np, torch
+import paper_2010_16114_b200 as bs
+from paper_2010_16114_b200 import _lib
+from oracle import blockstat_oracle as orc
+m, n = 3000, 301
+x = np.random.Generator(np.random.Philox(41)).integers(0, 3, size=(m, n)).astype(np.int8)
+dev = torch.device("cuda:0")
+XP = torch.from_numpy(orc.pack_genotypes_u2(x).ravel(order="F")).to(dev)
+Q = torch.zeros(bs.packed_bytes_per_column(n) * m, dtype=torch.uint8, device=dev)
+_lib.call("bs_genotype_transpose_packed", _lib.ptr(XP), m, n, _lib.ptr(Q), _lib.stream_ptr())
+out = {}
+for dt, code in ((torch.float32, _lib.BS_F32), (torch.float64, _lib.BS_F64)):
+    beta = torch.from_numpy(np.random.Generator(np.random.Philox(42)).standard_normal(n)).to(dev, dt)
+    ws = torch.zeros(_lib.query("bs_cox_xbeta_workspace", _lib.BS_U2T, m, n), dtype=torch.uint8, device=dev)
+    xb = torch.zeros(m, dtype=torch.float64, device=dev)
+    bs.gemm_path_counts(reset=True)
+    _lib.call("bs_cox_xbeta", _lib.ptr(Q), _lib.BS_U2T, _lib.ptr(beta), code, m, n, _lib.ptr(xb), _lib.ptr(ws),
+              ws.numel(), _lib.stream_ptr())
+    out[str(dt)] = (xb.cpu().numpy(), beta.double().cpu().numpy(), bs.gemm_path_counts()["cox_packed_tensor"])
+np.savez(sys.argv[1], x=x, **{k + "_xb": v[0] for k, v in out.items()}, **{k + "_b": v[1] for k, v in out.items()},
+         **{k + "_tc": np.array(v[2]) for k, v in out.items()})
+"""
+
+
+@pytest.mark.gpu
+def test_transposed_xbeta_without_tcgen05(tmp_path):
+    """BS_DISABLE_TCGEN05=1: X beta from the packed transpose falls back to the CUDA-core packed
+    kernel (same sums), in float32 and float64."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    f = tmp_path / "notc.npz"
+    env = dict(os.environ, BS_DISABLE_TCGEN05="1", PYTHONPATH=str(root))
+    subprocess.run([sys.executable, "-c", _NO_TC_SCRIPT, str(f)], check=True, env=env, cwd=root, timeout=600)
+    r = np.load(f)
+    x = r["x"].astype(np.float64)
+    for dt, tol in (("torch.float32", 2e-6), ("torch.float64", 1e-13)):
+        b = r[dt + "_b"]
+        want = x @ b
+        sc = np.abs(x) @ np.abs(b)
+        assert int(r[dt + "_tc"]) == 0  # the tensor-core path did not run
+        assert np.max(np.abs(r[dt + "_xb"] - want) / sc) < tol
