@@ -27,6 +27,10 @@ Cases (SURVEY.md §8(c) parity protocol; VERDICT r01 "Next round" item 1):
   cox_breslow_f64    Cox, X 4,000 x 3,000 (uniform - 0.5), Breslow ties, default
                      power-iteration sigma, 100 iterations (solvers.py:337-450)
   cox_f32            same X in float32, explicit sigma, 100 iterations
+  cox_geno_f64       Cox on genotypes (the counter-based generator of this build, values
+                     0/1/2 handed to the reference as float64 — it has no int8 arithmetic),
+                     4,000 x 3,000, Breslow ties, default sigma, 100 iterations: pins the
+                     packed-genotype tensor-core passes in float64 against the reference
 """
 
 from __future__ import annotations
@@ -163,6 +167,19 @@ def main(only=None):
         out[f"{name}_meta"] = np.array([m, n, 2060, lam, -1.0 if sigma is None else sigma, 100], dtype=np.float64)
         out[f"{name}_trace"], out[f"{name}_beta"], out[f"{name}_sigma"] = tr, beta, np.array([sig])
         print(f"{name} {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)} sigma={sig:.6e}", flush=True)
+
+    if want("cox_geno_f64"):
+        sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+        from oracle import blockstat_oracle as orc
+
+        m, n, seed = 4000, 3000, 2070
+        xg = orc.genotype_fill(m, n, seed).astype(np.float64)
+        y = np.floor(np.arange(m, 0, -1) / 4.0)
+        delta = (np.random.Generator(np.random.Philox(seed + 7)).random(m) < 0.4).astype(np.float64)
+        tr, beta, sig = bs.run_inproc(2, cox_run, xg, y, delta, 2e-6, None, 100, np.float64)[0]
+        out["cox_geno_f64_meta"] = np.array([m, n, seed, 2e-6, -1.0, 100], dtype=np.float64)
+        out["cox_geno_f64_trace"], out["cox_geno_f64_beta"], out["cox_geno_f64_sigma"] = tr, beta, np.array([sig])
+        print(f"cox_geno_f64 {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)} sigma={sig:.6e}", flush=True)
 
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT} ({len(out)} arrays, {OUT.stat().st_size / 1e6:.1f} MB)")

@@ -189,3 +189,33 @@ def test_cox_4000x3000_breslow_100_iterations(gs, name):
     else:
         np.testing.assert_allclose(tr, gs[f"{name}_trace"], rtol=2e-5)
         assert normwise(beta, ref_beta) <= 1e-4
+
+
+@pytest.mark.parametrize("storage,p", [("packed", 1), ("packed", 2), ("int8", 2)])
+def test_cox_genotypes_float64_against_reference(gs, storage, p):
+    """Genotype Cox in float64 against the reference run on the same 0/1/2 matrix as float64
+    (make_golden_scale.py cox_geno_f64): packed storage takes both passes on the tensor cores
+    (kind::mxf4 with 32 digits), int8 storage the exact CUDA-core kernels."""
+    m, n, seed, lam, _, iters = gs["cox_geno_f64_meta"]
+    m, n, seed, iters = int(m), int(n), int(seed), int(iters)
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(seed + 7)).random(m) < 0.4).astype(np.float64)
+
+    def fn(comm):
+        if storage == "packed":
+            x = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        else:
+            x = bs.genotype_fill(bs.empty((m, n), comm, np.int8), seed)
+        bs.gemm_path_counts(reset=True)
+        st = bs.cox_init(x, y, delta, lam=float(lam), ties="breslow", dtype=np.float64)
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.beta), st.sigma, bs.gemm_path_counts()["cox_packed_tensor"]
+
+    tr, beta, sig, passes = bs.run_inproc(p, fn)[0]
+    if storage == "packed":
+        assert passes >= 2 * iters
+    ref_beta = gs["cox_geno_f64_beta"]
+    np.testing.assert_allclose(sig, gs["cox_geno_f64_sigma"][0], rtol=1e-9)
+    np.testing.assert_allclose(tr, gs["cox_geno_f64_trace"], rtol=1e-9)
+    assert normwise(beta, ref_beta) <= 1e-8
+    np.testing.assert_array_equal(beta == 0, ref_beta == 0)
