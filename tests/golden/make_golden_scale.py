@@ -180,6 +180,10 @@ def main(only=None):
         out["cox_geno_f64_meta"] = np.array([m, n, seed, 2e-6, -1.0, 100], dtype=np.float64)
         out["cox_geno_f64_trace"], out["cox_geno_f64_beta"], out["cox_geno_f64_sigma"] = tr, beta, np.array([sig])
         print(f"cox_geno_f64 {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)} sigma={sig:.6e}", flush=True)
+        # the same in float32 arithmetic (the C5 setting), with the float64 run's sigma
+        tr, beta, sig = bs.run_inproc(2, cox_run, xg, y, delta, 2e-6, float(sig), 100, np.float32)[0]
+        out["cox_geno_f32_trace"], out["cox_geno_f32_beta"], out["cox_geno_f32_sigma"] = tr, beta, np.array([sig])
+        print(f"cox_geno_f32 {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)}", flush=True)
 
     np.savez_compressed(OUT, **out)
     print(f"wrote {OUT} ({len(out)} arrays, {OUT.stat().st_size / 1e6:.1f} MB)")

@@ -219,3 +219,25 @@ def test_cox_genotypes_float64_against_reference(gs, storage, p):
     np.testing.assert_allclose(tr, gs["cox_geno_f64_trace"], rtol=1e-9)
     assert normwise(beta, ref_beta) <= 1e-8
     np.testing.assert_array_equal(beta == 0, ref_beta == 0)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cox_genotypes_float32_against_reference(gs, p):
+    """The C5 setting (packed genotypes, float32 arithmetic, both passes on the tensor cores)
+    against the reference's float32 run on the same matrix: traces at 2e-5 (the reference's own
+    float32 rounding), beta at 1e-4 normwise."""
+    m, n, seed, lam, _, iters = gs["cox_geno_f64_meta"]
+    m, n, seed, iters = int(m), int(n), int(seed), int(iters)
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(seed + 7)).random(m) < 0.4).astype(np.float64)
+    sigma = float(gs["cox_geno_f32_sigma"][0])
+
+    def fn(comm):
+        x = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        st = bs.cox_init(x, y, delta, lam=float(lam), sigma=sigma, ties="breslow", dtype=np.float32)
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.beta)
+
+    tr, beta = bs.run_inproc(p, fn)[0]
+    np.testing.assert_allclose(tr, gs["cox_geno_f32_trace"], rtol=2e-5)
+    assert normwise(beta, gs["cox_geno_f32_beta"]) <= 1e-4
