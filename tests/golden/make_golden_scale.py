@@ -24,6 +24,8 @@ Cases (SURVEY.md §8(c) parity protocol; VERDICT r01 "Next round" item 1):
                      cancels catastrophically
   mds_n2000_{f32,f64} MDS, 2,000 points from 100-dim data, q = 20, 100 iterations
                      (solvers.py:269-305)
+  mds_n8000_f32      MDS, 8,000 points, q = 20, 20 iterations, float32 (several row
+                     segments and column blocks per rank in the tensor-core pass)
   cox_breslow_f64    Cox, X 4,000 x 3,000 (uniform - 0.5), Breslow ties, default
                      power-iteration sigma, 100 iterations (solvers.py:337-450)
   cox_f32            same X in float32, explicit sigma, 100 iterations
@@ -151,6 +153,29 @@ def main(only=None):
         out[f"{name}_meta"] = np.array([100, 2000, 20, 2050, 2051, 100], dtype=np.int64)
         out[f"{name}_trace"], out[f"{name}_theta"] = tr, th
         print(f"{name} {time.time() - t0:.0f}s", flush=True)
+
+    if want("mds_n8000_f32"):
+        # more points than one segment of the tensor-core pass holds: several row segments
+        # and column blocks per rank, 20 iterations, float32
+        tr, th = bs.run_inproc(2, mds_run, 100, 8000, 20, 2080, 2081, np.float32, 20)[0]
+        out["mds_n8000_f32_meta"] = np.array([100, 8000, 20, 2080, 2081, 20], dtype=np.int64)
+        out["mds_n8000_f32_trace"], out["mds_n8000_f32_theta"] = tr, th
+        # The reference's float32 stress is a float32 dot over n^2 = 64M terms: 1.5e-4 low at
+        # theta0 against the same float32 terms summed in float64.  Store that float64 sum for
+        # the first trace entry (the same float32 Y, theta0 and Gram-identity distances).
+        sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+        from oracle import blockstat_oracle as orc
+
+        xf = orc.rand_fill_common((100, 8000), 2080, np.float32)
+        yf = orc.pairwise_euclidean(xf)
+        th0 = orc.mds_init(yf, 20, 2081)
+        g0 = th0.T @ th0
+        nr = np.diag(g0)
+        d0 = np.sqrt(np.maximum(nr[:, None] + nr[None, :] - 2 * g0, 0)).astype(np.float32)
+        np.fill_diagonal(d0, 0)
+        out["mds_n8000_f32_stress0_f64"] = np.array([float(np.sum((yf.astype(np.float64) - d0) ** 2))])
+        print(f"mds_n8000_f32 {time.time() - t0:.0f}s  reference trace[0] / float64 sum - 1 = "
+              f"{tr[0] / out['mds_n8000_f32_stress0_f64'][0] - 1:.2e}", flush=True)
 
     def cox_run(comm, x, y, delta, lam, sigma, iters, dt):
         xd = bs.distribute(x.astype(dt) if comm.rank == 0 else None, comm)

@@ -241,3 +241,29 @@ def test_cox_genotypes_float32_against_reference(gs, p):
     tr, beta = bs.run_inproc(p, fn)[0]
     np.testing.assert_allclose(tr, gs["cox_geno_f32_trace"], rtol=2e-5)
     assert normwise(beta, gs["cox_geno_f32_beta"]) <= 1e-4
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_mds_n8000_f32_20_iterations(gs, p):
+    """MDS with 8,000 points through the tcgen05 pass (several row segments and column blocks
+    per rank) against the reference's float32 run.  The reference's float32 stress is a float32
+    dot over n^2 = 64M terms, 1.5e-4 low at theta0 against a float64 sum of the same float32 terms
+    (make_golden_scale.py): our first trace entry is checked against that float64 sum at 1e-5,
+    the trace against the reference at 5e-4, the final theta at 1e-4 normwise."""
+    d, n, q, xs, ts, iters = (int(v) for v in gs["mds_n8000_f32_meta"])
+
+    def fn(comm):
+        x = bs.empty((d, n), comm, np.float32)
+        bs.rand_fill(x, seed=xs, common_init=True)
+        y = bs.empty((n, n), comm, np.float32)
+        bs.pairwise_euclidean(y, x)
+        st = bs.mds_init(y, q, seed=ts)
+        bs.gemm_path_counts(reset=True)
+        bs.mds_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.theta), bs.gemm_path_counts()["mds_tensor"]
+
+    tr, th, passes = bs.run_inproc(p, fn)[0]
+    assert passes >= iters
+    np.testing.assert_allclose(tr[0], gs["mds_n8000_f32_stress0_f64"][0], rtol=1e-5)
+    np.testing.assert_allclose(tr, gs["mds_n8000_f32_trace"], rtol=5e-4)
+    assert normwise(th, gs["mds_n8000_f32_theta"]) <= 1e-4
