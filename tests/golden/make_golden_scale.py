@@ -29,6 +29,8 @@ Cases (SURVEY.md §8(c) parity protocol; VERDICT r01 "Next round" item 1):
   cox_breslow_f64    Cox, X 4,000 x 3,000 (uniform - 0.5), Breslow ties, default
                      power-iteration sigma, 100 iterations (solvers.py:337-450)
   cox_f32            same X in float32, explicit sigma, 100 iterations
+  cox_f32_fused      Cox float32, X 20,000 x 2,000 (uniform - 0.5), Breslow, explicit sigma,
+                     50 iterations: large enough for the one-stream fused pass (C4's kernel)
   cox_geno_f64       Cox on genotypes (the counter-based generator of this build, values
                      0/1/2 handed to the reference as float64 — it has no int8 arithmetic),
                      4,000 x 3,000, Breslow ties, default sigma, 100 iterations: pins the
@@ -192,6 +194,16 @@ def main(only=None):
         out[f"{name}_meta"] = np.array([m, n, 2060, lam, -1.0 if sigma is None else sigma, 100], dtype=np.float64)
         out[f"{name}_trace"], out[f"{name}_beta"], out[f"{name}_sigma"] = tr, beta, np.array([sig])
         print(f"{name} {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)} sigma={sig:.6e}", flush=True)
+
+    if want("cox_f32_fused"):
+        # float32 X large enough for the one-stream fused pass (m >= 4096, n >= 128): the C4
+        # kernel (bs_cox_grad_xbeta) against the reference's float32 arithmetic
+        m2, n2 = 20000, 2000
+        x2, y2, delta2 = cox_inputs(m2, n2, 2090)
+        tr, beta, sig = bs.run_inproc(2, cox_run, x2, y2, delta2, 2e-3, 1e-4, 50, np.float32)[0]
+        out["cox_f32_fused_meta"] = np.array([m2, n2, 2090, 2e-3, 1e-4, 50], dtype=np.float64)
+        out["cox_f32_fused_trace"], out["cox_f32_fused_beta"] = tr, beta
+        print(f"cox_f32_fused {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)}", flush=True)
 
     if want("cox_geno_f64"):
         sys.path.insert(0, str(Path(__file__).resolve().parents[2]))

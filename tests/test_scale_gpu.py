@@ -267,3 +267,32 @@ def test_mds_n8000_f32_20_iterations(gs, p):
     np.testing.assert_allclose(tr[0], gs["mds_n8000_f32_stress0_f64"][0], rtol=1e-5)
     np.testing.assert_allclose(tr, gs["mds_n8000_f32_trace"], rtol=5e-4)
     assert normwise(th, gs["mds_n8000_f32_theta"]) <= 1e-4
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cox_f32_fused_pass_against_reference(gs, p):
+    """float32 Cox large enough for the one-stream fused pass (bs_cox_grad_xbeta, C4's kernel:
+    m >= 4096, n_loc >= 128) against the reference's float32 run: traces at 2e-5, beta 1e-4."""
+    from paper_2010_16114_b200 import _lib
+
+    m, n, seed, lam, sigma, iters = gs["cox_f32_fused_meta"]
+    m, n, seed, iters = int(m), int(n), int(seed), int(iters)
+    y, delta = cox_inputs(m, n, seed)
+
+    def fn(comm):
+        x64 = bs.empty((m, n), comm, np.float64)
+        bs.rand_fill(x64, seed=seed, common_init=True)
+        x = bs.empty((m, n), comm, np.float32)
+        x.local.copy_(x64.local - 0.5)
+        del x64
+        st = bs.cox_init(x, y, delta, lam=float(lam), sigma=float(sigma), ties="breslow")
+        with _lib.profile(["bs_cox_grad_xbeta"]) as prof:
+            bs.cox_fit(st, iters)
+            torch.cuda.synchronize()
+        return np.asarray(st.trace), bs.gather_full(st.beta), len(prof.elapsed_ms().get("bs_cox_grad_xbeta", []))
+
+    tr, beta, fused = bs.run_inproc(p, fn)[0]
+    if p == 1:  # (the profile hook is process-wide: rank threads would share it)
+        assert fused >= iters - 1  # every iteration after the first takes the one-stream pass
+    np.testing.assert_allclose(tr, gs["cox_f32_fused_trace"], rtol=2e-5)
+    assert normwise(beta, gs["cox_f32_fused_beta"]) <= 1e-4
