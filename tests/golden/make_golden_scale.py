@@ -18,6 +18,7 @@ Cases (SURVEY.md §8(c) parity protocol; VERDICT r01 "Next round" item 1):
   c2k_slice          NMF-APG float32, X 200,000 x 1,024, r = 60, 20 iterations: scn a
                      reduces over K = m = 200,000 as in C2 (solvers.py:165-185,
                      distlinalg.py:239-243)
+  nmf_apg_f64_r60    NMF-APG float64, 20,000 x 2,000, r = 60 (C2's rank), 20 iterations
   nmf_mu_f32         NMF-MU float32, 2,000 x 1,500, r = 20, 100 iterations
   nmf_planted_*      float32 X = V*^T W* + 1e-3 noise started next to (V*, W*): the
                      objective is ~1e-6 of ||X||^2, where a Gram-identity objective
@@ -118,6 +119,15 @@ def main(only=None):
         print(f"c2k_slice {time.time() - t0:.0f}s trace[-1]={tr[-1]:.9e} obj64={out['c2k_slice_obj64'][0]:.9e}",
               flush=True)
         del x
+
+    if want("nmf_apg_f64_r60"):
+        # C2's rank in float64: the cp.async m16n8k16 DMMA kernel at RP = 64
+        tr, vt, w = bs.run_inproc(2, nmf_run, 20000, 2000, 60, 2035, 2036, np.float64, "apg", 20, 1)[0]
+        out["nmf_apg_f64_r60_meta"] = np.array([20000, 2000, 60, 2035, 2036, 20, 1, 1], dtype=np.int64)
+        out["nmf_apg_f64_r60_trace"], out["nmf_apg_f64_r60_w"] = tr, w
+        out["nmf_apg_f64_r60_vt_sample"] = np.ascontiguousarray(vt[:, ::20])  # keeps the fixture small
+        out["nmf_apg_f64_r60_vt_rowsum"] = vt.sum(axis=1)
+        print(f"nmf_apg_f64_r60 {time.time() - t0:.0f}s", flush=True)
 
     if want("nmf_mu_f32"):
         tr, vt, w = bs.run_inproc(2, nmf_run, 2000, 1500, 20, 2030, 2031, np.float32, "mu", 100, 10)[0]

@@ -296,3 +296,15 @@ def test_cox_f32_fused_pass_against_reference(gs, p):
         assert fused >= iters - 1  # every iteration after the first takes the one-stream pass
     np.testing.assert_allclose(tr, gs["cox_f32_fused_trace"], rtol=2e-5)
     assert normwise(beta, gs["cox_f32_fused_beta"]) <= 1e-4
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_nmf_apg_f64_rank60_against_reference(gs, p):
+    """C2's rank in float64 (the cp.async m16n8k16 DMMA kernel at RP = 64) against the reference:
+    trace 1e-9, iterates 1e-8 normwise."""
+    m, n, r, xs, fs, iters, every, _ = (int(v) for v in gs["nmf_apg_f64_r60_meta"])
+    tr, vt, w, _ = bs.run_inproc(p, _nmf, m, n, r, xs, fs, np.float64, 1, iters, every)[0]
+    np.testing.assert_allclose(tr, gs["nmf_apg_f64_r60_trace"], rtol=1e-9)
+    assert normwise(vt[:, ::20], gs["nmf_apg_f64_r60_vt_sample"]) <= 1e-8
+    np.testing.assert_allclose(vt.sum(axis=1), gs["nmf_apg_f64_r60_vt_rowsum"], rtol=1e-9)
+    assert normwise(w, gs["nmf_apg_f64_r60_w"]) <= 1e-8
