@@ -32,6 +32,8 @@ Cases (SURVEY.md §8(c) parity protocol; VERDICT r01 "Next round" item 1):
   cox_f32            same X in float32, explicit sigma, 100 iterations
   cox_f32_fused      Cox float32, X 20,000 x 2,000 (uniform - 0.5), Breslow, explicit sigma,
                      50 iterations: large enough for the one-stream fused pass (C4's kernel)
+  cox_geno_long_f64  Cox on genotypes, 200,000 x 1,024, float64, 10 iterations (long K for
+                     the packed tensor-core passes)
   cox_geno_f64       Cox on genotypes (the counter-based generator of this build, values
                      0/1/2 handed to the reference as float64 — it has no int8 arithmetic),
                      4,000 x 3,000, Breslow ties, default sigma, 100 iterations: pins the
@@ -204,6 +206,23 @@ def main(only=None):
         out[f"{name}_meta"] = np.array([m, n, 2060, lam, -1.0 if sigma is None else sigma, 100], dtype=np.float64)
         out[f"{name}_trace"], out[f"{name}_beta"], out[f"{name}_sigma"] = tr, beta, np.array([sig])
         print(f"{name} {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)} sigma={sig:.6e}", flush=True)
+
+    if want("cox_geno_long_f64"):
+        # long K for the packed tensor-core passes: 200,000 samples (98 groups of 2,048 rows in
+        # the gradient), 1,024 variants, float64, default sigma, 10 iterations
+        sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+        from oracle import blockstat_oracle as orc
+
+        m3, n3, seed3 = 200000, 1024, 2095
+        xg3 = orc.genotype_fill(m3, n3, seed3).astype(np.float64)
+        y3 = np.floor(np.arange(m3, 0, -1) / 4.0)
+        delta3 = (np.random.Generator(np.random.Philox(seed3 + 7)).random(m3) < 0.3).astype(np.float64)
+        tr, beta, sig = bs.run_inproc(2, cox_run, xg3, y3, delta3, 1e-7, None, 10, np.float64)[0]
+        out["cox_geno_long_f64_meta"] = np.array([m3, n3, seed3, 1e-7, -1.0, 10], dtype=np.float64)
+        out["cox_geno_long_f64_trace"], out["cox_geno_long_f64_beta"] = tr, beta
+        out["cox_geno_long_f64_sigma"] = np.array([sig])
+        print(f"cox_geno_long_f64 {time.time() - t0:.0f}s nnz={np.count_nonzero(beta)}", flush=True)
+        del xg3
 
     if want("cox_f32_fused"):
         # float32 X large enough for the one-stream fused pass (m >= 4096, n >= 128): the C4

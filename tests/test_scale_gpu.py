@@ -308,3 +308,26 @@ def test_nmf_apg_f64_rank60_against_reference(gs, p):
     assert normwise(vt[:, ::20], gs["nmf_apg_f64_r60_vt_sample"]) <= 1e-8
     np.testing.assert_allclose(vt.sum(axis=1), gs["nmf_apg_f64_r60_vt_rowsum"], rtol=1e-9)
     assert normwise(w, gs["nmf_apg_f64_r60_w"]) <= 1e-8
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_cox_genotypes_long_k_float64(gs, p):
+    """200,000 samples x 1,024 packed variants in float64 (the tensor-core passes over 98
+    scale groups) against the reference: sigma, trace 1e-9, beta 1e-8, zero pattern."""
+    m, n, seed, lam, _, iters = gs["cox_geno_long_f64_meta"]
+    m, n, seed, iters = int(m), int(n), int(seed), int(iters)
+    y = np.floor(np.arange(m, 0, -1) / 4.0)
+    delta = (np.random.Generator(np.random.Philox(seed + 7)).random(m) < 0.3).astype(np.float64)
+
+    def fn(comm):
+        x = bs.genotype_fill(bs.PackedGenotypes(comm, (m, n)), seed)
+        st = bs.cox_init(x, y, delta, lam=float(lam), ties="breslow", dtype=np.float64)
+        bs.cox_fit(st, iters)
+        return np.asarray(st.trace), bs.gather_full(st.beta), st.sigma
+
+    tr, beta, sig = bs.run_inproc(p, fn)[0]
+    ref = gs["cox_geno_long_f64_beta"]
+    np.testing.assert_allclose(sig, gs["cox_geno_long_f64_sigma"][0], rtol=1e-9)
+    np.testing.assert_allclose(tr, gs["cox_geno_long_f64_trace"], rtol=1e-9)
+    assert normwise(beta, ref) <= 1e-8
+    np.testing.assert_array_equal(beta == 0, ref == 0)
