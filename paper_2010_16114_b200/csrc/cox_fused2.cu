@@ -407,7 +407,11 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
   const int nst = as_[ci] + bs_[ci];
   const int64_t rmax = std::min<int64_t>(1024 * kb_[ci], (4 * F2_STAGE_MAX / nst) / (4 * CW));
   int best_s = 0, best_u = 0;
-  for (int S = int(ceil_div(m, rmax)); S <= G; ++S) {
+  const int s_min = int(ceil_div(m, rmax));
+  for (int S = s_min; S <= G; ++S) {  // a segment count that fills every SM, if one is near
+    if (G % S == 0 && S * 4 <= s_min * 5) { best_s = S; best_u = G; break; }
+  }
+  for (int S = s_min; S <= G && best_u < G; ++S) {
     const int u = S * (G / S);
     if (u > best_u) { best_u = u; best_s = S; }
     if (u * 100 >= G * 96) { best_s = S; best_u = u; break; }
