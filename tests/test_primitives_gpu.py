@@ -203,3 +203,26 @@ def test_normal_fill_is_rank_count_independent_and_normal(dt):
         z = orc.philox_normal(77, e, 1)[0]
         assert abs(float(flat[e]) - z) <= (1e-6 if dt == np.float32 else 1e-12) * max(1.0, abs(z))
     assert abs(flat.mean()) < 0.02 and abs(flat.std() - 1.0) < 0.02
+
+
+@pytest.mark.parametrize("p", [1, 3])
+def test_transposed_view_is_a_lazy_row_split_transpose(p):
+    """transpose / TransposedView (distarray.py:111-136): shape swapped, the parent's partition
+    (rows of the view), no copy, and transposing twice gives the parent back."""
+    x = np.arange(7 * 11, dtype=np.float64).reshape((7, 11), order="F")
+
+    def fn(comm):
+        a = bs.distribute(x if comm.rank == 0 else None, comm)
+        t = bs.transpose(a)
+        assert isinstance(t, bs.TransposedView)
+        assert t.shape == (11, 7) and t.dtype == a.dtype and t.comm is comm
+        assert t.partition.counts() == a.partition.counts()  # the view's rows = the parent's columns
+        assert bs.transpose(t) is a
+        with pytest.raises(TypeError):
+            bs.transpose(np.zeros((2, 2)))
+        # the rank's rows of the view are its columns of the parent, no copy
+        return a.local.data_ptr(), t.parent.local.data_ptr(), bs.gather_full(t.parent)
+
+    for ptr_a, ptr_t, full in bs.run_inproc(p, fn):
+        assert ptr_a == ptr_t
+        np.testing.assert_array_equal(full, x)
