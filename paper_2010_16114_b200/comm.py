@@ -37,6 +37,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import os
+import re
 import threading
 
 import numpy as np
@@ -599,6 +600,11 @@ class _TorchCommunicator(Communicator):
 # ---------------------------------------------------------------------------
 
 
+_TCP_ENTRY = r"([^,]+?):(\d+)(?=,|$)"  # host (IPv6 brackets included) : port
+_TCP_RE = re.compile(r"tcp:(?P<hosts>[^,]+?:\d+(?:,[^,]+?:\d+)*),rank=(?P<rank>\d+)")
+_TCP_ENTRY_RE = re.compile(_TCP_ENTRY)
+
+
 def _parse_descriptor(descriptor):
     if descriptor.startswith("inproc:"):
         try:
@@ -613,18 +619,12 @@ def _parse_descriptor(descriptor):
     if descriptor.startswith("tcp:"):
         # tcp:host:port,...,rank=<r> (comm.py:501-519): one process per rank; here the
         # first entry is the TCPStore that bootstraps NCCL (gloo without a GPU).
-        parts = descriptor[4:].split(",")
-        if len(parts) < 2 or not parts[-1].startswith("rank="):
+        m = _TCP_RE.fullmatch(descriptor)
+        if m is None:
             raise CommInitError(f"bad tcp descriptor {descriptor!r}; expected tcp:host:port,...,rank=<r>")
-        try:
-            rank = int(parts[-1][5:])
-            hosts = []
-            for entry in parts[:-1]:
-                host, port = entry.rsplit(":", 1)
-                hosts.append((host, int(port)))
-        except ValueError:
-            raise CommInitError(f"bad tcp descriptor {descriptor!r}") from None
-        if not 0 <= rank < len(hosts):
+        hosts = [(h, int(pt)) for h, pt in _TCP_ENTRY_RE.findall(m.group("hosts"))]
+        rank = int(m.group("rank"))
+        if rank >= len(hosts):
             raise CommInitError(f"rank {rank} out of range for {len(hosts)} hosts")
         return "tcp", (hosts, rank)
     raise CommInitError(f"unknown backend descriptor {descriptor!r}")
