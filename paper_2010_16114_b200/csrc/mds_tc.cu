@@ -110,11 +110,11 @@ __device__ __noinline__ float direct_d2(const float* ti, const float* tj, int q)
 // The 16 pairs of one (column, row slice) with every special case of the MM step:
 // buf[0..16) = y, buf[16..32) = d2 from the tensor core; writes w = (W - Z)_ij to
 // buf[32..48) and returns the slice's stress.
-__device__ __noinline__ float careful_block(float* buf, int64_t ib, int64_t i_end, int64_t jg, bool live, float thr,
+__device__ __noinline__ float careful_block(float* buf, int ib, int i_end, int jg, bool live, float thr,
                                            const float* theta, int q, int perturb, double& zeros) {
   float st = 0.f;
   for (int e = 0; e < 16; ++e) {
-    const int64_t i = ib + e;
+    const int i = ib + e;
     const float y = buf[e];
     float w = 0.f;
     if (live && i < i_end) {
@@ -122,7 +122,7 @@ __device__ __noinline__ float careful_block(float* buf, int64_t ib, int64_t i_en
         st = fmaf(y, y, st);
       } else {
         float d2 = buf[16 + e];
-        if (!(d2 > thr)) d2 = direct_d2(theta + i * q, theta + jg * q, q);
+        if (!(d2 > thr)) d2 = direct_d2(theta + int64_t(i) * q, theta + int64_t(jg) * q, q);
         float d, z;
         if (d2 > 0.f) {
           const float r = rsqrt_approx(d2);
@@ -392,10 +392,13 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       int64_t j0, i0;
       int nch, seg;
       unit_range(u, j0, i0, nch, seg);
-      const int64_t jl = j0 + jrow;
+      // 32-bit row / column indices (n <= INT32_MAX is part of mds_tc_eligible): 64-bit ones
+      // cost four registers the 96-register budget does not have (they were spilled)
+      const int jl = int(j0) + jrow;
       const bool live = jl < a.n_loc;
-      const int64_t jg = a.lo + (live ? jl : 0);
-      const int64_t i_end = min(a.n, i0 + a.rows_per_seg);
+      const int jg = int(a.lo) + (live ? jl : 0);
+      const int i0i = int(i0);
+      const int i_end = int(min(a.n, i0 + a.rows_per_seg));
       // A1: v_j into TMEM (K-major): sub 0/1 write hi k 0-15/16-31, sub 2/3 the lo half
       mbar_wait(a1_empty, (ut & 1) ^ 1);
       tc_fence_after();
@@ -436,7 +439,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       for (int t = 0; t < nch; ++t, ++cc) {
         const int s = int(cc % NY);
         const uint32_t b = cc & 1;
-        const int64_t ib = i0 + int64_t(t) * CHI + 16 * sub;  // first row of this warp's 16
+        const int ib = i0i + t * CHI + 16 * sub;  // first row of this warp's 16
         // Y tile: box sub/2 holds rows 32 (sub/2) .. +31; row jrow is 128 B of 16 B chunks
         // stored at chunk ^ (jrow & 7) (SWIZZLE_128B)
         uint4 yv[4];
@@ -539,7 +542,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           const int kk = 8 * sub + k;
           if (kk < q) tp[kk] = double(Tacc[k]);
           if (kk == q) {
-            const int64_t cnt = (i_end - i0) - ((jg >= i0 && jg < i_end) ? 1 : 0);
+            const int cnt = (i_end - i0i) - ((jg >= i0i && jg < i_end) ? 1 : 0);
             a.zsum_part[int64_t(seg) * a.n_loc + jl] = double(cnt) - double(Tacc[k]);
           }
         }
