@@ -10,7 +10,9 @@
 // so zsum_j = (#i) - T_aug[j][q].  For a tile of 128 columns j x 64 rows i:
 //   MMA1  D1[j][i]  = sum_k V[j][k] U[i][k]       M = 128, N = 64, K = 8 * ceil((q + 2) / 8)
 //   MMA2  D2[j][k] += sum_i W[j][i] U[i][k]       M = 128, N = 32, K = 64
-// both in 3xTF32 (hi*hi + hi*lo + lo*hi: fp32-level error).  Per pair the CUDA cores only
+// both in 3xTF32 (hi*hi + hi*lo + lo*hi: fp32-level error).  When 1 <= max_i |theta_i|^2 < 2^14
+// MMA1 runs on an f16 hi/lo split instead (kind::f16, K = 16 per instruction: 6 MMAs per chunk
+// instead of 9 at q = 20; same three products, error ~2^-23 of the operands; see f16_range).  Per pair the CUDA cores only
 // do rsqrt, d, z, (y - d)^2, 1 - z and the tf32 split (about 9 instructions).  Y is read
 // once, by TMA, like the CUDA-core pass (mds.cu).
 //
@@ -33,6 +35,8 @@
 // points give d = 0 exactly, as the reference's Gram identity does on its own input
 // (solvers.py:246, 290-296).
 #include "tc_common.cuh"
+
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <mutex>
@@ -57,6 +61,11 @@ constexpr int OFF_B2 = OFF_B1 + NB1 * B_STAGE;
 constexpr int RINGS = OFF_B2 + NB2 * B_STAGE;
 constexpr int SMEM = RINGS + 1024 /*align*/ + 512 /*barriers*/ + 16 * 2 * 8 /*stress fold*/ + 512;
 constexpr uint32_t T_D1 = 0, T_D2 = 128, T_A1 = 192, T_A2 = 256;
+constexpr int B1_F16 = CHI * 128;    // f16 B1 stage: one 128-byte row [hi k0..31 | lo k0..31] per i
+// f16 range of MMA1's operands: |theta| < 128 and |theta|^2 < 2^14 keep every hi part finite;
+// below max |theta|^2 = 1 the subnormal lo parts of small coordinates would cost more than the
+// tf32 split's error, so that case stays on 3xTF32.
+__host__ __device__ inline bool f16_range(float nmax) { return nmax >= 1.0f && nmax < 16384.0f; }
 constexpr float CANCEL = 1.0f / 4096.0f;
 
 // One 8-wide k step of MMA1: D += A_hi Bh + A_hi Bl + A_lo Bh (K-major smem B).
@@ -72,6 +81,23 @@ __device__ __forceinline__ void mma3_kstep(uint32_t d, uint32_t a_hi, uint32_t a
       "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(id), "r"(acc0)
       : "memory");
 }
+
+// The same k step on the f16 split (K = 16): D += A_hi Bh + A_hi Bl + A_lo Bh.
+__device__ __forceinline__ void mma3_kstep_f16(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh, uint64_t bl,
+                                               uint32_t id, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.b32 q, %6, 0;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, q;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, 1;\n\t"
+      "@p tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, 1;\n\t}" ::"r"(d),
+      "r"(a_hi), "r"(a_lo), "l"(bh), "l"(bl), "r"(id), "r"(acc0)
+      : "memory");
+}
+
+// kind::f16 (f16 x f16 -> f32), both operands K-major.
+constexpr uint32_t idesc_f16(int M, int N) { return (1u << 4) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24); }
 
 __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
   uint64_t r;
@@ -159,6 +185,8 @@ struct MdsTcArgs {
   const float* theta;   // q x n (theta_full, column-major)
   const float* vj_hi;   // n x 32: [-2 theta_j, |theta_j|^2, 1, 0...] tf32 hi
   const float* vj_lo;   //         ... lo
+  const uint32_t* vj16; // n x 32 words: the same row as f16 [hi k0..31 | lo k0..31]
+  int f16_ok;           // 0: MMA1 always in 3xTF32 (BS_MDS_TC_F16=0)
   const float* norms;   // n
   const float* nmax;    // max_i |theta_i|^2 (1 float)
   int64_t n, lo, n_loc;
@@ -178,7 +206,8 @@ template <int KS>
 __global__ void __launch_bounds__(MT_THREADS, 1)
 mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ CUtensorMap tmKh,
               const __grid_constant__ CUtensorMap tmKl, const __grid_constant__ CUtensorMap tmMh,
-              const __grid_constant__ CUtensorMap tmMl, const MdsTcArgs a) {
+              const __grid_constant__ CUtensorMap tmMl, const __grid_constant__ CUtensorMap tmK16,
+              const MdsTcArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RINGS);
@@ -231,6 +260,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmY);
     prefetch_tmap(&tmKh);
+    prefetch_tmap(&tmK16);
     prefetch_tmap(&tmKl);
     prefetch_tmap(&tmMh);
     prefetch_tmap(&tmMl);
@@ -245,6 +275,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int units = a.jblocks * a.segs;
+  const bool f16 = a.f16_ok && f16_range(__ldg(a.nmax));  // uniform over the grid
   auto unit_range = [&](int u, int64_t& j0, int64_t& i0, int& nch, int& seg) {
     seg = u / a.jblocks;
     j0 = int64_t(u - seg * a.jblocks) * BJ;
@@ -267,9 +298,14 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
             const int s = int(cc % NB1);
             mbar_wait_sleep(b1_empty(s), ((cc / NB1) & 1) ^ 1);
             const uint32_t fb = b1_full(s), base = smem_u32(b1_at(cc));
-            mbar_expect_tx(fb, B_STAGE);
-            tma_load_2d(base, &tmKh, 0, ic, fb);
-            tma_load_2d(base + 8192, &tmKl, 0, ic, fb);
+            if (f16) {
+              mbar_expect_tx(fb, B1_F16);
+              tma_load_2d(base, &tmK16, 0, ic, fb);
+            } else {
+              mbar_expect_tx(fb, B_STAGE);
+              tma_load_2d(base, &tmKh, 0, ic, fb);
+              tma_load_2d(base + 8192, &tmKl, 0, ic, fb);
+            }
           }
           {
             const int s = int(cc % NY);
@@ -300,6 +336,8 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
     // MMA2 of the oldest chunk goes as soon as its A2 is written.  The tensor pipe
     // executes in issue order.
     constexpr uint32_t id1 = idesc_tf32(128, CHI, false, false);
+    constexpr uint32_t id1h = idesc_f16(128, CHI);
+    constexpr int KS16 = (KS + 1) / 2;
     constexpr uint32_t id2w = idesc_tf32(128, 2 * KP, false, true);
     constexpr uint32_t id2n = idesc_tf32(128, KP, false, true);
     uint32_t cbase = 0, gi = 0, ut = 0;
@@ -327,9 +365,16 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
             const uint32_t ah = __shfl_sync(0xffffffffu, tmem + T_A1, 0);
             const uint32_t bh = __shfl_sync(0xffffffffu, smem_u32(b1_at(c)), 0);
             const uint64_t dh = sdesc(bh, 16, 1024, LAYOUT_SW128), dl = sdesc(bh + 8192, 16, 1024, LAYOUT_SW128);
+            if (f16) {
+              // A1: hi in columns 0-15, lo in 16-31 (two f16 per column); B1 row: hi at +0, lo at +64 B
 #pragma unroll
-            for (int k = 0; k < KS; ++k)
-              if (!(a.mode & 2)) mma3_kstep(d, ah + 8 * k, ah + 32 + 8 * k, dh + 2 * k, dl + 2 * k, id1, k > 0);
+              for (int k = 0; k < KS16; ++k)
+                if (!(a.mode & 2)) mma3_kstep_f16(d, ah + 8 * k, ah + 16 + 8 * k, dh + 2 * k, dh + 4 + 2 * k, id1h, k > 0);
+            } else {
+#pragma unroll
+              for (int k = 0; k < KS; ++k)
+                if (!(a.mode & 2)) mma3_kstep(d, ah + 8 * k, ah + 32 + 8 * k, dh + 2 * k, dl + 2 * k, id1, k > 0);
+            }
             mma_commit_elect(d1_full(b));
             if (lane == 0) tr_mark(a.trace, 0, c);  // MMA1 issued
             mma_commit_elect(b1_empty(s));
@@ -402,7 +447,19 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
       // A1: v_j into TMEM (K-major): sub 0/1 write hi k 0-15/16-31, sub 2/3 the lo half
       mbar_wait(a1_empty, (ut & 1) ^ 1);
       tc_fence_after();
-      {
+      if (f16) {  // sub 0 / 1 write the hi / lo half (16 columns each)
+        if (sub < 2) {
+          uint32_t v[16];
+          const uint4* src = reinterpret_cast<const uint4*>(a.vj16 + int64_t(jg) * KP + 16 * sub);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 w = live ? __ldg(src + c) : make_uint4(0u, 0u, 0u, 0u);
+            v[4 * c] = w.x; v[4 * c + 1] = w.y; v[4 * c + 2] = w.z; v[4 * c + 3] = w.w;
+          }
+          tmem_st16(tmem + lane_addr + T_A1 + 16 * sub, v);
+          tmem_wait_st();
+        }
+      } else {
         uint32_t v[16];
         const float4* src = reinterpret_cast<const float4*>((sub >= 2 ? a.vj_lo : a.vj_hi) + jg * KP + 16 * (sub & 1));
 #pragma unroll
@@ -591,7 +648,8 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
 // their float bits order like integers).
 __global__ void mds_tc_prep_kernel(const float* __restrict__ theta, int64_t n, int q, float* __restrict__ uh,
                                    float* __restrict__ ul, float* __restrict__ vh, float* __restrict__ vl,
-                                   float* __restrict__ norms, float* __restrict__ nmax) {
+                                   __half* __restrict__ u16, __half* __restrict__ v16, float* __restrict__ norms,
+                                   float* __restrict__ nmax) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const float* t = theta + i * q;
     float s = 0.f;
@@ -602,6 +660,8 @@ __global__ void mds_tc_prep_kernel(const float* __restrict__ theta, int64_t n, i
     float* ulr = ul + i * KP;
     float* vhr = vh + i * KP;
     float* vlr = vl + i * KP;
+    __half* u16r = u16 + i * 2 * KP;
+    __half* v16r = v16 + i * 2 * KP;
     for (int k = 0; k < KP; ++k) {
       const float u = k < q ? t[k] : k == q ? 1.f : k == q + 1 ? s : 0.f;
       const float v = k < q ? -2.f * t[k] : k == q ? s : k == q + 1 ? 1.f : 0.f;
@@ -610,6 +670,12 @@ __global__ void mds_tc_prep_kernel(const float* __restrict__ theta, int64_t n, i
       ulr[k] = u - __uint_as_float(hu);
       vhr[k] = __uint_as_float(hv);
       vlr[k] = v - __uint_as_float(hv);
+      // f16 split (used only when f16_range holds: no overflow then)
+      const __half u1 = __float2half_rn(u), v1 = __float2half_rn(v);
+      u16r[k] = u1;
+      u16r[KP + k] = __float2half_rn(u - __half2float(u1));
+      v16r[k] = v1;
+      v16r[KP + k] = __float2half_rn(v - __half2float(v1));
     }
   }
 }
@@ -662,7 +728,7 @@ int64_t mds_tc_workspace(int64_t n, int64_t n_loc, int q) {
   TcGrid g = tc_grid(n, n_loc);
   return ws_bytes<unsigned int>(1) + ws_bytes<double>(2 * int64_t(g.grid)) + ws_bytes<double>(int64_t(g.segs) * n_loc) +
          ws_bytes<double>(int64_t(g.segs) * n_loc * q) + ws_bytes<float>(n) + ws_bytes<float>(1) +
-         4 * ws_bytes<float>(n * KP);
+         6 * ws_bytes<float>(n * KP);
 }
 
 // Returns BS_OK with *segs_out / the partial pointers set for mds_fold_kernel.
@@ -679,25 +745,30 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
   float* ul = ws.take<float>(n * KP);
   float* vh = ws.take<float>(n * KP);
   float* vl = ws.take<float>(n * KP);
-  if (!ctr || !parts || !zp || !tp || !norms || !nmax || !uh || !ul || !vh || !vl) {
+  float* u16 = ws.take<float>(n * KP);  // n rows of 64 halves
+  float* v16 = ws.take<float>(n * KP);
+  if (!ctr || !parts || !zp || !tp || !norms || !nmax || !uh || !ul || !vh || !vl || !u16 || !v16) {
     set_error("bs_mds_pass: workspace too small");
     return BS_EWORK;
   }
-  CUtensorMap mY, mKh, mKl, mMh, mMl;
+  CUtensorMap mY, mKh, mKl, mMh, mMl, mK16;
   bool ok = make_map_f32(&mY, Y, uint64_t(n), uint64_t(n_loc), 32, BJ, CU_TENSOR_MAP_SWIZZLE_128B) &&
             make_map_f32(&mKh, uh, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
             make_map_f32(&mKl, ul, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&
+            make_map_f32(&mK16, u16, KP, uint64_t(n), KP, CHI, CU_TENSOR_MAP_SWIZZLE_128B) &&  // 128-byte f16 rows
             make_map_f32(&mMh, uh, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
             make_map_f32(&mMl, ul, KP, uint64_t(n), KP, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok) {
     set_error("bs_mds_pass: cuTensorMapEncodeTiled failed");
     return BS_ECUDA;
   }
-  static int group = -1, mode = 0;
+  static int group = -1, mode = 0, f16_ok = 1;
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = getenv("BS_MDS_TC_GROUP");
     group = (e && atoi(e) > 0) ? atoi(e) : 2;
+    const char* h = getenv("BS_MDS_TC_F16");  // A/B switch: 0 keeps MMA1 in 3xTF32
+    f16_ok = (h && atoi(h) == 0) ? 0 : 1;
 #ifdef BS_DEBUG_MODES  // work-skipping switches only in debug builds (scripts/mds_modes.sh)
     const char* m = getenv("BS_MDS_TC_MODE");
     mode = m ? atoi(m) : 0;
@@ -712,17 +783,17 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
     return BS_ECUDA;
   }
   mds_tc_prep_kernel<<<int(std::min<int64_t>(ceil_div(n, 256), 2048)), 256, 0, st>>>(theta, n, q, uh, ul, vh, vl,
-                                                                                    norms, nmax);
+      reinterpret_cast<__half*>(u16), reinterpret_cast<__half*>(v16), norms, nmax);
   static unsigned long long* trace = nullptr;
   static const bool tracing = getenv("BS_MDS_TC_TRACE") != nullptr;
   if (tracing && !trace) cudaMalloc(&trace, sizeof(unsigned long long) * 5 * TR_CHUNKS);
-  MdsTcArgs args{theta, vh, vl, norms, nmax, n, lo, n_loc, q, perturb, group, mode, trace, g.jblocks, g.segs, g.rows_per_seg,
+  MdsTcArgs args{theta, vh, vl, reinterpret_cast<const uint32_t*>(v16), f16_ok, norms, nmax, n, lo, n_loc, q, perturb, group, mode, trace, g.jblocks, g.segs, g.rows_per_seg,
                  zp, tp, parts, ctr, red};
   switch ((q + 2 + 7) / 8) {
-    case 1: mds_tc_kernel<1><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
-    case 2: mds_tc_kernel<2><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
-    case 3: mds_tc_kernel<3><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
-    default: mds_tc_kernel<4><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, args); break;
+    case 1: mds_tc_kernel<1><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mK16, args); break;
+    case 2: mds_tc_kernel<2><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mK16, args); break;
+    case 3: mds_tc_kernel<3><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mK16, args); break;
+    default: mds_tc_kernel<4><<<g.grid, MT_THREADS, SMEM, st>>>(mY, mKh, mKl, mMh, mMl, mK16, args); break;
   }
   if (tracing && trace) {  // debug: CTA 0 event intervals (ns), averaged over chunks 100..1100
     std::vector<unsigned long long> h(5 * TR_CHUNKS);

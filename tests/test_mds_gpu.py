@@ -86,6 +86,21 @@ def test_mds_f32_tensor_core_pass_matches_oracle(n, q, p):
     assert np.abs(th - oth).max() <= 2e-5 * np.abs(oth).max()
 
 
+@pytest.mark.parametrize("scale", [0.05, 1.0, 30.0, 100.0])
+def test_mds_f32_tensor_core_gram_split_ranges(scale):
+    """MMA1 (the Gram product) runs on an f16 hi/lo split when 1 <= max |theta|^2 < 2^14 and on
+    3xTF32 otherwise (mds_tc.cu f16_range): scales 0.05 and 100 take tf32, 1 and 30 f16.  MDS is
+    scale-equivariant, so every case must match the oracle at the same relative tolerance."""
+    n, q = 516, 20
+    x = orc.rand_fill_common((12, n), 180, np.float32)
+    y = (orc.pairwise_euclidean(x) * scale).astype(np.float32)
+    th0 = (orc.mds_init(y, q, 190) * scale).astype(np.float32)
+    tr, th = bs.run_inproc(2, _run, y, th0, 6)[0]
+    oth, otr = orc.mds_fit(y.astype(np.float64), th0.astype(np.float64), 6)
+    np.testing.assert_allclose(tr, otr, rtol=2e-5)
+    assert np.abs(th - oth).max() <= 2e-5 * np.abs(oth).max()
+
+
 def test_mds_f32_tensor_core_coincident_points():
     """Exactly coincident embedding points give d = 0 exactly on the tcgen05 path too
     (cancellation guard): the reference raises, or perturbs d to 1e-10 (solvers.py:290-296)."""
