@@ -28,6 +28,9 @@ for it in range(iters):
         saved = st.theta.local.clone()
     if saved is not None:
         st.theta.local.copy_(saved)
+    if os.environ.get("MDS_IDLE_AT") and it == int(os.environ["MDS_IDLE_AT"]):
+        import time
+        time.sleep(float(os.environ.get("MDS_IDLE_S", "5")))  # let the device idle
     with _lib.profile(["bs_mds_pass"]) as prof:
         bs.mds_fit(st, 1)
         torch.cuda.synchronize()
