@@ -1,21 +1,39 @@
-"""Key throughput / stall numbers of one-kernel ncu reports: python scripts/ncu_summary.py rep [rep...]."""
-import csv, subprocess, sys
+"""Key metrics and the top stall reasons of every launch in an ncu report (--page raw).
 
-KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-        "smsp__inst_executed.sum", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__sass_inst_executed_op_local_ld.sum",
-        "smsp__sass_inst_executed_op_local_st.sum", "sm__cycles_active.avg"]
-for rep in sys.argv[1:]:
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(out.splitlines()))
-    h, v = r[0], r[2]
-    d = dict(zip(h, v))
-    print(rep)
-    for k in KEYS:
-        print(f"  {k:70s} {d.get(k, '?')}")
-    st = [(float(x), k) for k, x in d.items()
-          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued") and x]
-    tot = sum(a for a, _ in st) or 1
-    for a, k in sorted(st, reverse=True)[:8]:
-        print(f"  {100 * a / tot:5.1f}% {k[len('smsp__pcsamp_warps_issue_stalled_'):]}")
+    python scripts/ncu_summary.py REPORT.ncu-rep
+"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "lts__t_sector_hit_rate.pct",
+        "smsp__sass_inst_executed_op_local_ld.sum", "sm__cycles_elapsed.avg.per_second", "launch__registers_per_thread",
+        "launch__grid_size"]
+
+
+def main():
+    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        print(f"# {r[hdr.index('Kernel Name')][:110]}")
+        for k in KEYS:
+            if k in hdr:
+                print(f"  {k:66s} {r[hdr.index(k)]:>18s} {units[hdr.index(k)]}")
+        st = []
+        for i, k in enumerate(hdr):
+            if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued"):
+                try:
+                    st.append((float(r[i].replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+                except ValueError:
+                    pass
+        tot = sum(a for a, _ in st) or 1.0
+        print("  stalls: " + ", ".join(f"{k} {100 * a / tot:.1f}%" for a, k in sorted(st, reverse=True)[:6]))
+
+
+if __name__ == "__main__":
+    main()
