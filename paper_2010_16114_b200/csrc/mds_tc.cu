@@ -785,7 +785,11 @@ int mds_tc_pass(const float* Y, const float* theta, int64_t n, int64_t lo, int64
   mds_tc_prep_kernel<<<int(std::min<int64_t>(ceil_div(n, 256), 2048)), 256, 0, st>>>(theta, n, q, uh, ul, vh, vl,
       reinterpret_cast<__half*>(u16), reinterpret_cast<__half*>(v16), norms, nmax);
   static unsigned long long* trace = nullptr;
+#ifdef BS_DEBUG_MODES  // the event trace exists only in debug builds (tr_mark)
   static const bool tracing = getenv("BS_MDS_TC_TRACE") != nullptr;
+#else
+  constexpr bool tracing = false;
+#endif
   if (tracing && !trace) cudaMalloc(&trace, sizeof(unsigned long long) * 5 * TR_CHUNKS);
   MdsTcArgs args{theta, vh, vl, reinterpret_cast<const uint32_t*>(v16), f16_ok, norms, nmax, n, lo, n_loc, q, perturb, group, mode, trace, g.jblocks, g.segs, g.rows_per_seg,
                  zp, tp, parts, ctr, red};
