@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
   float* bnew = reinterpret_cast<float*>(bold + (F2_LAG + 1) * F2_W);  // [2][W]
   float* red = bnew + 2 * F2_W;                                        // [2][8][W]
   uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 8 * F2_W);
-  // barriers: afull[AS], aempty[AS], bfull[BS], bempty[BS], pfull[2], pempty[2]
+  // barriers: afull[AS], aempty[AS], bfull[BS], bempty[BS], pfull[2], pempty[2], bnfull[2], bnempty[2]
   auto bar = [&](int i) { return smem_u32(bars + i); };
   constexpr int AF = 0, AE = F2_AS, BF = 2 * F2_AS, BE = 2 * F2_AS + F2_BS, PF = 2 * F2_AS + 2 * F2_BS, PE = PF + 2;
+  constexpr int NF = PE + 2, NE = NF + 2;
   if (tid == 0) {
     for (int i = 0; i < F2_AS; ++i) {
       mbar_init(bar(AF + i), 1);
@@ -114,6 +115,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(PF + i), 1);
       mbar_init(bar(PE + i), 1);
+      mbar_init(bar(NF + i), 1);
+      mbar_init(bar(NE + i), 8);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -155,23 +158,28 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
     }
     return;
   }
-  if (warp == 1) {  // ---------------- B producer: partial block, then L2 -> ring ----------------
-    if (lane == 0) {
-      uint64_t drop;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
-      // B stages do not depend on the partials: the first F2_BS stages of wave u are issued
-      // before waiting for the group's counter, so they land while the fold is pending
-      auto bstage = [&](int u, int q) {
-        const int k = u * F2_QPW + q, s = k % F2_BS;
-        mbar_wait_sleep(bar(BE + s), uint32_t((k / F2_BS) & 1) ^ 1u);
-        const int64_t j0 = c0 + int64_t(u) * F2_W + q * F2_CW;
-        const int nc = int(c1 - j0 <= 0 ? 0 : (c1 - j0 < F2_CW ? c1 - j0 : F2_CW));
-        mbar_expect_tx(bar(BF + s), bytes_col * uint32_t(nc));
-        for (int jj = 0; jj < nc; ++jj)
-          bulk(smem_u32(bring + s * stage_f + jj * R), a.X + (j0 + jj) * m + r0, bytes_col, bar(BF + s), drop);
-      };
-      constexpr int EARLY = F2_BS < F2_QPW ? F2_BS : F2_QPW;
-      for (int u = 0; u < nw; ++u) {
+  if (warp == 1) {  // ---------------- B producer: partial block, L2 -> ring, and the fold ----------------
+    // The warp also folds each wave's group partials into beta_new as soon as they land (lanes
+    // 0..W-1, segment order: identical in every CTA of the group), so the consumers find
+    // beta_new ready when they reach B(u) instead of waiting for one of them to fold.
+    uint64_t drop = 0;
+    if (lane == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(drop));
+    // B stages do not depend on the partials: the first F2_BS stages of wave u are issued
+    // before waiting for the group's counter, so they land while the fold is pending
+    auto bstage = [&](int u, int q) {
+      const int k = u * F2_QPW + q, s = k % F2_BS;
+      mbar_wait_sleep(bar(BE + s), uint32_t((k / F2_BS) & 1) ^ 1u);
+      const int64_t j0 = c0 + int64_t(u) * F2_W + q * F2_CW;
+      const int nc = int(c1 - j0 <= 0 ? 0 : (c1 - j0 < F2_CW ? c1 - j0 : F2_CW));
+      mbar_expect_tx(bar(BF + s), bytes_col * uint32_t(nc));
+      for (int jj = 0; jj < nc; ++jj)
+        bulk(smem_u32(bring + s * stage_f + jj * R), a.X + (j0 + jj) * m + r0, bytes_col, bar(BF + s), drop);
+    };
+    constexpr int EARLY = F2_BS < F2_QPW ? F2_BS : F2_QPW;
+    double l1 = 0.0;
+    for (int u = 0; u < nw; ++u) {
+      const int pb = u & 1;
+      if (lane == 0) {
         if (rows > 0)
           for (int q = 0; q < EARLY; ++q) bstage(u, q);
         const int slot = u % F2_RING;
@@ -188,15 +196,47 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
           }
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        const int pb = u & 1;
         mbar_wait_sleep(bar(PE + pb), uint32_t((u >> 1) & 1) ^ 1u);
         const uint32_t pbytes = uint32_t(S) * F2_W * 8u;
         mbar_expect_tx(bar(PF + pb), pbytes);
         bulk(smem_u32(pbuf + pb * S * F2_W), a.partials + (int64_t(g) * F2_RING + slot) * S * F2_W, pbytes, bar(PF + pb),
              drop);
+      }
+      __syncwarp();
+      // ---- fold wave u: S_lambda(beta + sigma grad) (solvers.py:48-51, 447-449) ----
+      mbar_wait(bar(PF + pb), uint32_t((u >> 1) & 1));
+      mbar_wait(bar(NE + pb), uint32_t((u >> 1) & 1) ^ 1u);  // the consumers are done with bnew[pb] of wave u - 2
+      const int64_t ju = c0 + int64_t(u) * F2_W;
+      if (lane < F2_W) {
+        const double* pp = pbuf + pb * S * F2_W;
+        double gs = 0.0;
+        for (int k = 0; k < S; ++k) gs += pp[k * F2_W + lane];  // segment order: same in every CTA
+        const float gt = float(gs);
+        const float x = float(bold[(u % (F2_LAG + 1)) * F2_W + lane]) + float(a.sigma) * gt;
+        const float mag = fabsf(x) - float(a.lam);
+        const bool live = ju + lane < c1;
+        const float bn = live && mag > 0.f ? copysignf(mag, x) : 0.f;
+        bnew[pb * F2_W + lane] = bn;
+        if (sg == 0 && live) {
+          a.grad[ju + lane] = gt;
+          a.beta[ju + lane] = bn;
+          l1 += fabs(double(bn));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(bar(PE + pb));
+        mbar_arrive(bar(NF + pb));
+        // the wave's later B stages reuse stages that only B(u) itself frees, so they go after
+        // beta_new is published (issuing them first would wait on the consumers' B(u) forever)
         if (rows > 0)
           for (int q = EARLY; q < F2_QPW; ++q) bstage(u, q);
       }
+      __syncwarp();
+    }
+    if (sg == 0) {  // ||beta_new||_1 of the group's columns, fixed order
+      const double t = warp_sum(l1);
+      if (lane == 0) a.l1_parts[g] = t;
     }
     return;
   }
@@ -213,7 +253,6 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
       vr[4 * k + e] = i < rows ? float(a.v[r0 + i]) : 0.f;
       xbr[4 * k + e] = 0.0;
     }
-  double l1 = 0.0;
   float bpre = (ct < F2_W && c0 + ct < c1) ? a.beta[c0 + ct] : 0.f;  // beta of the next wave, loaded a wave early
   for (int w = 0; w < nw + F2_LAG; ++w) {
     if (w < nw) {
@@ -282,30 +321,7 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
     if (u >= 0) {
       // ---- B(u): fold the group's partials, S_lambda, then xb += X[:, wave u] beta_new ----
       const int pb = u & 1;
-      const int64_t ju = c0 + int64_t(u) * F2_W;
-      if (cw == 0) {
-        mbar_wait(bar(PF + pb), uint32_t((u >> 1) & 1));
-        if (ct < F2_W) {
-          const double* pp = pbuf + pb * S * F2_W;
-          double gs = 0.0;
-          for (int k = 0; k < S; ++k) gs += pp[k * F2_W + ct];  // segment order: same in every CTA
-          const float gt = float(gs);
-          // soft_threshold(b + sigma g, lam) = sign(x) max(|x| - lam, 0)   (solvers.py:48-51, 447-449)
-          const float x = float(bold[(u % (F2_LAG + 1)) * F2_W + ct]) + float(a.sigma) * gt;
-          const float mag = fabsf(x) - float(a.lam);
-          const bool live = ju + ct < c1;
-          const float bn = live && mag > 0.f ? copysignf(mag, x) : 0.f;
-          bnew[pb * F2_W + ct] = bn;
-          if (sg == 0 && live) {
-            a.grad[ju + ct] = gt;
-            a.beta[ju + ct] = bn;
-            l1 += fabs(double(bn));
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(PE + pb));
-      }
-      cons_sync();
+      mbar_wait(bar(NF + pb), uint32_t((u >> 1) & 1));  // beta_new of wave u, folded by warp 1
       float bq[F2_W];
 #pragma unroll
       for (int j = 0; j < F2_W; ++j) bq[j] = bnew[pb * F2_W + j];
@@ -338,6 +354,8 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
         __syncwarp();
         if (lane == 0 && rows > 0) mbar_arrive(bar(BE + s));
       }
+      __syncwarp();  // bq is consumed: bnew[pb] may be rewritten (wave u + 2)
+      if (lane == 0) mbar_arrive(bar(NE + pb));
     }
   }
 #pragma unroll
@@ -347,10 +365,6 @@ __global__ void __launch_bounds__(F2_THREADS, 1) cox_fused2_kernel(const F2Args 
       const int i = 4 * ct + 1024 * k + e;
       if (i < rows) a.xb_parts[int64_t(g) * m + r0 + i] = xbr[4 * k + e];
     }
-  if (sg == 0 && cw == 0) {  // ||beta_new||_1 of the group's columns, fixed order
-    const double t = warp_sum(l1);
-    if (lane == 0) a.l1_parts[g] = t;
-  }
 }
 
 // xb_out[i] = sum over groups of xb_parts[g][i] (group order); xb_out[m] = sum of l1_parts
@@ -428,7 +442,7 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
   if (p.R > rmax) return p;
   p.cpg = ceil_div(n_loc, int64_t(p.Gc));
   p.smem = size_t(nst * CW * p.R * 4 + 2 * int64_t(p.S) * W * 8 + (lag_[ci] + 1) * W * 8 + 2 * W * 4 +
-                  2 * 8 * W * 4 + (2 * nst + 4) * 8 + 64);
+                  2 * 8 * W * 4 + (2 * nst + 8) * 8 + 64);
   if (int64_t(p.smem) > int64_t(maxsm) - 1024) return p;
   p.ok = true;
   return p;
