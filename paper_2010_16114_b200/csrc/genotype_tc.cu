@@ -66,13 +66,23 @@ template <int NB>
 constexpr int b_bytes() { return NB * ROWB; }  // 4 / 8 KB per k-block
 constexpr int X_BYTES = BM * BKB;   // 16 KB per k-block
 constexpr int THREADS = 480;
-constexpr int RS = 6, BS = 6, CS = 2;
+// Ring depths.  The pass is bound by bytes in flight and by shared memory, so the packed-tile
+// ring takes whatever the 227 KB leave: 6 stages with the float32 (NB 16) B image, 5 with the
+// float64 one; three A stages let the converters run a k-block further ahead of the MMAs
+// (C5 gradient pass, measured: RS/CS 6/2 10.2 ms, 5/3 9.0, 6/3 8.6, 4/3 10.1).
+template <int NB>
+constexpr int rs_of() { return NB <= 16 ? 6 : 5; }
+constexpr int BS = 6, CS = 3;
 constexpr int ACC = 32;             // TMEM columns per accumulator buffer (>= NB)
 constexpr uint32_t T_SFA = 64, T_SFB = 96;  // scale-factor columns (all 2^0)
 constexpr int TMEM_COLS = 512;
-constexpr int OFF_A = RS * X_BYTES, OFF_B = OFF_A + CS * A_BYTES;
 template <int NB>
-constexpr int smem_bytes() { return OFF_B + BS * b_bytes<NB>() + 1024 + 512; }
+constexpr int off_a() { return rs_of<NB>() * X_BYTES; }
+template <int NB>
+constexpr int off_b() { return off_a<NB>() + CS * A_BYTES; }
+template <int NB>
+constexpr int smem_bytes() { return off_b<NB>() + BS * b_bytes<NB>() + 1024 + 512; }
+static_assert(smem_bytes<16>() <= 232448 && smem_bytes<32>() <= 232448, "227 KB of shared memory per CTA");
 // kind::mxf4 block-scaled descriptor: A, B e2m1 (1), scales ue8m0, N = NB, M = 128
 template <int NB>
 constexpr uint32_t idesc_f4() {
@@ -178,8 +188,9 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* a_base = smem + OFF_A;
-  uint8_t* b_base = smem + OFF_B;
+  constexpr int RS = rs_of<NB>();
+  uint8_t* a_base = smem + off_a<NB>();
+  uint8_t* b_base = smem + off_b<NB>();
   constexpr int B_BYTES = b_bytes<NB>();
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + BS * B_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * RS + 2 * BS + 2 * CS + 4);
