@@ -409,13 +409,13 @@ F2Plan f2_plan(int64_t m, int64_t n_loc) {
     const char* c = getenv("BS_F2_CFG");
     return c ? atoi(c) : 0;
   }();
-  static const int as_[15] = {2, 3, 2, 3, 2, 3, 3, 2, 4, 2, 2, 2, 4, 3, 4},
-                   bs_[15] = {2, 1, 2, 1, 2, 2, 2, 3, 2, 2, 2, 3, 4, 3, 3},
-                   lag_[15] = {2, 2, 3, 3, 4, 3, 2, 2, 2, 1, 2, 1, 2, 2, 2},
-                   w_[15] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 32, 16, 16, 16},
-                   cw_[15] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 2, 2, 2},
-                   kb_[15] = {3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 4, 4, 4};
-  const int ci = cfg >= 0 && cfg < 15 ? cfg : 0;
+  static const int as_[17] = {2, 3, 2, 3, 2, 3, 3, 2, 4, 2, 2, 2, 4, 3, 4, 2, 3},
+                   bs_[17] = {2, 1, 2, 1, 2, 2, 2, 3, 2, 2, 2, 3, 4, 3, 3, 2, 2},
+                   lag_[17] = {1, 2, 3, 3, 4, 3, 2, 2, 2, 1, 2, 1, 2, 2, 2, 2, 1},
+                   w_[17] = {16, 16, 16, 16, 16, 16, 16, 16, 16, 32, 32, 32, 16, 16, 16, 16, 16},
+                   cw_[17] = {4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 4, 2, 2, 2, 4, 4},
+                   kb_[17] = {3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 3, 4, 4, 4, 3, 3};
+  const int ci = cfg >= 0 && cfg < 17 ? cfg : 0;
   const int W = w_[ci], CW = cw_[ci];
   p.cfg = ci;
   const int nst = as_[ci] + bs_[ci];
@@ -491,7 +491,9 @@ int f2_launch(const F2Plan& p, const float* X, int64_t m, int64_t n_loc, const d
     case 12: F2K(4, 4, 2, 16, 2, 4) break;
     case 13: F2K(3, 3, 2, 16, 2, 4) break;
     case 14: F2K(4, 3, 2, 16, 2, 4) break;
-    default: F2K(2, 2, 2, 16, 4, 3) break;
+    case 15: F2K(2, 2, 2, 16, 4, 3) break;  // the default before the fold moved to warp 1
+    case 16: F2K(3, 2, 1, 16, 4, 3) break;
+    default: F2K(2, 2, 1, 16, 4, 3) break;  // lag 1: beta_new is folded off the consumers' path
   }
 #undef F2K
   void* args[] = {&a};
