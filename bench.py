@@ -356,14 +356,32 @@ def _measure(comm, wl, steps, warmup):
     per = prof.elapsed_ms()
     tot = {k: float(np.sum(v)) for k, v in per.items() if v}
     dom = max(tot, key=tot.get)
-    avg_ms = _max_over_ranks(comm, float(np.mean(per[dom])))
+    samples = per[dom]
+    if len(samples) < 3:
+        # CUDA-graph replays (single-GPU NMF) are not individually visible to the per-call
+        # hook, which then holds the one eager launch of the call: time a few more launches
+        # of the same entry point eagerly (same data and state) instead of trusting one sample
+        from paper_2010_16114_b200 import solvers as _solvers
+
+        saved = _solvers._GRAPHS
+        _solvers._GRAPHS = False
+        try:
+            with _lib.profile(kernels) as prof2:
+                step(5)
+            torch.cuda.synchronize()
+            extra = prof2.elapsed_ms().get(dom, [])
+        finally:
+            _solvers._GRAPHS = saved
+        if extra:
+            samples = list(extra)
+    avg_ms = _max_over_ranks(comm, float(np.mean(samples)))
     bytes_launch = _bytes_per_launch(dom, wl, comm, data)
     peak, peak_kind = _peaks()
     achieved = bytes_launch / (avg_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "unit": "GB/s",
             "frac": achieved / peak, "traffic": _traffic(wl, dom), "bytes_per_launch": bytes_launch,
-            "avg_launch_ms": avg_ms, "launches_timed": len(per[dom]),
+            "avg_launch_ms": avg_ms, "launches_timed": len(samples),
             # one launch of the dominant entry point per iteration (replayed CUDA-graph iterations
             # are not individually timed, so the share is per-launch time over per-step time)
             "share_of_step": avg_ms / (ms / steps)}
