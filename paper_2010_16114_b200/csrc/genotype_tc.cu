@@ -66,13 +66,16 @@ template <int NB>
 constexpr int b_bytes() { return NB * ROWB; }  // 4 / 8 KB per k-block
 constexpr int X_BYTES = BM * BKB;   // 16 KB per k-block
 constexpr int THREADS = 480;
-// Ring depths.  The pass is bound by bytes in flight and by shared memory, so the packed-tile
-// ring takes whatever the 227 KB leave: 6 stages with the float32 (NB 16) B image, 5 with the
-// float64 one; three A stages let the converters run a k-block further ahead of the MMAs
-// (C5 gradient pass, measured: RS/CS 6/2 10.2 ms, 5/3 9.0, 6/3 8.6, 4/3 10.1).
+// Ring depths.  The pass is bound by bytes in flight and by shared memory: 6 packed-tile stages
+// and three A stages (the converters run a k-block further ahead of the MMAs), with the B-image
+// ring shrunk to 3 stages for the 8 KB float64 image so both fit the 227 KB (C5 gradient pass,
+// measured: RS/CS 6/2 10.2 ms, 5/3 9.0, 6/3 8.6, 4/3 10.1; float64 RS 5 -> 6 with 3 B stages -3%).
 template <int NB>
-constexpr int rs_of() { return NB <= 16 ? 6 : 5; }
-constexpr int BS = 6, CS = 3;
+constexpr int rs_of() { return 6; }
+// B-image stages: 6 of 4 KB (float32) or 3 of 8 KB (float64, so the packed ring keeps 6 stages)
+template <int NB>
+constexpr int bs_of() { return NB <= 16 ? 6 : 3; }
+constexpr int CS = 3;
 constexpr int ACC = 32;             // TMEM columns per accumulator buffer (>= NB)
 constexpr uint32_t T_SFA = 64, T_SFB = 96;  // scale-factor columns (all 2^0)
 constexpr int TMEM_COLS = 512;
@@ -81,7 +84,7 @@ constexpr int off_a() { return rs_of<NB>() * X_BYTES; }
 template <int NB>
 constexpr int off_b() { return off_a<NB>() + CS * A_BYTES; }
 template <int NB>
-constexpr int smem_bytes() { return off_b<NB>() + BS * b_bytes<NB>() + 1024 + 512; }
+constexpr int smem_bytes() { return off_b<NB>() + bs_of<NB>() * b_bytes<NB>() + 1024 + 512; }
 static_assert(smem_bytes<16>() <= 232448 && smem_bytes<32>() <= 232448, "227 KB of shared memory per CTA");
 // kind::mxf4 block-scaled descriptor: A, B e2m1 (1), scales ue8m0, N = NB, M = 128
 template <int NB>
@@ -188,7 +191,7 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
   if (flags && (*flags & BS_FLAG_NONFINITE)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int RS = rs_of<NB>();
+  constexpr int RS = rs_of<NB>(), BS = bs_of<NB>();
   uint8_t* a_base = smem + off_a<NB>();
   uint8_t* b_base = smem + off_b<NB>();
   constexpr int B_BYTES = b_bytes<NB>();
@@ -265,7 +268,8 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
     // g % CS and its B stage g % BS.  Unrolling six k-blocks at a time makes both stages
     // compile-time constants: every MMA operand is then a loop-invariant base plus an
     // immediate, so the single issuing warp spends a few instructions per MMA.
-    static_assert(BS == 6 && (CS == 2 || CS == 3), "the unrolled issue loop assumes 6 B stages, 2 or 3 A stages");
+    constexpr int UNR = BS;  // issue-loop unroll covering whole B and A rings
+    static_assert(UNR % BS == 0 && UNR % CS == 0, "the unrolled issue loop covers whole B and A rings");
     static_assert(TMEM_COLS == 512, "a whole-TMEM allocation starts at address 0");
     if (tmem != 0u) __trap();
     const uint32_t my_tiles = uint32_t((tiles - int(blockIdx.x) + int(gridDim.x) - 1) / int(gridDim.x));
@@ -276,10 +280,10 @@ gradtc_kernel(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict
     const uint32_t blo0 = uint32_t(b_desc0), bhi = uint32_t(b_desc0 >> 32);
     int kb = 0;
     uint32_t gi = 0;
-    for (uint32_t g0 = 0; g0 < total; g0 += 6) {
-      const uint32_t bph = (g0 / 6) & 1u;
+    for (uint32_t g0 = 0; g0 < total; g0 += UNR) {
+      const uint32_t bph = (g0 / UNR) & 1u;
 #pragma unroll
-      for (int u = 0; u < 6; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         if (g0 + uint32_t(u) >= total) break;
         const int cs = u % CS;
         const uint32_t cph = (g0 / CS + uint32_t(u / CS)) & 1u;
