@@ -493,6 +493,19 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         ++gi;
         fold_pending = false;
       };
+      // D1 of the next chunk is waited for and its TMEM load started at the end of the previous
+      // chunk; the load's completion is awaited only after the Y loads of the chunk are issued
+      uint32_t g[16];
+      auto d1_issue = [&](uint32_t c) {
+        mbar_wait(d1_full(c & 1), (c >> 1) & 1);
+        tc_fence_after();
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(g[0]), "=r"(g[1]), "=r"(g[2]), "=r"(g[3]), "=r"(g[4]), "=r"(g[5]), "=r"(g[6]), "=r"(g[7]),
+              "=r"(g[8]), "=r"(g[9]), "=r"(g[10]), "=r"(g[11]), "=r"(g[12]), "=r"(g[13]), "=r"(g[14]), "=r"(g[15])
+            : "r"(tmem + lane_addr + T_D1 + (c & 1) * CHI + 16 * sub));
+      };
+      if (nch > 0) d1_issue(cc);
       for (int t = 0; t < nch; ++t, ++cc) {
         const int s = int(cc % NY);
         const uint32_t b = cc & 1;
@@ -517,11 +530,12 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
           y[4 * c] = __uint_as_float(yv[c].x); y[4 * c + 1] = __uint_as_float(yv[c].y);
           y[4 * c + 2] = __uint_as_float(yv[c].z); y[4 * c + 3] = __uint_as_float(yv[c].w);
         }
-        mbar_wait(d1_full(b), (cc >> 1) & 1);
         if (warp == 2 && lane == 0) tr_mark(a.trace, 3, cc);  // D1 ready
-        tc_fence_after();
-        uint32_t g[16];
-        tmem_ld16_u(tmem + lane_addr + T_D1 + b * CHI + 16 * sub, g);
+        asm volatile("tcgen05.wait::ld.sync.aligned;"  // tied to g: no use of g moves above it
+                     : "+r"(g[0]), "+r"(g[1]), "+r"(g[2]), "+r"(g[3]), "+r"(g[4]), "+r"(g[5]), "+r"(g[6]), "+r"(g[7]),
+                       "+r"(g[8]), "+r"(g[9]), "+r"(g[10]), "+r"(g[11]), "+r"(g[12]), "+r"(g[13]), "+r"(g[14]), "+r"(g[15])
+                     :
+                     : "memory");
         tc_fence_before();
         mbar_arrive(d1_empty(b));
         uint32_t wz[16], wl[16];
@@ -586,6 +600,7 @@ mds_tc_kernel(const __grid_constant__ CUtensorMap tmY, const __grid_constant__ C
         tc_fence_before();
         mbar_arrive(a2_full(b));
         if (warp == 2 && lane == 0) tr_mark(a.trace, 4, cc);  // A2 written (warp 2)
+        if (t + 1 < nch) d1_issue(cc + 1);
         if (fold_pending) fold();
         if (gpos == a.G - 1 || t == nch - 1) fold_pending = true;
         gpos = gpos == a.G - 1 ? 0 : gpos + 1;
